@@ -1,0 +1,308 @@
+/*
+ * embcomm_gpu.h — C-ABI of libembcomm_gpu.so, the B200-native (sm_100a)
+ * implementation of the embedding-lookup hot path of arXiv 2411.01611 behind
+ * the reference library's core/ API surface (/root/reference/proj/core).
+ *
+ * The reference is a C++20 static library with no FFI.  Each
+ * entry point below names the reference interface it replaces
+ * (file:line into /root/reference/proj).  Reference spans become
+ * (pointer, length); value results become caller-owned POD structs; C++
+ * exceptions become status codes.  No torch or C++ types cross this ABI.
+ *
+ * Conventions
+ *   - Every function returns an ec_status.  EC_EINVAL (=2) is the reference's
+ *     ValidationError, EC_EINVARIANT (=3) its InvariantError
+ *     (core/include/embcomm/error.hpp:10-19; CLI exit codes
+ *     tools/src/main.cpp:220-229).  ec_last_error() returns the thread-local
+ *     message of the last failure (messages name the offending id/size as the
+ *     reference's do, e.g. core/src/distribution.cpp:22-24).
+ *   - `stream` arguments are cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  Device pointers are marked _dev, host pointers _host.
+ *   - Handles are not thread-safe; use one handle per host thread / GPU.
+ *   - There is no CPU fallback: GPU entry points fail with EC_ECUDA when no
+ *     device is present.
+ */
+#ifndef EMBCOMM_GPU_H_
+#define EMBCOMM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EC_OK = 0,
+  EC_EINVAL = 2,      /* embcomm::ValidationError  (error.hpp:10-13) */
+  EC_EINVARIANT = 3,  /* embcomm::InvariantError   (error.hpp:16-19) */
+  EC_ECUDA = 4,       /* CUDA runtime / launch failure, or no GPU */
+  EC_ENCCL = 5,       /* NCCL failure */
+  EC_ENOMEM = 6       /* device / pinned-host allocation failure */
+} ec_status;
+
+const char* ec_last_error(void);
+const char* ec_version(void);
+/* kCostUnitsNote, core/include/embcomm/cost_model.hpp:13-14 */
+const char* ec_cost_units_note(void);
+/* kRngAlgorithm, core/include/embcomm/rng.hpp:41 */
+const char* ec_rng_algorithm(void);
+
+/* ------------------------------------------------------------------ RNG */
+/* substream_seed, core/include/embcomm/rng.hpp:33-38 */
+uint64_t ec_substream_seed(uint64_t master, uint64_t index);
+
+/* ---------------------------------------------------------- distributions
+ * EmbeddingDistribution (core/include/embcomm/distribution.hpp:19-49) and
+ * DistributionSpec materialisation (distribution_spec.hpp:36-67).  Host
+ * objects; probabilities and rank maps are computed in the reference's exact
+ * arithmetic order so downstream fp64 results are bit-identical. */
+typedef struct ec_dist_s* ec_dist;
+enum { EC_ZIPF = 0, EC_EXPONENTIAL = 1, EC_HALF_NORMAL = 2, EC_EMPIRICAL = 3 };
+
+int ec_dist_from_probabilities(const double* probs_host, uint64_t n, ec_dist* out); /* distribution.cpp:13-55 */
+int ec_dist_uniform(uint64_t n, ec_dist* out);                                      /* distribution.cpp:57-60 */
+int ec_dist_materialize(int kind, uint64_t size, double shape, ec_dist* out);       /* distribution_spec.cpp:195-203 */
+int ec_dist_materialize_extended(int kind, uint64_t size, double shape, int64_t factor,
+                                 ec_dist* out);                                     /* distribution_spec.cpp:215-226 */
+int ec_default_shape(int kind, double* out);                                        /* distribution_spec.cpp:85-93 */
+void ec_dist_destroy(ec_dist d);
+uint64_t ec_dist_size(ec_dist d);
+int ec_dist_prob(ec_dist d, uint32_t id, double* out);                              /* distribution.cpp:62-68 */
+int ec_dist_prob_at_rank(ec_dist d, uint64_t rank, double* out);                    /* :70-75 */
+int ec_dist_id_at_rank(ec_dist d, uint64_t rank, uint32_t* out);                    /* :77-82 */
+int ec_dist_rank_of(ec_dist d, uint32_t id, uint64_t* out);                         /* :84-90 */
+int ec_dist_top_ids(ec_dist d, uint64_t k, uint32_t* out_host);                     /* :92-98 */
+int ec_dist_mass_of(ec_dist d, const uint32_t* ids_host, uint64_t n, double* out);  /* :100-104 */
+/* ranked probabilities (non-increasing) and rank->id map; either may be NULL */
+int ec_dist_export(ec_dist d, double* ranked_probs_host, uint32_t* rank_to_id_host);
+
+/* ------------------------------------------------------------ cost model
+ * core/include/embcomm/cost_model.hpp:17-64.  Host fp64, reference
+ * summation order (a GPU reduction would reorder the sum). */
+typedef struct {
+  int64_t num_samples;        /* Q */
+  int64_t batch_size;         /* b */
+  int64_t lookups_per_sample; /* d */
+} ec_workload;                /* WorkloadSpec, cost_model.hpp:17-25 (validated: Q>=b>=1, d>=1) */
+
+typedef struct {
+  double index_cost;
+  double embedding_cost;
+  double total;
+} ec_cost; /* CostBreakdown, cost_model.hpp:27-32 */
+
+int ec_workload_validate(const ec_workload* w);                                     /* cost_model.cpp:23-34 */
+int ec_batch_presence_prob(double p, int64_t b, double* out);                       /* cost_model.cpp:36-46 */
+int ec_expected_unique_per_batch(ec_dist d, int64_t b, double* out);                /* cost_model.cpp:61-63 */
+int ec_expected_unique_from_rank(ec_dist d, int64_t b, uint64_t first_rank, double* out); /* :48-59 */
+int ec_coalesced_batch_cost(ec_dist d, int64_t b, ec_cost* out);                    /* :65-71 */
+int ec_baseline_epoch_cost(const ec_workload* w, double* out);                      /* :73-76 */
+int ec_coalesced_epoch_cost(ec_dist d, const ec_workload* w, ec_cost* out);         /* :78-86 */
+int ec_cached_epoch_cost(ec_dist d, const ec_workload* w, const uint32_t* cache_ids_host,
+                         uint64_t k, ec_cost* out);                                 /* :88-111 */
+
+/* ------------------------------------------------- cache placement policy
+ * core/include/embcomm/cache_planner.hpp:16-81 (host). */
+typedef struct {
+  int64_t total_params;                 /* M */
+  int64_t activation_params_per_sample; /* a */
+  int64_t embedding_params;             /* d_emb */
+  double memory_efficiency;             /* (0, 1] */
+} ec_device_model;                      /* DeviceModel, cache_planner.hpp:16-24 */
+
+typedef struct {
+  uint32_t candidate_id;
+  double presence_gain;
+  double threshold;
+  double delta_comm;
+  int32_t recommend;
+} ec_marginal; /* MarginalReport, cache_planner.hpp:34-44 */
+
+typedef struct {
+  uint64_t cache_size;
+  int64_t batch_size;
+  ec_cost expected_epoch_cost;
+  int32_t feasible;
+  int32_t used_scan_fallback;
+} ec_cache_plan; /* CachePlan, cache_planner.hpp:55-62; cached ids returned separately */
+
+int ec_device_model_validate(const ec_device_model* m);                             /* cache_planner.cpp:90-112 */
+/* *out = -1 when no batch fits (std::nullopt) */
+int ec_max_batch_size(const ec_device_model* m, int64_t cache_size, int64_t* out);  /* :114-136 */
+int ec_delta_comm(ec_dist d, const ec_device_model* m, int64_t num_samples,
+                  int64_t current_cache_size, ec_marginal* out);                    /* :138-186 */
+/* cached_ids_host (capacity >= dist size) may be NULL */
+int ec_optimal_cache_size_scan(ec_dist d, const ec_device_model* m, const ec_workload* w,
+                               ec_cache_plan* out, uint32_t* cached_ids_host);      /* :188-204 */
+int ec_optimal_cache_size_search(ec_dist d, const ec_device_model* m, const ec_workload* w,
+                                 ec_cache_plan* out, uint32_t* cached_ids_host);    /* :206-289 */
+int ec_memory_io_proxy(ec_dist d, const ec_workload* w, const uint32_t* cache_ids_host,
+                       uint64_t k, double* out);                                    /* :291-294 */
+/* Multi-table placement under one row budget: global top-`budget_rows` by
+ * access probability across tables (ties: lower table, then the
+ * distribution's own rank order).  Per table the chosen set is always a
+ * probability-ranked prefix, i.e. dist.top_ids(k_t) (cache_planner.cpp:71-79).
+ * Presence 1-(1-p)^n is monotone in p, so for equal per-table batch sizes
+ * this maximises expected cached distinct rows. */
+int ec_place_topk_global(const ec_dist* dists, uint32_t num_tables, uint64_t budget_rows,
+                         uint64_t* k_per_table_host);
+
+/* --------------------------------------------------------- GPU sampler (K0)
+ * DiscreteSampler (core/src/simulator.cpp:110-130) on the device: the CDF is
+ * built on the host in the reference's Kahan order, uploaded once; draws are
+ * the closed form  u_m = (mix64(seed + (m+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53
+ * followed by an fp64 upper_bound — bit-identical ids. */
+typedef struct ec_sampler_s* ec_sampler;
+int ec_sampler_create(ec_dist d, int device, ec_sampler* out);
+void ec_sampler_destroy(ec_sampler s);
+/* ids_dev[i] = draw #(start+i) of SplitMix64(seed) */
+int ec_sample_stream(ec_sampler s, uint64_t seed, uint64_t start, uint64_t count,
+                     uint32_t* ids_dev, void* stream);
+/* sample_batch (simulator.cpp:132-143): b*d ids sample-major into a HOST
+ * buffer; *rng_state is the SplitMix64 state, advanced by b*d draws exactly
+ * as the reference's generator would be. */
+int ec_sample_batch(ec_sampler s, int64_t b, int64_t d, uint64_t* rng_state,
+                    uint32_t* out_host);
+
+/* -------------------------------------------- GPU Monte Carlo simulator
+ * SimResult (core/include/embcomm/simulator.hpp:34-48).  Distinct and
+ * non-cached distinct counts per (batch, feature column) are computed on the
+ * device (K0 + K1 count mode); mean / std-error / cost are folded on the host
+ * in the reference's fixed order, so results are bit-identical. */
+typedef struct {
+  double unique_mean, unique_std_error;       /* unique_per_batch */
+  double non_cached_mean, non_cached_std_error; /* non_cached_unique */
+  ec_cost measured_epoch_cost;
+  double hot_batch_fraction;
+} ec_sim_result;
+
+int ec_measure_unique(ec_sampler s, int64_t batch_size, int64_t trials, uint64_t seed,
+                      ec_sim_result* out);                                          /* simulator.cpp:145-167 */
+int ec_simulate_epoch(ec_sampler s, const ec_workload* w, const uint32_t* cache_ids_host,
+                      uint64_t k, int64_t epochs, uint64_t seed, ec_sim_result* out); /* :169-220 */
+/* trace replay through the hot/normal schedule (simulator.cpp:222-273) */
+int ec_simulate_trace(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
+                      uint64_t vocab, int64_t batch_size, const uint32_t* cache_ids_host,
+                      uint64_t k, int device, ec_sim_result* out);
+
+/* ----------------------------------------------- traces on the GPU (§8f)
+ * classify_samples (core/src/trace.cpp:185-204): hot_host[s] = 1 iff every
+ * id of sample s is cached.  build_schedule (trace.cpp:206-240) without
+ * shuffle: order_host = hot samples then normal samples, stable;
+ * *num_hot = number of hot samples. */
+int ec_classify_samples(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
+                        uint64_t vocab, const uint32_t* cache_ids_host, uint64_t k, int device,
+                        uint8_t* hot_host);
+int ec_schedule_order(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
+                      uint64_t vocab, const uint32_t* cache_ids_host, uint64_t k, int device,
+                      uint32_t* order_host, uint64_t* num_hot);
+
+/* --------------------------------------------------------- lookup engine
+ * No reference counterpart (SURVEY.md §2 "★ new"): row-wise sharded fp32
+ * tables, a replicated HBM hot-row cache, per-table batch dedup (K1), hit/miss
+ * partition (K2), 128-bit row gather from HBM and from pinned host memory on a
+ * side stream (K3), unique-only exchange between shards (K4), pooled
+ * EmbeddingBag sum through inverse indices (K5) and dedup-then-scatter-add SGD
+ * backward into the owning shard and the cache (K6).
+ *
+ * Dedup domain (SURVEY §7 hard part 1, mapping M1): all lookups of one table
+ * in one batch.  Unique ids are kept in FIRST-OCCURRENCE order — the order in
+ * which the reference's UniqueCounter first marks them (simulator.cpp:96-98);
+ * inverse[i] is the position of lookup i's id in that list.  The number of
+ * uniques and of non-cached uniques per table is exactly what
+ * simulate_epoch(Trace{d=1}, n, C) / count_batch_unique count. */
+typedef struct ec_tables_s* ec_tables;
+
+enum { EC_STORAGE_HBM = 0, EC_STORAGE_HOST = 1 };
+
+typedef struct {
+  uint32_t num_tables;
+  uint32_t dim;                  /* D, fp32 elements per row; multiple of 4 */
+  const uint64_t* rows_host;     /* E_t per table, each in [1, 2^32-1] */
+  int32_t storage;               /* cold tier: EC_STORAGE_HBM or EC_STORAGE_HOST (pinned) */
+  int32_t rank, world;           /* row sharding: owner(id) = id % world, local row id / world */
+  uint64_t max_lookups_per_table;/* workspace sizing: n_t of any batch */
+  uint32_t max_batch_size;       /* workspace sizing: bags per table */
+  int32_t device;                /* CUDA ordinal */
+} ec_tables_config;
+
+int ec_tables_create(const ec_tables_config* cfg, ec_tables* out);
+void ec_tables_destroy(ec_tables t);
+/* bytes of device / pinned-host memory held */
+int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
+/* Deterministic synthetic weights: row (t, id) element c =
+ *   scale * (2 * ((mix64(seed + 0x9E3779B97F4A7C15 * ((t << 40) ^ (id * D + c))) >> 40) * 2^-24) - 1)
+ * in fp32; every rank can evaluate any row, so shards and replicated cache
+ * rows initialise consistently without communication. */
+int ec_tables_init_synthetic(ec_tables t, uint64_t seed, float scale, void* stream);
+/* Cache placement: cached_ids[t] lists the k_t ids of table t held in the
+ * replicated HBM cache (distinct, in range; typically dist.top_ids(k_t)).
+ * Replaces any previous placement; cached rows are (re)initialised from the
+ * current authoritative values when world == 1, and from the synthetic init
+ * (seed/scale of the last ec_tables_init_synthetic) otherwise. */
+int ec_tables_place_cache(ec_tables t, const uint32_t* const* cached_ids_host,
+                          const uint64_t* k_host);
+/* Authoritative row values (cache copy for cached ids, else the shard) —
+ * host copies for tests/checkpointing.  Ids must be owned by this rank unless
+ * cached. */
+int ec_tables_read_rows(ec_tables t, uint32_t table, const uint32_t* ids_host, uint64_t n,
+                        float* out_host);
+int ec_tables_write_rows(ec_tables t, uint32_t table, const uint32_t* ids_host, uint64_t n,
+                         const float* rows_host);
+
+/* One batch: lookups of table t are indices_dev[table_offsets_host[t] ..
+ * table_offsets_host[t+1]); each table has batch_size bags.  Bags are either
+ * fixed-size (bag_offsets_dev == NULL: bag s of table t is lookups
+ * [s*P, (s+1)*P) of that table, P = pooling) or CSR: bag_offsets_dev has
+ * num_tables*batch_size+1 entries, table-major, in global lookup positions. */
+typedef struct {
+  const uint32_t* indices_dev;
+  const int64_t* table_offsets_host;
+  const int64_t* bag_offsets_dev;
+  uint32_t batch_size;
+  uint32_t pooling;
+} ec_batch;
+
+/* Forward: out_dev[s, t*D + c] = sum over bag (t, s) of row values.  Runs
+ * K1..K5 on `stream` (host misses on an internal side stream joined by an
+ * event).  No host synchronisation unless world > 1. */
+int ec_lookup_fwd(ec_tables t, const ec_batch* batch, float* out_dev, void* stream);
+/* Backward of the last forward: grad_dev laid out like out_dev; applies
+ * w <- w - lr * (sum of grads of every lookup of the row) to the cache copy
+ * of cached rows and to the owning shard of the others (K6). */
+int ec_lookup_bwd(ec_tables t, const float* grad_dev, float lr, void* stream);
+
+typedef struct {
+  uint64_t lookups;        /* sum_t n_t (with duplicates) */
+  uint64_t unique_rows;    /* sum_t U_t */
+  uint64_t hit_rows;       /* sum_t |U_t ∩ C_t| */
+  uint64_t miss_rows;      /* sum_t |U_t \ C_t| = model rows (reference embedding units) */
+  uint64_t index_units;    /* sum_t n_t (M1: one index unit per lookup) */
+  uint64_t model_bytes;    /* miss_rows*D*4 + index_units*4 */
+  uint64_t wire_rows;      /* misses owned by another rank (fetched over the exchange) */
+  uint64_t wire_bytes;     /* bytes actually sent + received by this rank's exchange */
+  uint64_t hot_tables;     /* tables whose batch touched no uncached row */
+} ec_batch_stats;
+/* Synchronises `stream`; per-table arrays (length num_tables) may be NULL. */
+int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* unique_per_table_host,
+                    int64_t* miss_per_table_host);
+/* Parity exports of the last forward (synchronise): unique ids of table t in
+ * first-occurrence order, inverse (positions into that list), per-unique hit
+ * flag, and the gathered unique rows. */
+int ec_export_unique(ec_tables t, uint32_t table, uint32_t* unique_host, uint64_t cap,
+                     uint64_t* count);
+int ec_export_inverse(ec_tables t, uint32_t table, uint32_t* inverse_host);
+int ec_export_hit(ec_tables t, uint32_t table, uint8_t* hit_host);
+int ec_export_rows(ec_tables t, uint32_t table, float* rows_host);
+
+/* ------------------------------------------------- multi-GPU (K4, NCCL)
+ * One process per GPU.  Rank 0 calls ec_comm_unique_id and distributes the
+ * 128 bytes (e.g. torch.distributed broadcast); every rank then attaches. */
+int ec_comm_unique_id(uint8_t* id128_host);
+int ec_tables_attach_comm(ec_tables t, const uint8_t* id128_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMBCOMM_GPU_H_ */

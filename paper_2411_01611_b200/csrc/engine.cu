@@ -1,0 +1,1015 @@
+// Lookup engine: row-sharded fp32 tables, replicated HBM hot-row cache, and
+// the per-batch forward/backward pipeline (K1..K6).
+//
+//   forward  K1 dedup      k_insert -> k_count -> k_scan -> k_emit -> k_inverse
+//            K2 partition  k_partition  (hit/miss per unique, miss queue, hash reset)
+//            K3 gather     k_gather (HBM: cache hits and local-HBM misses)
+//                          k_gather_host (pinned host misses, side stream)
+//            K4 exchange   exchange.cu (world > 1)
+//            K5 pool       k_pool (EmbeddingBag sum through inverse indices)
+//   backward K6            k_zero -> k_scatter (grad -> unique rows) -> k_apply (SGD)
+//
+// Reference anchors: the dedup reproduces count_batch_unique's distinct and
+// non-cached distinct counts (core/src/simulator.cpp:85-106) per table batch
+// (mapping M1), with the unique ids kept in the order the
+// reference's UniqueCounter first marks them (simulator.cpp:96-98); the cache
+// is the probability-ranked prefix the planner selects
+// (core/src/cache_planner.cpp:71-79) and a lookup misses iff
+// !cached[id] (simulator.cpp:99).  Gather, pool, exchange and backward have no
+// reference counterpart (SURVEY §2 "★ new").
+//
+// HBM layout (device `dev`, rank r of `world`):
+//   store  : per table t, local shard rows (ids with id % world == r, local
+//            row id / world), D fp32 each, tables back to back — HBM or
+//            pinned host (mapped, read by the GPU over PCIe/C2C)
+//   cache  : K_total rows x D fp32 (replicated top-k rows of every table)
+//   remap  : per table, int32[E_t]: global cache row or -1
+//   hash   : per table, uint64[cap_t] open-addressing set, (id << 32 | value);
+//            cap_t = pow2 >= 2*min(max lookups, E_t); self-cleaning per batch
+//   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
+//            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.hpp"
+#include "device_util.cuh"
+#include "engine.hpp"
+
+namespace ec {
+
+// ----------------------------------------------------------- runtime bits
+int sm_count(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cached[device]) {
+    int n = 0;
+    EC_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    cached[device] = n;
+  }
+  return cached[device];
+}
+
+void use_device(int device) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw Error(EC_ECUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                              "); libembcomm_gpu has no CPU fallback");
+  if (device < 0 || device >= n) invalid("CUDA device " + std::to_string(device) + " out of range");
+  EC_CUDA(cudaSetDevice(device));
+}
+
+// ------------------------------------------------------------------ K1
+constexpr int kThreads = 256;
+constexpr int kItems = 4;
+constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
+
+__device__ __forceinline__ uint32_t hash_insert(unsigned long long* tab, uint32_t mask, uint32_t shift,
+                                                uint32_t id, uint32_t lpos) {
+  const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
+  uint32_t h = hash_slot(id, shift);
+  for (;;) {
+    unsigned long long cur = __ldcg(tab + h);
+    if (cur == kEmptySlot) {
+      cur = atomicCAS(tab + h, kEmptySlot, mine);
+      if (cur == kEmptySlot) return h;
+    }
+    if (static_cast<uint32_t>(cur >> 32) == id) {
+      // same key: keep the smallest position (high words equal -> packed min)
+      if (static_cast<uint32_t>(cur) > lpos) atomicMin(tab + h, mine);
+      return h;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// Insert every lookup of a tile; warp lanes holding the same id collapse to
+// their lowest lane (= smallest position) before touching the table.
+__global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                     const uint32_t* __restrict__ indices,
+                                                     uint32_t* __restrict__ slot_of, int* __restrict__ err) {
+  const Tile tile = tiles[blockIdx.x];
+  const TableDev t = td[tile.table];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    bool live = off < tile.count;
+    const int64_t p = tile.start + off;
+    uint32_t id = live ? __ldcs(indices + p) : kEmptyKey;
+    if (live && id >= t.rows) {
+      atomicExch(err, 1);
+      live = false;
+      id = kEmptyKey;
+    }
+    const unsigned peers = __match_any_sync(kFull, id);
+    const int leader = __ffs(peers) - 1;
+    uint32_t h = 0;
+    if (live && leader == lane_id()) h = hash_insert(t.hash, t.mask, t.shift, id, static_cast<uint32_t>(p - t.base));
+    h = __shfl_sync(kFull, h, leader);
+    if (live) slot_of[p] = h;
+  }
+}
+
+// First-occurrence flags per tile: lookup p is first iff the slot's packed
+// minimum position is p.
+__device__ __forceinline__ bool is_first(const TableDev& t, const uint32_t* slot_of, int64_t p, uint32_t* h) {
+  *h = slot_of[p];
+  return static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
+}
+
+__global__ void __launch_bounds__(kThreads) k_count(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                    const uint32_t* __restrict__ slot_of, int* __restrict__ tile_cnt) {
+  const Tile tile = tiles[blockIdx.x];
+  const TableDev t = td[tile.table];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    uint32_t h;
+    if (off < tile.count && is_first(t, slot_of, tile.start + off, &h)) ++c;
+  }
+  __shared__ int w[kThreads / 32];
+  const int s = __reduce_add_sync(kFull, c);
+  if (lane_id() == 0) w[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int k = 0; k < kThreads / 32; ++k) tot += w[k];
+    tile_cnt[blockIdx.x] = tot;
+  }
+}
+
+// Single block: exclusive scan of tile counts in (table, position) order ->
+// global unique index base of each tile; per-table U and ubase; resets the
+// per-batch miss counters.
+__global__ void __launch_bounds__(1024) k_scan(int* __restrict__ tile_cnt, int ntiles, const int* __restrict__ first_tile,
+                                               int T, int* __restrict__ ctr) {
+  __shared__ int sw[32];
+  int carry = 0;
+  for (int base = 0; base < ntiles; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < ntiles ? tile_cnt[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan<1024>(v, sw, &tot);
+    if (i < ntiles) tile_cnt[i] = carry + ex;  // in place: now tile bases
+    carry += tot;
+  }
+  __syncthreads();
+  Counters c = counters(ctr, T);
+  for (int t = threadIdx.x; t <= T; t += blockDim.x) {
+    const int ft = first_tile[t];
+    c.ubase[t] = ft < ntiles ? tile_cnt[ft] : carry;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    c.U[t] = c.ubase[t + 1] - c.ubase[t];
+    c.M[t] = 0;
+  }
+  if (threadIdx.x == 0) *c.miss_total = 0;
+}
+
+// Emit unique ids in first-occurrence order and tag each slot with the
+// unique's global index (low word | kRankTag, so no later flag test can
+// mistake it for a position).
+__global__ void __launch_bounds__(kThreads) k_emit(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                   const uint32_t* __restrict__ indices,
+                                                   const uint32_t* __restrict__ slot_of, const int* __restrict__ tile_base,
+                                                   uint32_t* __restrict__ uniq, uint32_t* __restrict__ uslot,
+                                                   uint16_t* __restrict__ utab) {
+  __shared__ int sw[kThreads / 32];
+  const Tile tile = tiles[blockIdx.x];
+  const TableDev t = td[tile.table];
+  int run = tile_base[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    uint32_t h = 0;
+    const bool first = off < tile.count && is_first(t, slot_of, tile.start + off, &h);
+    int tot;
+    const int ex = block_exclusive_scan<kThreads>(first ? 1 : 0, sw, &tot);
+    if (first) {
+      const uint32_t g = static_cast<uint32_t>(run + ex);
+      const uint32_t id = indices[tile.start + off];
+      uniq[g] = id;
+      uslot[g] = h;
+      utab[g] = static_cast<uint16_t>(tile.table);
+      t.hash[h] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
+    }
+    run += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_inverse(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                      const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ inv) {
+  const Tile tile = tiles[blockIdx.x];
+  const TableDev t = td[tile.table];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    if (off < tile.count) {
+      const int64_t p = tile.start + off;
+      inv[p] = static_cast<uint32_t>(__ldcg(t.hash + slot_of[p])) & ~kRankTag;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K2
+// Per unique row: cache slot or miss; per-table miss counts; miss queue
+// (rows the GPU must fetch from the cold tier / owner); hash slot reset.
+__global__ void __launch_bounds__(kThreads) k_partition(const TableDev* __restrict__ td, int T, int* __restrict__ ctr,
+                                                        const uint32_t* __restrict__ uniq,
+                                                        const uint16_t* __restrict__ utab,
+                                                        const uint32_t* __restrict__ uslot, int32_t* __restrict__ usrc,
+                                                        uint32_t* __restrict__ missq) {
+  Counters c = counters(ctr, T);
+  const int U = c.ubase[T];
+  for (int base = blockIdx.x * blockDim.x; base < U; base += gridDim.x * blockDim.x) {
+    const int g = base + threadIdx.x;
+    const bool live = g < U;
+    int tab = -1;
+    bool miss = false;
+    if (live) {
+      tab = utab[g];
+      const TableDev t = td[tab];
+      const int32_t s = __ldg(t.remap + uniq[g]);
+      usrc[g] = s;
+      miss = s < 0;
+      t.hash[uslot[g]] = kEmptySlot;
+    }
+    const unsigned peers = __match_any_sync(kFull, tab);
+    const int nm = group_count(peers, miss);
+    if (live && nm && (__ffs(peers) - 1) == lane_id()) atomicAdd(c.M + tab, nm);
+    const unsigned mb = __ballot_sync(kFull, miss);
+    int qbase = 0;
+    if (mb && lane_id() == __ffs(mb) - 1) qbase = atomicAdd(c.miss_total, __popc(mb));
+    qbase = __shfl_sync(kFull, qbase, __ffs(mb ? mb : 1u) - 1);
+    if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
+  }
+}
+
+// ------------------------------------------------------------------ K3
+// VEC = D/4 lanes per row, 128-bit loads; each thread keeps R rows in flight.
+template <int VEC>
+struct RowMap {
+  static constexpr int kRowsPerWarp = 32 / VEC;
+  int sub, c;
+  __device__ RowMap() : sub(lane_id() / VEC), c(lane_id() % VEC) {}
+};
+
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                                                     const int32_t* __restrict__ usrc, const float* __restrict__ cache,
+                                                     float* __restrict__ urows, int local_hbm, int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
+    float4 v[R];
+    int dst[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      dst[r] = -1;
+      if (g < U) {
+        const int32_t s = usrc[g];
+        const float* src = nullptr;
+        if (s >= 0) {
+          src = cache + static_cast<int64_t>(s) * D;
+        } else if (local_hbm) {
+          const uint32_t id = uniq[g];
+          if (static_cast<int>(id % world) == rank) src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+        }
+        if (src) {
+          v[r] = ldg4(src + m.c * 4);
+          dst[r] = g;
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+}
+
+// Misses served from pinned host memory (UVA-mapped shard), side stream.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                          const uint32_t* __restrict__ missq,
+                                                          const uint32_t* __restrict__ uniq,
+                                                          const uint16_t* __restrict__ utab, float* __restrict__ urows,
+                                                          int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+    float4 v[R];
+    int dst[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      dst[r] = -1;
+      if (q < nm) {
+        const uint32_t g = missq[q];
+        const uint32_t id = uniq[g];
+        if (static_cast<int>(id % world) == rank) {
+          const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+          v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
+          dst[r] = static_cast<int>(g);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+}
+
+// ------------------------------------------------------------------ K5
+// Bags are visited sample-major (q = s*T + t) so each warp writes a
+// contiguous stretch of the [B, T*D] output.
+__device__ __forceinline__ void bag_range(const TableDev* td, const int64_t* bag_off, int T, int B, int P, int s,
+                                          int t, int64_t* lo, int64_t* hi) {
+  if (bag_off) {
+    *lo = bag_off[static_cast<int64_t>(t) * B + s];
+    *hi = bag_off[static_cast<int64_t>(t) * B + s + 1];
+  } else {
+    *lo = td[t].base + static_cast<int64_t>(s) * P;
+    *hi = *lo + P;
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
+                                                   const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
+                                                   const float* __restrict__ urows, float* __restrict__ out) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nbags = T * B;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW; q0 < nbags; q0 += nwarps * RPW) {
+    const int q = q0 + m.sub;
+    if (q >= nbags) continue;
+    const int s = q / T, t = q - s * T;
+    int64_t lo, hi;
+    bag_range(td, bag_off, T, B, P, s, t, &lo, &hi);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t i = lo;
+    for (; i + 4 <= hi; i += 4) {  // 4 rows in flight, summed in lookup order
+      const uint32_t u0 = inv[i], u1 = inv[i + 1], u2 = inv[i + 2], u3 = inv[i + 3];
+      const float4 a = ldg4(urows + static_cast<int64_t>(u0) * D + m.c * 4);
+      const float4 b = ldg4(urows + static_cast<int64_t>(u1) * D + m.c * 4);
+      const float4 c = ldg4(urows + static_cast<int64_t>(u2) * D + m.c * 4);
+      const float4 d = ldg4(urows + static_cast<int64_t>(u3) * D + m.c * 4);
+      acc = add4(add4(add4(add4(acc, a), b), c), d);
+    }
+    for (; i < hi; ++i) acc = add4(acc, ldg4(urows + static_cast<int64_t>(inv[i]) * D + m.c * 4));
+    st4(out + (static_cast<int64_t>(s) * T + t) * D + m.c * 4, acc);
+  }
+}
+
+// ------------------------------------------------------------------ K6
+__global__ void k_zero(float4* __restrict__ p, const int* __restrict__ ctr, int T, int vec_per_row) {
+  const int64_t n = static_cast<int64_t>(counters(const_cast<int*>(ctr), T).ubase[T]) * vec_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// grad of bag (s, t) is added to the unique row of every lookup in the bag.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
+                                                      const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
+                                                      const float* __restrict__ grad, float* __restrict__ ugrad) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nbags = T * B;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW; q0 < nbags; q0 += nwarps * RPW) {
+    const int q = q0 + m.sub;
+    if (q >= nbags) continue;
+    const int s = q / T, t = q - s * T;
+    int64_t lo, hi;
+    bag_range(td, bag_off, T, B, P, s, t, &lo, &hi);
+    const float4 gv = ld_stream4(grad + (static_cast<int64_t>(s) * T + t) * D + m.c * 4);
+    for (int64_t i = lo; i < hi; ++i)
+      atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(inv[i]) * D + m.c * 4), gv);
+  }
+}
+
+// SGD on every unique row: w = w_gathered - lr * g, written to the cache copy
+// (hits) or the owning local shard (misses, HBM or mapped host).
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                    const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                                                    const int32_t* __restrict__ usrc, const float* __restrict__ urows,
+                                                    const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
+                                                    int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      if (g >= U) continue;
+      const int32_t s = usrc[g];
+      float* dst = nullptr;
+      if (s >= 0) {
+        dst = cache + static_cast<int64_t>(s) * D;
+      } else {
+        const uint32_t id = uniq[g];
+        if (static_cast<int>(id % world) == rank) dst = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+      }
+      if (!dst) continue;
+      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
+      st4(dst + m.c * 4, make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+    }
+  }
+}
+
+// -------------------------------------------------- table maintenance
+__device__ __forceinline__ float synth_value(uint64_t seed, float scale, uint32_t t, uint64_t id, uint32_t D,
+                                            uint32_t c) {
+  const uint64_t x = mix64(seed + kGolden * ((static_cast<uint64_t>(t) << 40) ^ (id * D + c)));
+  const float f = static_cast<float>(x >> 40) * 0x1.0p-24f;
+  return scale * __fsub_rn(__fmul_rn(2.0f, f), 1.0f);
+}
+
+__global__ void k_init_shard(float* __restrict__ store, uint64_t local_rows, uint32_t t, uint32_t D, int rank,
+                             int world, uint64_t seed, float scale) {
+  const uint64_t n = local_rows * D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / D;
+    const uint32_t c = static_cast<uint32_t>(i - r * D);
+    store[i] = synth_value(seed, scale, t, r * world + rank, D, c);
+  }
+}
+
+__global__ void k_set_remap(int32_t* __restrict__ remap, const uint32_t* __restrict__ ids, uint64_t k, int64_t slot0) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += (uint64_t)gridDim.x * blockDim.x)
+    remap[ids[j]] = static_cast<int32_t>(slot0 + j);
+}
+
+// cache rows <- authoritative storage (world == 1) or the synthetic init.
+__global__ void k_fill_cache(float* __restrict__ cache, const uint32_t* __restrict__ ids, const uint16_t* __restrict__ tabs,
+                             uint64_t k, const TableDev* __restrict__ td, uint32_t D, int from_store, uint64_t seed,
+                             float scale, int rank, int world) {
+  const uint64_t n = k * D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = i / D;
+    const uint32_t c = static_cast<uint32_t>(i - j * D);
+    const uint32_t id = ids[j];
+    const uint32_t t = tabs[j];
+    if (from_store && static_cast<int>(id % world) == rank)
+      cache[i] = td[t].store[static_cast<uint64_t>(id / world) * D + c];
+    else
+      cache[i] = synth_value(seed, scale, t, id, D, c);
+  }
+}
+
+// Write back cached rows owned by this rank into the shard (placement change).
+__global__ void k_flush_cache(const float* __restrict__ cache, const uint32_t* __restrict__ ids,
+                              const uint16_t* __restrict__ tabs, uint64_t k, const TableDev* __restrict__ td, uint32_t D,
+                              int rank, int world) {
+  const uint64_t n = k * D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = i / D;
+    const uint32_t id = ids[j];
+    if (static_cast<int>(id % world) == rank)
+      td[tabs[j]].store[static_cast<uint64_t>(id / world) * D + (i - j * D)] = cache[i];
+  }
+}
+
+__global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uint32_t* __restrict__ ids, uint64_t n,
+                          uint32_t D, float* __restrict__ cache, float* __restrict__ buf, int write, int rank, int world,
+                          int* __restrict__ err) {
+  const TableDev tb = td[t];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * D; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = i / D;
+    const uint32_t c = static_cast<uint32_t>(i - j * D);
+    const uint32_t id = ids[j];
+    if (id >= tb.rows) { atomicExch(err, 1); continue; }
+    const int32_t s = tb.remap[id];
+    const bool own = static_cast<int>(id % world) == rank;
+    float* srow = own ? tb.store + static_cast<uint64_t>(id / world) * D : nullptr;
+    if (write) {
+      if (s >= 0) cache[static_cast<uint64_t>(s) * D + c] = buf[i];
+      if (srow) srow[c] = buf[i];
+      if (s < 0 && !srow) atomicExch(err, 2);
+    } else {
+      if (s >= 0) buf[i] = cache[static_cast<uint64_t>(s) * D + c];
+      else if (srow) buf[i] = srow[c];
+      else atomicExch(err, 2);
+    }
+  }
+}
+
+// ------------------------------------------------------------ host side
+static int persistent_grid(int device) { return sm_count(device) * 8; }
+
+static uint32_t log2_ceil(uint64_t x) {
+  uint32_t l = 0;
+  while ((1ull << l) < x) ++l;
+  return l;
+}
+
+Engine::~Engine() {
+  if (ev_part) cudaEventDestroy(ev_part);
+  if (ev_side) cudaEventDestroy(ev_side);
+  if (side) cudaStreamDestroy(side);
+  if (store_host) cudaFreeHost(store_host);
+  destroy_comm();
+}
+
+void Engine::create(const ec_tables_config& c) {
+  if (c.num_tables < 1) invalid("need at least one table");
+  if (c.num_tables > 65535) invalid("at most 65535 tables");
+  if (c.dim < 4 || c.dim % 4 != 0 || c.dim > 1024) invalid("dim must be a multiple of 4 in [4, 1024]");
+  if (c.world < 1 || c.rank < 0 || c.rank >= c.world) invalid("rank/world out of range");
+  if (c.storage != EC_STORAGE_HBM && c.storage != EC_STORAGE_HOST) invalid("unknown storage tier");
+  if (c.max_lookups_per_table < 1 || c.max_lookups_per_table > (1ull << 30))
+    invalid("max_lookups_per_table must be in [1, 2^30]");
+  if (c.max_batch_size < 1) invalid("max_batch_size must be >= 1");
+  if (!c.rows_host) invalid("null rows");
+  use_device(c.device);
+  device = c.device;
+  T = c.num_tables;
+  D = c.dim;
+  storage = c.storage;
+  rank = c.rank;
+  world = c.world;
+  max_n = c.max_lookups_per_table;
+  max_b = c.max_batch_size;
+  rows.assign(c.rows_host, c.rows_host + T);
+  local_rows.resize(T);
+  store_off.assign(T + 1, 0);
+  remap_off.assign(T + 1, 0);
+  hash_off.assign(T + 1, 0);
+  hash_lg.resize(T);
+  for (uint32_t t = 0; t < T; ++t) {
+    if (rows[t] < 1 || rows[t] > 0xFFFFFFFFull) invalid("table " + std::to_string(t) + " rows out of [1, 2^32-1]");
+    local_rows[t] = rows[t] > static_cast<uint64_t>(rank) ? (rows[t] - rank + world - 1) / world : 0;
+    store_off[t + 1] = store_off[t] + local_rows[t];
+    remap_off[t + 1] = remap_off[t] + rows[t];
+    hash_lg[t] = std::max<uint32_t>(5, log2_ceil(2 * std::min<uint64_t>(max_n, rows[t])));
+    hash_off[t + 1] = hash_off[t] + (1ull << hash_lg[t]);
+  }
+  const uint64_t store_elems = store_off[T] * D;
+  if (storage == EC_STORAGE_HBM) {
+    store_dev.alloc(store_elems);
+    store_base = store_dev.p;
+  } else {
+    EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&store_host), std::max<uint64_t>(store_elems, 1) * sizeof(float),
+                          cudaHostAllocMapped | cudaHostAllocPortable));
+    EC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&store_base), store_host, 0));
+  }
+  remap.alloc(remap_off[T]);
+  EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
+  hash.alloc(hash_off[T]);
+  EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
+  const uint64_t N = max_n * T;
+  slot_of.alloc(N);
+  inv.alloc(N);
+  uniq.alloc(N);
+  uslot.alloc(N);
+  usrc.alloc(N);
+  missq.alloc(N);
+  utab.alloc(N);
+  urows.alloc(N * D);
+  ugrad.alloc(N * D);
+  const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
+  tiles.alloc(max_tiles);
+  tile_cnt.alloc(max_tiles);
+  first_tile.alloc(T + 1);
+  ctr.alloc(counters_size(T));
+  EC_CUDA(cudaMemset(ctr.p, 0, ctr.bytes()));
+  tdev.alloc(T);
+  td_host.resize(T);
+  for (uint32_t t = 0; t < T; ++t) {
+    TableDev& d = td_host[t];
+    d.hash = hash.p + hash_off[t];
+    d.shift = 32 - hash_lg[t];
+    d.mask = static_cast<uint32_t>((1ull << hash_lg[t]) - 1);
+    d.remap = remap.p + remap_off[t];
+    d.store = store_base + store_off[t] * D;
+    d.rows = rows[t];
+    d.base = 0;
+    d.n = 0;
+  }
+  EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
+  EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+  EC_CUDA(cudaDeviceSynchronize());
+}
+
+uint64_t Engine::device_bytes() const {
+  return store_dev.bytes() + remap.bytes() + hash.bytes() + cache.bytes() + slot_of.bytes() + inv.bytes() +
+         uniq.bytes() + uslot.bytes() + usrc.bytes() + missq.bytes() + utab.bytes() + urows.bytes() +
+         ugrad.bytes() + tiles.bytes() + tile_cnt.bytes() + ctr.bytes() + cache_ids.bytes() + cache_tab.bytes() +
+         exch_bytes();
+}
+
+void Engine::init_synthetic(uint64_t seed, float scale, cudaStream_t st) {
+  use_device(device);
+  for (uint32_t t = 0; t < T; ++t) {
+    if (!local_rows[t]) continue;
+    const uint64_t n = local_rows[t] * D;
+    const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, persistent_grid(device) * 4ull));
+    k_init_shard<<<grid, 256, 0, st>>>(store_base + store_off[t] * D, local_rows[t], t, D, rank, world, seed, scale);
+    EC_LAUNCH();
+  }
+  synth_seed = seed;
+  synth_scale = scale;
+  synth_valid = true;
+  if (cache_k_total) fill_cache(st, /*from_store=*/world == 1);
+}
+
+void Engine::fill_cache(cudaStream_t st, bool from_store) {
+  if (!cache_k_total) return;
+  if (!from_store && !synth_valid)
+    invalid("multi-rank cache placement needs ec_tables_init_synthetic first (rows of other shards are not local)");
+  const uint64_t n = cache_k_total * D;
+  const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, persistent_grid(device) * 4ull));
+  k_fill_cache<<<grid, 256, 0, st>>>(cache.p, cache_ids.p, cache_tab.p, cache_k_total, tdev.p, D, from_store ? 1 : 0,
+                                     synth_seed, synth_scale, rank, world);
+  EC_LAUNCH();
+}
+
+void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
+  use_device(device);
+  // host-side validation + first-occurrence dedup of each table's list
+  std::vector<uint32_t> all_ids;
+  std::vector<uint16_t> all_tab;
+  std::vector<uint64_t> koff(T + 1, 0);
+  for (uint32_t t = 0; t < T; ++t) {
+    std::vector<uint8_t> seen;
+    const uint64_t kt = k ? k[t] : 0;
+    if (kt && (!ids || !ids[t])) invalid("null cache id list for table " + std::to_string(t));
+    if (kt > rows[t]) invalid("table " + std::to_string(t) + ": cache larger than the table");
+    if (kt) seen.assign(rows[t], 0);
+    for (uint64_t j = 0; j < kt; ++j) {
+      const uint32_t id = ids[t][j];
+      if (id >= rows[t])
+        invalid("cache id " + std::to_string(id) + " out of range [0, " + std::to_string(rows[t]) + ")");
+      if (seen[id]) continue;  // duplicates count once (cost_model.hpp:59-61)
+      seen[id] = 1;
+      all_ids.push_back(id);
+      all_tab.push_back(static_cast<uint16_t>(t));
+    }
+    koff[t + 1] = all_ids.size();
+  }
+  if (all_ids.size() > 0x7FFFFFFFull) invalid("cache larger than 2^31 rows");
+  EC_CUDA(cudaDeviceSynchronize());
+  // write back the current cache before dropping it
+  if (cache_k_total) {
+    const uint64_t n = cache_k_total * D;
+    const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, persistent_grid(device) * 4ull));
+    k_flush_cache<<<grid, 256>>>(cache.p, cache_ids.p, cache_tab.p, cache_k_total, tdev.p, D, rank, world);
+    EC_LAUNCH();
+  }
+  EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
+  cache_k_total = all_ids.size();
+  cache_k.resize(T);
+  for (uint32_t t = 0; t < T; ++t) cache_k[t] = koff[t + 1] - koff[t];
+  cache.alloc(cache_k_total * D);
+  cache_ids.alloc(cache_k_total);
+  cache_tab.alloc(cache_k_total);
+  if (cache_k_total) {
+    EC_CUDA(cudaMemcpy(cache_ids.p, all_ids.data(), cache_k_total * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    EC_CUDA(cudaMemcpy(cache_tab.p, all_tab.data(), cache_k_total * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    for (uint32_t t = 0; t < T; ++t) {
+      const uint64_t kt = koff[t + 1] - koff[t];
+      if (!kt) continue;
+      k_set_remap<<<static_cast<int>(std::min<uint64_t>((kt + 255) / 256, 4096)), 256>>>(
+          remap.p + remap_off[t], cache_ids.p + koff[t], kt, static_cast<int64_t>(koff[t]));
+      EC_LAUNCH();
+    }
+    fill_cache(nullptr, /*from_store=*/world == 1);
+  }
+  EC_CUDA(cudaDeviceSynchronize());
+}
+
+void Engine::rw_rows(uint32_t t, const uint32_t* ids, uint64_t n, float* buf_host, bool write) {
+  if (t >= T) invalid("table index out of range");
+  use_device(device);
+  if (!n) return;
+  DevBuf<uint32_t> dids(n);
+  DevBuf<float> dbuf(n * D);
+  DevBuf<int> derr(1);
+  EC_CUDA(cudaMemset(derr.p, 0, sizeof(int)));
+  EC_CUDA(cudaMemcpy(dids.p, ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  if (write) EC_CUDA(cudaMemcpy(dbuf.p, buf_host, n * D * sizeof(float), cudaMemcpyHostToDevice));
+  const int grid = static_cast<int>(std::min<uint64_t>((n * D + 255) / 256, 4096));
+  EC_CUDA(cudaDeviceSynchronize());
+  k_rw_rows<<<grid, 256>>>(tdev.p, t, dids.p, n, D, cache.p, dbuf.p, write ? 1 : 0, rank, world, derr.p);
+  EC_LAUNCH();
+  EC_CUDA(cudaDeviceSynchronize());
+  int e = 0;
+  EC_CUDA(cudaMemcpy(&e, derr.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (e == 1) invalid("row id out of range for table " + std::to_string(t));
+  if (e == 2) invalid("row not held by this rank (neither cached nor owned)");
+  if (!write) EC_CUDA(cudaMemcpy(buf_host, dbuf.p, n * D * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+// Per-batch geometry: tiles never straddle tables; uploaded only on change.
+void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
+  bool same = have_geom && b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed;
+  for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
+  if (same) return;
+  geom_off.assign(b.table_offsets_host, b.table_offsets_host + T + 1);
+  std::vector<Tile> tl;
+  std::vector<int> ft(T + 1);
+  for (uint32_t t = 0; t < T; ++t) {
+    const int64_t lo = geom_off[t], n = geom_off[t + 1] - geom_off[t];
+    ft[t] = static_cast<int>(tl.size());
+    for (int64_t s = 0; s < n; s += kTile)
+      tl.push_back(Tile{t, static_cast<uint32_t>(std::min<int64_t>(kTile, n - s)), lo + s});
+    td_host[t].base = lo;
+    td_host[t].n = n;
+  }
+  ft[T] = static_cast<int>(tl.size());
+  ntiles = static_cast<int>(tl.size());
+  EC_CUDA(cudaStreamSynchronize(st));
+  if (ntiles) EC_CUDA(cudaMemcpy(tiles.p, tl.data(), tl.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+  EC_CUDA(cudaMemcpy(first_tile.p, ft.data(), (T + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
+  geom_b = b.batch_size;
+  geom_p = b.pooling;
+  geom_fixed = b.bag_offsets_dev == nullptr;
+  have_geom = true;
+}
+
+template <int VEC>
+void Engine::launch_row_kernels_fwd(cudaStream_t st) {
+  const int grid = persistent_grid(device);
+  if (storage == EC_STORAGE_HOST) {
+    // host misses on the side stream, overlapping the HBM hit gather
+    EC_CUDA(cudaEventRecord(ev_part, st));
+    EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    k_gather_host<VEC, 4><<<grid, kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank, world);
+    EC_LAUNCH();
+    EC_CUDA(cudaEventRecord(ev_side, side));
+  }
+  k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, cache.p, urows.p,
+                                              storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+  EC_LAUNCH();
+  if (world > 1) exchange_fwd(st);
+  if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  k_pool<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, inv.p,
+                                         urows.p, out_ptr);
+  EC_LAUNCH();
+}
+
+template <int VEC>
+void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st) {
+  const int grid = persistent_grid(device);
+  k_zero<<<grid, kThreads, 0, st>>>(reinterpret_cast<float4*>(ugrad.p), ctr.p, T, VEC);
+  EC_LAUNCH();
+  k_scatter<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
+                                            inv.p, grad, ugrad.p);
+  EC_LAUNCH();
+  if (world > 1) exchange_bwd(lr, st);
+  k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
+                                             rank, world);
+  EC_LAUNCH();
+}
+
+#define EC_DISPATCH_VEC(FN, ...)                                                  \
+  switch (D / 4) {                                                                \
+    case 1: FN<1>(__VA_ARGS__); break;                                            \
+    case 2: FN<2>(__VA_ARGS__); break;                                            \
+    case 4: FN<4>(__VA_ARGS__); break;                                            \
+    case 8: FN<8>(__VA_ARGS__); break;                                            \
+    case 16: FN<16>(__VA_ARGS__); break;                                          \
+    case 32: FN<32>(__VA_ARGS__); break;                                          \
+    default: invalid("dim must be 4, 8, 16, 32, 64 or 128 for the lookup kernels"); \
+  }
+
+void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
+  if (!b.table_offsets_host || !b.indices_dev) invalid("batch needs indices and table offsets");
+  if (b.batch_size < 1 || b.batch_size > max_b) invalid("batch_size out of [1, max_batch_size]");
+  if (b.table_offsets_host[0] != 0) invalid("table_offsets[0] must be 0");
+  for (uint32_t t = 0; t < T; ++t) {
+    const int64_t n = b.table_offsets_host[t + 1] - b.table_offsets_host[t];
+    if (n < 0 || static_cast<uint64_t>(n) > max_n)
+      invalid("table " + std::to_string(t) + ": lookups " + std::to_string(n) + " out of [0, max_lookups_per_table]");
+    if (!b.bag_offsets_dev && n != static_cast<int64_t>(b.batch_size) * b.pooling)
+      invalid("table " + std::to_string(t) + ": fixed pooling needs batch_size*pooling lookups");
+  }
+  if (world > 1 && !comm_ready()) invalid("world > 1 needs ec_tables_attach_comm");
+  use_device(device);
+  set_geometry(b, st);
+  bag_off = b.bag_offsets_dev;
+  out_ptr = out;
+  const int grid = persistent_grid(device);
+  if (ntiles) {
+    k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, counters(ctr.p, T).err);
+    EC_LAUNCH();
+    k_count<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, tile_cnt.p);
+    EC_LAUNCH();
+  }
+  k_scan<<<1, 1024, 0, st>>>(tile_cnt.p, ntiles, first_tile.p, static_cast<int>(T), ctr.p);
+  EC_LAUNCH();
+  if (ntiles) {
+    k_emit<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, tile_cnt.p, uniq.p, uslot.p, utab.p);
+    EC_LAUNCH();
+    k_inverse<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p);
+    EC_LAUNCH();
+  }
+  k_partition<<<grid, kThreads, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, uslot.p, usrc.p, missq.p);
+  EC_LAUNCH();
+  EC_DISPATCH_VEC(launch_row_kernels_fwd, st);
+  have_fwd = true;
+}
+
+void Engine::backward(const float* grad, float lr, cudaStream_t st) {
+  if (!have_fwd) invalid("ec_lookup_bwd needs a preceding ec_lookup_fwd");
+  if (!grad) invalid("null gradient");
+  use_device(device);
+  EC_DISPATCH_VEC(launch_row_kernels_bwd, grad, lr, st);
+}
+
+void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
+  use_device(device);
+  h.resize(counters_size(T));
+  EC_CUDA(cudaStreamSynchronize(st));
+  EC_CUDA(cudaStreamSynchronize(side));
+  EC_CUDA(cudaMemcpy(h.data(), ctr.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  Counters c = counters(h.data(), T);
+  if (*c.err) {
+    *c.err = 0;
+    EC_CUDA(cudaMemset(counters(ctr.p, T).err, 0, sizeof(int)));
+    invalid("lookup id out of range of its table in the last batch");
+  }
+}
+
+}  // namespace ec
+
+// ===================================================================== ABI
+using namespace ec;
+
+struct ec_tables_s {
+  Engine e;
+};
+
+static Engine& E(ec_tables t) {
+  if (!t) invalid("null tables handle");
+  return t->e;
+}
+
+extern "C" {
+
+int ec_tables_create(const ec_tables_config* cfg, ec_tables* out) {
+  return guard([&] {
+    if (!cfg || !out) invalid("null argument");
+    auto* t = new ec_tables_s;
+    try {
+      t->e.create(*cfg);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+void ec_tables_destroy(ec_tables t) {
+  if (!t) return;
+  cudaSetDevice(t->e.device);
+  cudaDeviceSynchronize();
+  delete t;
+}
+
+int ec_tables_memory(ec_tables t, uint64_t* dev, uint64_t* host) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (dev) *dev = e.device_bytes();
+    if (host) *host = e.store_host ? e.store_off[e.T] * e.D * sizeof(float) : 0;
+  });
+}
+
+int ec_tables_init_synthetic(ec_tables t, uint64_t seed, float scale, void* stream) {
+  return guard([&] { E(t).init_synthetic(seed, scale, as_stream(stream)); });
+}
+
+int ec_tables_place_cache(ec_tables t, const uint32_t* const* ids, const uint64_t* k) {
+  return guard([&] { E(t).place_cache(ids, k); });
+}
+
+int ec_tables_read_rows(ec_tables t, uint32_t table, const uint32_t* ids, uint64_t n, float* out) {
+  return guard([&] { E(t).rw_rows(table, ids, n, out, false); });
+}
+
+int ec_tables_write_rows(ec_tables t, uint32_t table, const uint32_t* ids, uint64_t n, const float* rows) {
+  return guard([&] { E(t).rw_rows(table, ids, n, const_cast<float*>(rows), true); });
+}
+
+int ec_lookup_fwd(ec_tables t, const ec_batch* b, float* out, void* stream) {
+  return guard([&] {
+    if (!b || !out) invalid("null argument");
+    E(t).forward(*b, out, as_stream(stream));
+  });
+}
+
+int ec_lookup_bwd(ec_tables t, const float* grad, float lr, void* stream) {
+  return guard([&] { E(t).backward(grad, lr, as_stream(stream)); });
+}
+
+int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* u_per, int64_t* m_per) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (!e.have_fwd) invalid("no forward batch yet");
+    std::vector<int> h;
+    e.read_counters(as_stream(stream), h);
+    Counters c = counters(h.data(), e.T);
+    ec_batch_stats s{};
+    s.lookups = static_cast<uint64_t>(e.geom_off[e.T]);
+    s.index_units = s.lookups;
+    for (uint32_t i = 0; i < e.T; ++i) {
+      s.unique_rows += c.U[i];
+      s.miss_rows += c.M[i];
+      s.hot_tables += c.M[i] == 0;
+      if (u_per) u_per[i] = c.U[i];
+      if (m_per) m_per[i] = c.M[i];
+    }
+    s.hit_rows = s.unique_rows - s.miss_rows;
+    s.model_bytes = s.miss_rows * e.D * sizeof(float) + s.index_units * sizeof(uint32_t);
+    s.wire_rows = e.last_wire_rows;
+    s.wire_bytes = e.last_wire_bytes;
+    *out = s;
+  });
+}
+
+static void table_span(Engine& e, uint32_t table, std::vector<int>& h, int* lo, int* n) {
+  if (table >= e.T) invalid("table index out of range");
+  if (!e.have_fwd) invalid("no forward batch yet");
+  e.read_counters(nullptr, h);
+  Counters c = counters(h.data(), e.T);
+  *lo = c.ubase[table];
+  *n = c.U[table];
+}
+
+int ec_export_unique(ec_tables t, uint32_t table, uint32_t* out, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    Engine& e = E(t);
+    std::vector<int> h;
+    int lo, n;
+    table_span(e, table, h, &lo, &n);
+    *count = static_cast<uint64_t>(n);
+    if (out) EC_CUDA(cudaMemcpy(out, e.uniq.p + lo, std::min<uint64_t>(cap, n) * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+int ec_export_inverse(ec_tables t, uint32_t table, uint32_t* out) {
+  return guard([&] {
+    Engine& e = E(t);
+    std::vector<int> h;
+    int lo, n;
+    table_span(e, table, h, &lo, &n);
+    const int64_t a = e.geom_off[table], m = e.geom_off[table + 1] - a;
+    EC_CUDA(cudaMemcpy(out, e.inv.p + a, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < m; ++i) out[i] -= static_cast<uint32_t>(lo);
+  });
+}
+
+int ec_export_hit(ec_tables t, uint32_t table, uint8_t* out) {
+  return guard([&] {
+    Engine& e = E(t);
+    std::vector<int> h;
+    int lo, n;
+    table_span(e, table, h, &lo, &n);
+    std::vector<int32_t> s(n);
+    if (n) EC_CUDA(cudaMemcpy(s.data(), e.usrc.p + lo, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) out[i] = s[i] >= 0;
+  });
+}
+
+int ec_export_rows(ec_tables t, uint32_t table, float* out) {
+  return guard([&] {
+    Engine& e = E(t);
+    std::vector<int> h;
+    int lo, n;
+    table_span(e, table, h, &lo, &n);
+    if (n) EC_CUDA(cudaMemcpy(out, e.urows.p + static_cast<int64_t>(lo) * e.D, static_cast<int64_t>(n) * e.D * sizeof(float),
+                              cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

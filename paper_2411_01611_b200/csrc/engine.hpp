@@ -1,0 +1,109 @@
+// Lookup-engine state shared by engine.cu and exchange.cu.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+
+namespace ec {
+
+// Per-table constants + per-batch geometry, read by every engine kernel.
+struct TableDev {
+  unsigned long long* hash;  // open-addressing set for this table's batch
+  uint32_t shift, mask;      // hash_slot shift, capacity - 1
+  const int32_t* remap;      // id -> global cache row, -1 = not cached
+  float* store;              // local shard (device pointer; mapped if pinned host)
+  uint64_t rows;             // E_t
+  int64_t base;              // first lookup of this table in the batch
+  int64_t n;                 // lookups of this table in the batch
+};
+
+struct Tile {
+  uint32_t table;
+  uint32_t count;
+  int64_t start;
+};
+
+// Per-batch device counters, one int array: U[T] M[T] ubase[T+1] miss_total err
+struct Counters {
+  int *U, *M, *ubase, *miss_total, *err;
+};
+__host__ __device__ inline Counters counters(int* p, int T) {
+  return Counters{p, p + T, p + 2 * T, p + 3 * T + 1, p + 3 * T + 2};
+}
+inline size_t counters_size(int T) { return 3 * static_cast<size_t>(T) + 3; }
+
+struct Exchange;  // exchange.cu
+
+struct Engine {
+  int device = 0;
+  uint32_t T = 0, D = 0;
+  int storage = EC_STORAGE_HBM;
+  int rank = 0, world = 1;
+  uint64_t max_n = 0;
+  uint32_t max_b = 0;
+  std::vector<uint64_t> rows, local_rows, store_off, remap_off, hash_off;
+  std::vector<uint32_t> hash_lg;
+
+  DevBuf<float> store_dev;
+  float* store_host = nullptr;  // pinned, mapped
+  float* store_base = nullptr;  // device-visible base of the shard
+  DevBuf<int32_t> remap;
+  DevBuf<unsigned long long> hash;
+  DevBuf<float> cache;
+  DevBuf<uint32_t> cache_ids;
+  DevBuf<uint16_t> cache_tab;
+  uint64_t cache_k_total = 0;
+  std::vector<uint64_t> cache_k;
+  uint64_t synth_seed = 0;
+  float synth_scale = 0.f;
+  bool synth_valid = false;
+
+  DevBuf<uint32_t> slot_of, inv, uniq, uslot, missq;
+  DevBuf<int32_t> usrc;
+  DevBuf<uint16_t> utab;
+  DevBuf<float> urows, ugrad;
+  DevBuf<Tile> tiles;
+  DevBuf<int> tile_cnt, first_tile, ctr;
+  DevBuf<TableDev> tdev;
+  std::vector<TableDev> td_host;
+  int ntiles = 0;
+
+  // geometry of the last batch
+  bool have_geom = false, geom_fixed = true, have_fwd = false;
+  std::vector<int64_t> geom_off;
+  uint32_t geom_b = 0, geom_p = 0;
+  const int64_t* bag_off = nullptr;
+  float* out_ptr = nullptr;
+
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr;
+
+  Exchange* ex = nullptr;
+  uint64_t last_wire_rows = 0, last_wire_bytes = 0;
+
+  ~Engine();
+  void create(const ec_tables_config& c);
+  uint64_t device_bytes() const;
+  void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
+  void fill_cache(cudaStream_t st, bool from_store);
+  void place_cache(const uint32_t* const* ids, const uint64_t* k);
+  void rw_rows(uint32_t t, const uint32_t* ids, uint64_t n, float* buf, bool write);
+  void set_geometry(const ec_batch& b, cudaStream_t st);
+  void forward(const ec_batch& b, float* out, cudaStream_t st);
+  void backward(const float* grad, float lr, cudaStream_t st);
+  void read_counters(cudaStream_t st, std::vector<int>& h);
+  template <int VEC> void launch_row_kernels_fwd(cudaStream_t st);
+  template <int VEC> void launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st);
+
+  // multi-GPU (exchange.cu)
+  bool comm_ready() const;
+  void attach_comm(const uint8_t* id128);
+  void destroy_comm();
+  uint64_t exch_bytes() const;
+  void exchange_fwd(cudaStream_t st);
+  void exchange_bwd(float lr, cudaStream_t st);
+};
+
+}  // namespace ec

@@ -1,0 +1,174 @@
+"""EmbeddingTables: the lookup engine (K1..K6) behind a torch-friendly API.
+
+Thin wrapper over ``ec_tables_*`` / ``ec_lookup_*`` (include/embcomm_gpu.h).
+Torch provides device buffers and the current stream; every computation is
+one of the library's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import ValidationError, check
+
+STORAGE = {"hbm": 0, "host": 1}
+
+
+def _stream_ptr(torch, device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class EmbeddingTables:
+    """Row-wise sharded fp32 embedding tables with a replicated HBM hot-row cache.
+
+    rows: E_t per table; dim: D (4, 8, 16, 32, 64 or 128); storage: cold tier
+    "hbm" or "host" (pinned, read by the GPU over the host link); rank/world:
+    owner(id) = id % world.
+    """
+
+    def __init__(self, rows: Sequence[int], dim: int, *, storage: str = "hbm", rank: int = 0, world: int = 1,
+                 max_lookups_per_table: int, max_batch_size: int, device: int = 0):
+        import torch
+        self.torch = torch
+        self.rows = [int(r) for r in rows]
+        self.T = len(self.rows)
+        self.D = int(dim)
+        self.device = device
+        self.world = world
+        self.rank = rank
+        self._rows_c = (C.c_uint64 * self.T)(*self.rows)
+        cfg = N.TablesConfig(self.T, self.D, C.cast(self._rows_c, C.POINTER(C.c_uint64)), STORAGE[storage], rank,
+                             world, max_lookups_per_table, max_batch_size, device)
+        h = C.c_void_p()
+        check(N.lib().ec_tables_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._offsets = None
+        self._out = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().ec_tables_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----------------------------------------------------------- contents
+    def memory(self):
+        d, h = C.c_uint64(), C.c_uint64()
+        check(N.lib().ec_tables_memory(self._h, C.byref(d), C.byref(h)))
+        return {"device_bytes": d.value, "host_bytes": h.value}
+
+    def init_synthetic(self, seed: int, scale: float = 0.05):
+        check(N.lib().ec_tables_init_synthetic(self._h, seed, scale, _stream_ptr(self.torch, self.device)))
+
+    def place_cache(self, cached_ids: Sequence):
+        """cached_ids[t]: ids of table t held in the HBM cache (e.g. dist.top_ids(k_t))."""
+        arrs = [np.ascontiguousarray(c if c is not None else [], dtype=np.uint32) for c in cached_ids]
+        if len(arrs) != self.T:
+            raise ValidationError("need one cache id list per table")
+        ptrs = (C.c_void_p * self.T)(*[a.ctypes.data if a.size else None for a in arrs])
+        ks = np.array([a.size for a in arrs], dtype=np.uint64)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        check(N.lib().ec_tables_place_cache(self._h, ptrs, ks.ctypes.data))
+
+    def read_rows(self, table: int, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        out = np.empty((ids.size, self.D), np.float32)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        check(N.lib().ec_tables_read_rows(self._h, table, ids.ctypes.data, ids.size, out.ctypes.data))
+        return out
+
+    def write_rows(self, table: int, ids, rows):
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        rows = np.ascontiguousarray(rows, dtype=np.float32).reshape(ids.size, self.D)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        check(N.lib().ec_tables_write_rows(self._h, table, ids.ctypes.data, ids.size, rows.ctypes.data))
+
+    # -------------------------------------------------------------- batch
+    def forward(self, indices, table_offsets: Sequence[int], batch_size: int, pooling: int = 0,
+                bag_offsets=None, out=None):
+        """Pooled lookup.  indices: int32/uint32 CUDA tensor of all tables'
+        lookups concatenated; table_offsets: T+1 host ints; fixed pooling
+        (bag_offsets None) or CSR bag_offsets (int64 CUDA, T*B+1, table-major).
+        Returns [batch_size, T*D] fp32."""
+        torch = self.torch
+        if indices.dtype not in (torch.int32, torch.uint32) or not indices.is_cuda or not indices.is_contiguous():
+            raise ValidationError("indices must be a contiguous int32/uint32 CUDA tensor")
+        offs = np.ascontiguousarray(table_offsets, dtype=np.int64)
+        if offs.size != self.T + 1:
+            raise ValidationError("table_offsets needs num_tables+1 entries")
+        self._offsets = offs
+        if out is None:
+            out = torch.empty((batch_size, self.T * self.D), dtype=torch.float32, device=indices.device)
+        bo = 0
+        if bag_offsets is not None:
+            if bag_offsets.dtype != torch.int64 or not bag_offsets.is_cuda:
+                raise ValidationError("bag_offsets must be an int64 CUDA tensor")
+            bo = bag_offsets.data_ptr()
+        b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo or None, batch_size, pooling)
+        check(N.lib().ec_lookup_fwd(self._h, C.byref(b), out.data_ptr(), _stream_ptr(torch, self.device)))
+        self._out = out
+        return out
+
+    def backward(self, grad, lr: float):
+        torch = self.torch
+        if grad.dtype != torch.float32 or not grad.is_cuda or not grad.is_contiguous():
+            raise ValidationError("grad must be a contiguous fp32 CUDA tensor")
+        check(N.lib().ec_lookup_bwd(self._h, grad.data_ptr(), lr, _stream_ptr(torch, self.device)))
+
+    def stats(self, per_table: bool = False):
+        s = N.BatchStats()
+        u = np.zeros(self.T, np.int64)
+        m = np.zeros(self.T, np.int64)
+        check(N.lib().ec_lookup_stats(self._h, _stream_ptr(self.torch, self.device), C.byref(s), u.ctypes.data,
+                                      m.ctypes.data))
+        d = s.as_dict()
+        if per_table:
+            d["unique_per_table"] = u
+            d["miss_per_table"] = m
+        return d
+
+    # ------------------------------------------------------ parity exports
+    def export_unique(self, table: int) -> np.ndarray:
+        n = C.c_uint64()
+        check(N.lib().ec_export_unique(self._h, table, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.uint32)
+        check(N.lib().ec_export_unique(self._h, table, out.ctypes.data, out.size, C.byref(n)))
+        return out
+
+    def export_inverse(self, table: int) -> np.ndarray:
+        n = int(self._offsets[table + 1] - self._offsets[table])
+        out = np.empty(n, np.uint32)
+        check(N.lib().ec_export_inverse(self._h, table, out.ctypes.data))
+        return out
+
+    def export_hit(self, table: int) -> np.ndarray:
+        U = self.export_unique(table).size
+        out = np.empty(U, np.uint8)
+        check(N.lib().ec_export_hit(self._h, table, out.ctypes.data))
+        return out
+
+    def export_rows(self, table: int) -> np.ndarray:
+        U = self.export_unique(table).size
+        out = np.empty((U, self.D), np.float32)
+        check(N.lib().ec_export_rows(self._h, table, out.ctypes.data))
+        return out
+
+    # ---------------------------------------------------------- multi-GPU
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(N.lib().ec_comm_unique_id(buf))
+        return bytes(buf)
+
+    def attach_comm(self, uid: bytes):
+        buf = (C.c_uint8 * 128)(*uid)
+        check(N.lib().ec_tables_attach_comm(self._h, buf))
+

@@ -1,0 +1,187 @@
+"""Lookup engine (K1 dedup, K2 hit/miss, K3 gather, K5 pool, K6 backward) on
+the GPU vs the oracle and the compiled reference.
+
+Bar (north_star): unique sets, inverse indices, hit/miss sets and row counts
+bit-exact; gathered rows bitwise (rows are copied unchanged); pooled outputs
+and updated rows within 1e-5 relative of the fp64 restatement (tolerance
+written per assertion, atol covers values that cancel to ~0)."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-6
+KAGGLE = [1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683, 8351593, 3194, 27, 14992,
+          5461306, 10, 5652, 2173, 4, 7046547, 18, 15, 286181, 105, 142572]
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def make_ids(ec, torch, dists, n_per_table, seed):
+    """Table t's lookups = draws [0, n_t) of SplitMix64(substream(seed, t)) (K0)."""
+    offs = np.concatenate([[0], np.cumsum(n_per_table)]).astype(np.int64)
+    ids = torch.empty(int(offs[-1]), dtype=torch.int32, device="cuda")
+    for t, d in enumerate(dists):
+        if n_per_table[t]:
+            ec.DiscreteSampler(d).sample_into(ids.data_ptr() + 4 * int(offs[t]), ec.substream_seed(seed, t), 0,
+                                              int(n_per_table[t]))
+    torch.cuda.synchronize()
+    return ids, offs
+
+
+def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=None, P=None, B=None,
+                out=None, ref=None):
+    """Compare every export of the last forward with the oracle."""
+    T = len(rows)
+    stats = tab.stats(per_table=True)
+    pooled = out.cpu().numpy() if out is not None else None
+    for t in range(T):
+        seg = ids_host[offs[t]:offs[t + 1]]
+        u_o, inv_o = O.dedup(seg)
+        u_g = tab.export_unique(t)
+        assert (u_g == u_o).all(), f"table {t}: unique set/order"
+        assert (tab.export_inverse(t) == inv_o[:seg.size]).all(), f"table {t}: inverse"
+        slot = np.full(rows[t], -1, np.int32)
+        if len(caches[t]):
+            slot[np.asarray(caches[t], np.int64)] = np.arange(len(caches[t]), dtype=np.int32)
+        hit_o, miss_o = O.partition(u_o, slot)
+        assert (tab.export_hit(t) == hit_o).all(), f"table {t}: hit/miss"
+        assert stats["unique_per_table"][t] == u_o.size
+        assert stats["miss_per_table"][t] == miss_o
+        want_rows = O.synthetic_rows(seed, scale, t, u_o, D)
+        assert (tab.export_rows(t) == want_rows).all(), f"table {t}: gathered rows"
+        if ref is not None and seg.size:
+            a, nc = ref.ref_segment_counts(seg, [0, seg.size], [rows[t]], [np.asarray(caches[t], np.uint32)])
+            assert (a[0], nc[0]) == (u_o.size, miss_o), f"table {t}: counts vs reference"
+        if pooled is not None:
+            if bag_offs is None:
+                bo = np.arange(B + 1, dtype=np.int64) * P
+            else:
+                bo = bag_offs[t * B:(t + 1) * B + 1] - offs[t]
+            _, o64 = O.pool(want_rows, inv_o[:seg.size], bo)
+            np.testing.assert_allclose(pooled[:, t * D:(t + 1) * D], o64, rtol=RTOL, atol=ATOL)
+    return stats
+
+
+@pytest.mark.parametrize("storage", ["hbm", "host"])
+def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage):
+    rows, D, B, P = [1000, 37, 5000, 1], 16, 64, 7
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, [50, 0, 500, 1])]
+    tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
+    seed, scale = 1234, 0.05
+    tab.init_synthetic(seed, scale)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B * P] * len(rows), 77)
+    out = tab.forward(ids, offs, B, P)
+    ids_h = ids.cpu().numpy().view(np.uint32)
+    st = check_batch(ec, tab, ids_h, offs, caches, rows, D, seed, scale, P=P, B=B, out=out, ref=ref)
+    assert st["lookups"] == B * P * len(rows)
+    assert st["model_bytes"] == st["miss_rows"] * D * 4 + st["index_units"] * 4
+
+    # backward: SGD on every unique row, checked through read_rows
+    g = torch.randn(B, len(rows) * D, device="cuda", dtype=torch.float32)
+    lr = 0.25
+    tab.backward(g, lr)
+    torch.cuda.synchronize()
+    gh = g.cpu().numpy()
+    for t in range(len(rows)):
+        seg = ids_h[offs[t]:offs[t + 1]]
+        u, inv = O.dedup(seg)
+        w0 = O.synthetic_rows(seed, scale, t, u, D)
+        _, want = O.backward_sgd(np.ascontiguousarray(gh[:, t * D:(t + 1) * D]), inv[:seg.size],
+                                 np.arange(B + 1, dtype=np.int64) * P, w0, lr)
+        got = tab.read_rows(t, u)
+        np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    # a second batch sees the updated rows and a clean hash table
+    ids2, _ = make_ids(ec, torch, dists, [B * P] * len(rows), 78)
+    tab.forward(ids2, offs, B, P)
+    ids2_h = ids2.cpu().numpy().view(np.uint32)
+    for t in range(len(rows)):
+        seg = ids2_h[offs[t]:offs[t + 1]]
+        u, _ = O.dedup(seg)
+        assert (tab.export_unique(t) == u).all()
+        assert (tab.export_rows(t) == tab.read_rows(t, u)).all()
+    tab.close()
+
+
+def test_csr_bags_empty_bags_and_empty_table(ec, torch):
+    rows, D, B = [300, 50, 1000], 8, 40
+    rng = np.random.default_rng(3)
+    lens = [rng.integers(0, 9, B), np.zeros(B, np.int64), rng.integers(0, 4, B)]
+    lens[0][:5] = 0
+    n = [int(x.sum()) for x in lens]
+    offs = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+    ids_h = np.concatenate([rng.integers(0, r, k) for r, k in zip(rows, n)]).astype(np.uint32)
+    bag = np.concatenate([[0], np.cumsum(np.concatenate(lens))]).astype(np.int64)
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=max(n), max_batch_size=B)
+    tab.init_synthetic(5, 1.0)
+    caches = [np.arange(10), [], np.arange(0, 1000, 3)]
+    tab.place_cache(caches)
+    ids = torch.from_numpy(ids_h.view(np.int32)).cuda()
+    bag_t = torch.from_numpy(bag).cuda()
+    out = tab.forward(ids, offs, B, bag_offsets=bag_t)
+    check_batch(ec, tab, ids_h, offs, caches, rows, D, 5, 1.0, bag_offs=bag, B=B, out=out)
+    assert (out.cpu().numpy()[:, D:2 * D] == 0).all()  # empty table pools to zeros
+    g = torch.ones(B, 3 * D, device="cuda")
+    tab.backward(g, 0.5)
+    torch.cuda.synchronize()
+    tab.close()
+
+
+def test_out_of_range_id_is_a_validation_error(ec, torch):
+    tab = ec.EmbeddingTables([10], 4, max_lookups_per_table=4, max_batch_size=4)
+    tab.init_synthetic(1, 1.0)
+    ids = torch.tensor([1, 2, 10, 3], dtype=torch.int32, device="cuda")
+    tab.forward(ids, [0, 4], 4, 1)
+    with pytest.raises(ec.ValidationError):
+        tab.stats()
+    with pytest.raises(ec.ValidationError):
+        tab.place_cache([[11]])
+    with pytest.raises(ec.ValidationError):
+        tab.forward(ids, [0, 5], 4, 1)
+    tab.close()
+
+
+def test_config1_full_size_counts_and_sets(ec, torch, ref):
+    """Config 1 (BASELINE.json configs[0]): 8 tables x 1M rows, D=64, b=4096,
+    P=20 (n = 81,920 per table); counts bit-exact vs the reference,
+    unique/inverse/hit sets bit-exact vs the oracle, three cache sizes."""
+    T, E, D, B, P = 8, 1_000_000, 64, 4096, 20
+    dist = ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, E, 1.05))
+    tab = ec.EmbeddingTables([E] * T, D, max_lookups_per_table=B * P, max_batch_size=B)
+    tab.init_synthetic(9, 0.01)
+    for k in (0, 10_000, 100_000):
+        caches = [dist.top_ids(k)] * T
+        tab.place_cache(caches)
+        ids, offs = make_ids(ec, torch, [dist] * T, [B * P] * T, 20241101 + k)
+        out = tab.forward(ids, offs, B, P)
+        check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, [E] * T, D, 9, 0.01, P=P, B=B,
+                    out=out, ref=ref)
+    tab.close()
+
+
+def test_config2_kaggle_shape_host_tier(ec, torch, ref):
+    """Config 2 (BASELINE.json configs[1]): 26 Kaggle-cardinality tables, D=16,
+    b=16384, P=1, 256 MB HBM cache placed by global top-k probability, cold
+    rows in pinned host memory.  Counts vs reference, sets vs oracle."""
+    D, B = 16, 16384
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in KAGGLE]
+    ks = ec.place_topk_global(dists, (256 << 20) // (D * 4))
+    caches = [d.top_ids(k) for d, k in zip(dists, ks)]
+    tab = ec.EmbeddingTables(KAGGLE, D, storage="host", max_lookups_per_table=B, max_batch_size=B)
+    tab.init_synthetic(3, 0.1)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B] * 26, 555)
+    out = tab.forward(ids, offs, B, 1)
+    st = check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, KAGGLE, D, 3, 0.1, P=1, B=B,
+                     out=out, ref=ref)
+    assert st["miss_rows"] > 0 and st["hit_rows"] > 0
+    tab.close()
