@@ -1,0 +1,428 @@
+"""Benchmark: embedding lookups/s (+ HBM GB/s, comm bytes/batch vs the
+reference cost model) of the B200 lookup engine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload kaggle|cfg1|tb] [--impl ours|reference]
+
+Workload (default, BASELINE.json configs[1]): 26 Criteo-Kaggle-cardinality
+tables, D=16 fp32, batch 16384 samples x 1 lookup per table, Zipf(1.05) ids
+from the reference's own sampler stream (generated on the GPU, bit-exact),
+256 MiB HBM hot-row cache placed by global top-k probability, cold rows in
+pinned host DRAM.  One step = forward (dedup, hit/miss, gather, pool) +
+backward (grad dedup/scatter-add + SGD into cache and cold tier) of one batch.
+Under torchrun (N > 1) every rank runs its own batch of the same shape
+against row-sharded tables (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KAGGLE = [1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683, 8351593, 3194, 27, 14992,
+          5461306, 10, 5652, 2173, 4, 7046547, 18, 15, 286181, 105, 142572]
+TB = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546, 403346, 10, 2208, 11938, 155,
+      4, 976, 14, 39979771, 25641295, 39664984, 585935, 12972, 108, 36]
+
+WORKLOADS = {
+    "kaggle": dict(rows=KAGGLE, dim=16, batch=16384, pooling=1, alpha=1.05, cache_bytes=256 << 20,
+                   storage="host", name="criteo-kaggle-shaped (BASELINE configs[1])"),
+    "cfg1": dict(rows=[1_000_000] * 8, dim=64, batch=4096, pooling=20, alpha=1.05, cache_bytes=0,
+                 storage="hbm", name="8x1M zipf1.05 D64 b4096 P20 (BASELINE configs[0] shape)"),
+    "tb": dict(rows=TB, dim=64, batch=65536, pooling=1, alpha=1.05, cache_bytes=1 << 30, storage="hbm",
+               name="criteo-terabyte-shaped (BASELINE configs[2])"),
+}
+SEED = 20241101
+N_BATCHES = 4          # distinct batches cycled through the timed steps
+FLUSH_BYTES = 256 << 20  # > 126 MB L2, written between timed steps
+LR = 0.01
+
+
+def batch_seed(rank, j, t):
+    """Ids of table t in batch j on rank r: draws [0, n) of SplitMix64(this)."""
+    from paper_2411_01611_b200 import substream_seed
+    return substream_seed(substream_seed(substream_seed(SEED, rank), j), t)
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ our arm
+def build_tables(ec, torch, wl, rank, world, device):
+    rows, D, B, P = wl["rows"], wl["dim"], wl["batch"], wl["pooling"]
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, wl["alpha"])) for r in rows]
+    budget = wl["cache_bytes"] // (D * 4)
+    ks = ec.place_topk_global(dists, budget) if budget else [0] * len(rows)
+    caches = [d.top_ids(k) for d, k in zip(dists, ks)]
+    tab = ec.EmbeddingTables(rows, D, storage=wl["storage"], rank=rank, world=world,
+                             max_lookups_per_table=B * P, max_batch_size=B, device=device)
+    tab.init_synthetic(SEED, 0.05)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [ec.EmbeddingTables.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        tab.attach_comm(uid[0])
+    tab.place_cache(caches)
+    return tab, dists, caches, ks
+
+
+def gen_batches(ec, torch, dists, wl, rank, nb):
+    B, P, T = wl["batch"], wl["pooling"], len(dists)
+    n = B * P
+    ids = torch.empty((nb, T * n), dtype=torch.int32, device="cuda")
+    for j in range(nb):
+        for t, d in enumerate(dists):
+            ec.DiscreteSampler(d, torch.cuda.current_device()).sample_into(
+                ids[j].data_ptr() + 4 * n * t, batch_seed(rank, j, t), 0, n)
+    torch.cuda.synchronize()
+    offs = (np.arange(T + 1, dtype=np.int64) * n).tolist()
+    return ids, offs
+
+
+def phase_bytes(st, wl, T):
+    """Algorithmic bytes per step by phase (SURVEY §8d definitions; i = s = 4 B)."""
+    D, B, P = wl["dim"], wl["batch"], wl["pooling"]
+    n = st["lookups"]
+    U, H, M = st["unique_rows"], st["hit_rows"], st["miss_rows"]
+    row = D * 4
+    hbm_rows = U if wl["storage"] == "hbm" else H
+    host_rows = 0 if wl["storage"] == "hbm" else M
+    return {
+        "dedup": n * 4 + n * 4 + U * 4,
+        "partition": U * 4 * 3,
+        "gather_hbm": hbm_rows * row * 2 + U * 4,
+        "gather_host": host_rows * row * 2 + host_rows * 4,
+        "pool": n * 4 + n * row + B * T * row,
+        "grad_scatter": U * row + B * T * row + n * 4 + n * row,
+        "sgd_apply": U * row * 3 + U * 4,
+    }
+
+
+def run_ours(args, wl):
+    import torch
+    import paper_2411_01611_b200 as ec
+    rank, world, local = env_rank()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
+    t0 = time.time()
+    tab, dists, caches, ks = build_tables(ec, torch, wl, rank, world, local)
+    ids, offs = gen_batches(ec, torch, dists, wl, rank, N_BATCHES)
+    setup_s = time.time() - t0
+    out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(j):
+        o = tab.forward(ids[j], offs, B, P, out=out)
+        tab.backward(o, LR)  # loss = 0.5*||pooled||^2  ->  d loss / d pooled = pooled
+
+    # per-batch stats (deterministic per batch; outside any timed region)
+    stats = []
+    for j in range(N_BATCHES):
+        step(j)
+        stats.append(tab.stats(per_table=True))
+    for w in range(args.warmup):
+        step(w % N_BATCHES)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            starts[k].record(stream)
+            step(k % N_BATCHES)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(step_ms) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    lookups_per_step = T * B * P
+    value = lookups_per_step * world / (ms * 1e-3)
+
+    # ---- phase profile pass (same steps, CUDA events per phase, live)
+    tab.profile(True)
+    tab.profile_read(reset=True)
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        step(k % N_BATCHES)
+    torch.cuda.synchronize()
+    prof = tab.profile_read(reset=True)
+    tab.profile(False)
+    launches_per_step = prof["launches"] / args.steps
+
+    # ---- e2e through the public API with host buffers (pinned), K steps
+    host_ids = ids.cpu().pin_memory()
+    dev_ids = torch.empty_like(ids[0])
+    counters = None
+    e2e_start = torch.cuda.Event(enable_timing=True)
+    e2e_end = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e2e_start.record(stream)
+    for k in range(args.steps):
+        dev_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
+        o = tab.forward(dev_ids, offs, B, P, out=out)
+        tab.backward(o, LR)
+        counters = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
+    e2e_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e2e_start.elapsed_time(e2e_end) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel + whole-step algorithmic traffic
+    import statistics as S
+    pb = [phase_bytes(s, wl, T) for s in stats]
+    mean_bytes = {k: S.mean(p[k] for p in pb) for k in pb[0]}
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    phases = {}
+    for name, tot in prof["ms"].items():
+        calls = prof["calls"][name]
+        if not calls:
+            continue
+        per = tot / calls
+        b = mean_bytes.get(name)
+        phases[name] = {"ms_per_call": round(per, 5), "share": None,
+                        "alg_bytes": b, "gbs": round(b / (per * 1e-3) / 1e9, 1) if b else None}
+    tot_ms = sum(p["ms_per_call"] for p in phases.values())
+    for p in phases.values():
+        p["share"] = round(p["ms_per_call"] / tot_ms, 3)
+    hbm_phases = {k: v for k, v in phases.items() if k not in ("gather_host", "exchange")}
+    dom = max(hbm_phases, key=lambda k: hbm_phases[k]["ms_per_call"])
+    dom_gbs = hbm_phases[dom]["gbs"]
+    step_alg = sum(mean_bytes.values())
+
+    s0 = stats[0]
+    res = {
+        "metric": "embedding lookups/sec (fwd+bwd step)",
+        "value": round(value, 1),
+        "unit": "lookups/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32 rows, uint32 ids",
+        "data": "synthetic: Zipf(1.05) ids from the reference sampler stream (GPU K0, bit-exact), synthetic rows",
+        "config": {"workload": wl["name"], "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
+                   "cache_rows": int(sum(ks)), "cache_bytes": int(sum(ks)) * D * 4, "cold_tier": wl["storage"],
+                   "l2": "flushed between timed steps (256 MiB write outside the per-step events)",
+                   "step": "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD)",
+                   "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
+        "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
+                "ms_per_step": round(e2e_ms, 5),
+                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int(T * 8 * 2 + 72)},
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": round(dom_gbs / peak, 4), "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+        "step_alg_bytes": int(step_alg),
+        "step_alg_gbs": round(step_alg / (ms * 1e-3) / 1e9, 1),
+        "phases": phases,
+        "comm": {"model_rows_per_batch": s0["miss_rows"], "model_bytes_per_batch": s0["model_bytes"],
+                 "unique_rows_per_batch": s0["unique_rows"], "hit_rows_per_batch": s0["hit_rows"],
+                 "wire_bytes_per_batch": s0["wire_bytes"]},
+        "setup_s": round(setup_s, 1),
+    }
+    res["clocks"] = clk.summary()
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(ids.cpu().numpy().view(np.uint32), offs, wl, caches, args.cpu_seconds)
+        res["comm"]["reference_model_rows_per_batch"] = res["cpu_baseline"].pop("model_rows_batch0")
+        res["comm"]["equal_to_reference"] = res["comm"]["reference_model_rows_per_batch"] == s0["miss_rows"]
+    if rank == 0:
+        print(json.dumps(res))
+    tab.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------ reference
+def _ref_caches(wl):
+    D = wl["dim"]
+    budget = wl["cache_bytes"] // (D * 4)
+    if not budget:
+        return [np.zeros(0, np.uint32) for _ in wl["rows"]]
+    # same placement rule as ours; parametric Zipf ranks == ids, so top-k = arange(k)
+    import heapq  # global top-k over per-table non-increasing probabilities
+    import oracle as O
+    ks = [0] * len(wl["rows"])
+    ranked = [O.RefDist.parametric("zipf", r, wl["alpha"]).export()[0] for r in wl["rows"]]
+    heap = [(-p[0], t) for t, p in enumerate(ranked)]
+    heapq.heapify(heap)
+    for _ in range(min(budget, sum(wl["rows"]))):
+        _, t = heapq.heappop(heap)
+        ks[t] += 1
+        if ks[t] < len(ranked[t]):
+            heapq.heappush(heap, (-ranked[t][ks[t]], t))
+    return [np.arange(k, dtype=np.uint32) for k in ks]
+
+
+def cpu_baseline(ids_host, offs, wl, caches, seconds, threads=1):
+    """The reference's own dedup + hit/miss counting (simulate_epoch(Trace{d=1}, n, C_t),
+    core/src/simulator.cpp:222-273) over the same batches, via oracle/_ref."""
+    import oracle as O
+    T = len(wl["rows"])
+    caches = [np.ascontiguousarray(c, dtype=np.uint32) for c in caches]
+    nb = ids_host.shape[0]
+    done = 0
+    model_rows0 = None
+    t0 = time.perf_counter()
+    while True:
+        j = done % nb
+        _, nc = O.ref_segment_counts(ids_host[j], offs, wl["rows"], caches, threads=threads, want_all=False)
+        if done == 0:
+            model_rows0 = int(nc.sum())
+        done += 1
+        if time.perf_counter() - t0 >= seconds and done >= 1:
+            break
+    dt = time.perf_counter() - t0
+    look = done * T * wl["batch"] * wl["pooling"]
+    return {"value": round(look / dt, 1), "unit": "lookups/s", "cores": threads, "kind": "reference",
+            "sample": f"{done} batches ({look} lookups) of this workload through the reference's "
+                      f"simulate_epoch(Trace{{d=1}}, n, C_t) per table (dedup + hit/miss counts only; the "
+                      f"reference has no gather/pool/backward), {dt:.1f} s",
+            "model_rows_batch0": model_rows0}
+
+
+def run_reference(args, wl):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle as O
+    T, B, P = len(wl["rows"]), wl["batch"], wl["pooling"]
+    n = B * P
+    dists = [O.RefDist.parametric("zipf", r, wl["alpha"]) for r in wl["rows"]]
+    caches = _ref_caches(wl)
+    # ids: the reference's own sampler (sample_batch) with the same seeds as our arm
+    ss = O.ref_substream_seed
+
+    def bseed(j, t):
+        return ss(ss(ss(SEED, 0), j), t)
+    nb = min(N_BATCHES, max(1, args.steps))
+    ids = np.empty((nb, T * n), np.uint32)
+    for j in range(nb):
+        for t, d in enumerate(dists):
+            ids[j, t * n:(t + 1) * n] = O.ref_sample_batch(d, B, P, bseed(j, t))
+    offs = (np.arange(T + 1, dtype=np.int64) * n).tolist()
+    threads = os.cpu_count() or 1
+    for w in range(args.warmup):
+        O.ref_segment_counts(ids[w % nb], offs, wl["rows"], caches, threads=threads, want_all=False)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        O.ref_segment_counts(ids[k % nb], offs, wl["rows"], caches, threads=threads, want_all=False)
+    dt = time.perf_counter() - t0
+    ms = dt * 1e3 / args.steps
+    value = T * n / (ms * 1e-3)
+    res = {"impl": "reference", "metric": "embedding lookups/sec (fwd+bwd step)", "value": round(value, 1),
+           "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "uint32 ids", "data": "synthetic: Zipf(1.05) ids from the reference's sample_batch",
+           "config": {"workload": wl["name"], "tables": T, "batch_per_gpu": B, "pooling": P,
+                      "cache_rows": int(sum(c.size for c in caches))},
+           "cpu_baseline": {"value": round(value, 1), "unit": "lookups/s", "cores": threads, "kind": "reference",
+                            "sample": f"{args.steps} batches through the reference's simulate_epoch(Trace{{d=1}}, n, "
+                                      f"C_t), one table per thread; dedup + hit/miss counting is all the reference "
+                                      f"implements of this path"},
+           "e2e": {"value": round(value, 1), "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="kaggle")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -231,6 +231,15 @@ int ec_tables_create(const ec_tables_config* cfg, ec_tables* out);
 void ec_tables_destroy(ec_tables t);
 /* bytes of device / pinned-host memory held */
 int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
+/* Per-phase CUDA-event timing of ec_lookup_fwd/bwd (events on the launching
+ * streams).  Phases: 0 dedup (K1), 1 hit/miss partition (K2), 2 HBM gather
+ * (K3), 3 pinned-host miss gather (K3, side stream), 4 exchange (K4),
+ * 5 pool (K5), 6 grad scatter (K6a), 7 SGD apply (K6b).  profile_read
+ * returns accumulated ms and call counts per phase (8 entries each) and the
+ * number of kernels the engine launched; reset != 0 clears them. */
+int ec_tables_profile(ec_tables t, int enable);
+int ec_tables_profile_read(ec_tables t, double* ms_host, uint64_t* calls_host, uint64_t* launches,
+                           int reset);
 /* Deterministic synthetic weights: row (t, id) element c =
  *   scale * (2 * ((mix64(seed + 0x9E3779B97F4A7C15 * ((t << 40) ^ (id * D + c))) >> 40) * 2^-24) - 1)
  * in fp32; every rank can evaluate any row, so shards and replicated cache

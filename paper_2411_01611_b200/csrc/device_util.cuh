@@ -11,6 +11,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr unsigned long long kEmptySlot = ~0ull;  // packed (id << 32 | value); ids < 2^32-1
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kRankTag = 0x80000000u;  // low word holds a (tagged) unique index
+constexpr uint32_t kInvalidSlot = 0xFFFFFFFFu;  // lookup whose id is out of range
 
 // Fibonacci hashing: top `bits` bits of id * 2^32/phi.  Consecutive ids (the
 // hot ranks of a parametric distribution) land far apart.

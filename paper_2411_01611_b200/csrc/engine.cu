@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     if (live && leader == lane_id()) h = hash_insert(t.hash, t.mask, t.shift, id, static_cast<uint32_t>(p - t.base));
     h = __shfl_sync(kFull, h, leader);
     if (live) slot_of[p] = h;
+    else if (off < tile.count) slot_of[p] = kInvalidSlot;  // out-of-range id: skipped downstream
   }
 }
 
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
 // minimum position is p.
 __device__ __forceinline__ bool is_first(const TableDev& t, const uint32_t* slot_of, int64_t p, uint32_t* h) {
   *h = slot_of[p];
-  return static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
+  return *h != kInvalidSlot && static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
 }
 
 __global__ void __launch_bounds__(kThreads) k_count(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_inverse(const Tile* __restrict__ t
     const uint32_t off = j * kThreads + threadIdx.x;
     if (off < tile.count) {
       const int64_t p = tile.start + off;
-      inv[p] = static_cast<uint32_t>(__ldcg(t.hash + slot_of[p])) & ~kRankTag;
+      const uint32_t h = slot_of[p];
+      inv[p] = h == kInvalidSlot ? kInvalidSlot : static_cast<uint32_t>(__ldcg(t.hash + h)) & ~kRankTag;
     }
   }
 }
@@ -347,6 +349,12 @@ __device__ __forceinline__ void bag_range(const TableDev* td, const int64_t* bag
   }
 }
 
+// Row u's float4 #c of the compact unique-row buffer; invalid lookups read 0.
+__device__ __forceinline__ float4 load_row(const float* urows, uint32_t u, int D, int c) {
+  if (u == kInvalidSlot) return make_float4(0.f, 0.f, 0.f, 0.f);
+  return ldg4(urows + static_cast<int64_t>(u) * D + c * 4);
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
                                                    const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
@@ -366,14 +374,13 @@ __global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ 
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t i = lo;
     for (; i + 4 <= hi; i += 4) {  // 4 rows in flight, summed in lookup order
-      const uint32_t u0 = inv[i], u1 = inv[i + 1], u2 = inv[i + 2], u3 = inv[i + 3];
-      const float4 a = ldg4(urows + static_cast<int64_t>(u0) * D + m.c * 4);
-      const float4 b = ldg4(urows + static_cast<int64_t>(u1) * D + m.c * 4);
-      const float4 c = ldg4(urows + static_cast<int64_t>(u2) * D + m.c * 4);
-      const float4 d = ldg4(urows + static_cast<int64_t>(u3) * D + m.c * 4);
+      const float4 a = load_row(urows, inv[i], D, m.c);
+      const float4 b = load_row(urows, inv[i + 1], D, m.c);
+      const float4 c = load_row(urows, inv[i + 2], D, m.c);
+      const float4 d = load_row(urows, inv[i + 3], D, m.c);
       acc = add4(add4(add4(add4(acc, a), b), c), d);
     }
-    for (; i < hi; ++i) acc = add4(acc, ldg4(urows + static_cast<int64_t>(inv[i]) * D + m.c * 4));
+    for (; i < hi; ++i) acc = add4(acc, load_row(urows, inv[i], D, m.c));
     st4(out + (static_cast<int64_t>(s) * T + t) * D + m.c * 4, acc);
   }
 }
@@ -403,8 +410,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const TableDev* __restrict
     int64_t lo, hi;
     bag_range(td, bag_off, T, B, P, s, t, &lo, &hi);
     const float4 gv = ld_stream4(grad + (static_cast<int64_t>(s) * T + t) * D + m.c * 4);
-    for (int64_t i = lo; i < hi; ++i)
-      atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(inv[i]) * D + m.c * 4), gv);
+    for (int64_t i = lo; i < hi; ++i) {
+      const uint32_t u = inv[i];
+      if (u != kInvalidSlot) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + m.c * 4), gv);
+    }
   }
 }
 
@@ -763,32 +772,47 @@ void Engine::launch_row_kernels_fwd(cudaStream_t st) {
     // host misses on the side stream, overlapping the HBM hit gather
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    PhaseScope ph(prof, kPhaseGatherHost, side);
     k_gather_host<VEC, 4><<<grid, kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank, world);
-    EC_LAUNCH();
+    launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
+  {
+  PhaseScope ph(prof, kPhaseGather, st);
   k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, cache.p, urows.p,
                                               storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
-  EC_LAUNCH();
-  if (world > 1) exchange_fwd(st);
+  launched();
+  }
+  if (world > 1) {
+    PhaseScope ph(prof, kPhaseExchange, st);
+    exchange_fwd(st);
+  }
   if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  PhaseScope ph(prof, kPhasePool, st);
   k_pool<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, inv.p,
                                          urows.p, out_ptr);
-  EC_LAUNCH();
+  launched();
 }
 
 template <int VEC>
 void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st) {
   const int grid = persistent_grid(device);
+  {
+  PhaseScope ph(prof, kPhaseScatter, st);
   k_zero<<<grid, kThreads, 0, st>>>(reinterpret_cast<float4*>(ugrad.p), ctr.p, T, VEC);
-  EC_LAUNCH();
+  launched();
   k_scatter<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
                                             inv.p, grad, ugrad.p);
-  EC_LAUNCH();
-  if (world > 1) exchange_bwd(lr, st);
+  launched();
+  }
+  if (world > 1) {
+    PhaseScope ph(prof, kPhaseExchange, st);
+    exchange_bwd(lr, st);
+  }
+  PhaseScope ph(prof, kPhaseApply, st);
   k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
                                              rank, world);
-  EC_LAUNCH();
+  launched();
 }
 
 #define EC_DISPATCH_VEC(FN, ...)                                                  \
@@ -819,22 +843,28 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   bag_off = b.bag_offsets_dev;
   out_ptr = out;
   const int grid = persistent_grid(device);
+  {
+  PhaseScope ph(prof, kPhaseDedup, st);
   if (ntiles) {
     k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, counters(ctr.p, T).err);
-    EC_LAUNCH();
+    launched();
     k_count<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, tile_cnt.p);
-    EC_LAUNCH();
+    launched();
   }
   k_scan<<<1, 1024, 0, st>>>(tile_cnt.p, ntiles, first_tile.p, static_cast<int>(T), ctr.p);
-  EC_LAUNCH();
+  launched();
   if (ntiles) {
     k_emit<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, tile_cnt.p, uniq.p, uslot.p, utab.p);
-    EC_LAUNCH();
+    launched();
     k_inverse<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p);
-    EC_LAUNCH();
+    launched();
   }
+  }
+  {
+  PhaseScope ph(prof, kPhasePartition, st);
   k_partition<<<grid, kThreads, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, uslot.p, usrc.p, missq.p);
-  EC_LAUNCH();
+  launched();
+  }
   EC_DISPATCH_VEC(launch_row_kernels_fwd, st);
   have_fwd = true;
 }
@@ -858,6 +888,49 @@ void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
     EC_CUDA(cudaMemset(counters(ctr.p, T).err, 0, sizeof(int)));
     invalid("lookup id out of range of its table in the last batch");
   }
+}
+
+
+// ------------------------------------------------------------ profiling
+PhaseScope::PhaseScope(Profiler& p, int phase, cudaStream_t st) : p_(p), phase_(phase), st_(st) {
+  if (!p_.on) return;
+  a_ = p_.take();
+  EC_CUDA(cudaEventRecord(a_, st_));
+}
+PhaseScope::~PhaseScope() {
+  if (!p_.on || !a_) return;
+  cudaEvent_t b = p_.take();
+  cudaEventRecord(b, st_);
+  p_.recs.push_back({phase_, a_, b});
+}
+cudaEvent_t Profiler::take() {
+  if (free_.empty()) {
+    cudaEvent_t e;
+    EC_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = free_.back();
+  free_.pop_back();
+  return e;
+}
+void Profiler::collect() {
+  for (const Rec& r : recs) {
+    EC_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    EC_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    ms_[r.phase] += ms;
+    calls_[r.phase] += 1;
+    free_.push_back(r.a);
+    free_.push_back(r.b);
+  }
+  recs.clear();
+}
+Profiler::~Profiler() {
+  for (auto& r : recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : free_) cudaEventDestroy(e);
 }
 
 }  // namespace ec
@@ -895,6 +968,32 @@ void ec_tables_destroy(ec_tables t) {
   cudaSetDevice(t->e.device);
   cudaDeviceSynchronize();
   delete t;
+}
+
+int ec_tables_profile(ec_tables t, int enable) {
+  return guard([&] {
+    Engine& e = E(t);
+    use_device(e.device);
+    e.prof.collect();
+    e.prof.on = enable != 0;
+  });
+}
+
+int ec_tables_profile_read(ec_tables t, double* ms, uint64_t* calls, uint64_t* launches, int reset) {
+  return guard([&] {
+    Engine& e = E(t);
+    use_device(e.device);
+    e.prof.collect();
+    for (int i = 0; i < kNumPhases; ++i) {
+      if (ms) ms[i] = e.prof.ms_[i];
+      if (calls) calls[i] = e.prof.calls_[i];
+    }
+    if (launches) *launches = e.launches;
+    if (reset) {
+      for (int i = 0; i < kNumPhases; ++i) e.prof.ms_[i] = 0.0, e.prof.calls_[i] = 0;
+      e.launches = 0;
+    }
+  });
 }
 
 int ec_tables_memory(ec_tables t, uint64_t* dev, uint64_t* host) {

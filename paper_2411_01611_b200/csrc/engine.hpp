@@ -36,6 +36,34 @@ inline size_t counters_size(int T) { return 3 * static_cast<size_t>(T) + 3; }
 
 struct Exchange;  // exchange.cu
 
+enum { kPhaseDedup = 0, kPhasePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange, kPhasePool,
+       kPhaseScatter, kPhaseApply, kNumPhases };
+
+// Optional per-phase CUDA-event timing on the launching streams.
+struct Profiler {
+  struct Rec {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  bool on = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> free_;
+  double ms_[kNumPhases] = {};
+  uint64_t calls_[kNumPhases] = {};
+  cudaEvent_t take();
+  void collect();
+  ~Profiler();
+};
+
+struct PhaseScope {
+  PhaseScope(Profiler& p, int phase, cudaStream_t st);
+  ~PhaseScope();
+  Profiler& p_;
+  int phase_;
+  cudaStream_t st_;
+  cudaEvent_t a_ = nullptr;
+};
+
 struct Engine {
   int device = 0;
   uint32_t T = 0, D = 0;
@@ -79,6 +107,13 @@ struct Engine {
 
   cudaStream_t side = nullptr;
   cudaEvent_t ev_part = nullptr, ev_side = nullptr;
+
+  Profiler prof;
+  uint64_t launches = 0;
+  void launched() {
+    EC_LAUNCH();
+    ++launches;
+  }
 
   Exchange* ex = nullptr;
   uint64_t last_wire_rows = 0, last_wire_bytes = 0;

@@ -65,6 +65,21 @@ class EmbeddingTables:
         check(N.lib().ec_tables_memory(self._h, C.byref(d), C.byref(h)))
         return {"device_bytes": d.value, "host_bytes": h.value}
 
+    PHASES = ("dedup", "partition", "gather_hbm", "gather_host", "exchange", "pool", "grad_scatter", "sgd_apply")
+
+    def profile(self, enable: bool = True):
+        """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""
+        check(N.lib().ec_tables_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self, reset: bool = True):
+        ms = np.zeros(8, np.float64)
+        calls = np.zeros(8, np.uint64)
+        launches = C.c_uint64()
+        check(N.lib().ec_tables_profile_read(self._h, ms.ctypes.data, calls.ctypes.data, C.byref(launches),
+                                             1 if reset else 0))
+        return {"ms": dict(zip(self.PHASES, ms.tolist())), "calls": dict(zip(self.PHASES, calls.tolist())),
+                "launches": int(launches.value)}
+
     def init_synthetic(self, seed: int, scale: float = 0.05):
         check(N.lib().ec_tables_init_synthetic(self._h, seed, scale, _stream_ptr(self.torch, self.device)))
 
