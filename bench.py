@@ -98,7 +98,7 @@ class ClockSampler:
         sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if "Active" in r[5 + i]})
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
 
@@ -162,6 +162,8 @@ def run_ours(args, wl):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    # a non-default stream, so the engine can capture and replay CUDA graphs
+    torch.cuda.set_stream(torch.cuda.Stream())
     T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
     t0 = time.time()
     tab, dists, caches, ks = build_tables(ec, torch, wl, rank, world, local)

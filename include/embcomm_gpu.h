@@ -238,6 +238,12 @@ int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
  * returns accumulated ms and call counts per phase (8 entries each) and the
  * number of kernels the engine launched; reset != 0 clears them. */
 int ec_tables_profile(ec_tables t, int enable);
+/* CUDA-graph replay of the per-batch kernel sequence (default on): the first
+ * ec_lookup_fwd/bwd with a given (indices, bag offsets, out) / (grad, lr) on a
+ * capturable stream is captured, later ones replay it.  Off, or on the legacy
+ * stream, under profiling, inside an outer capture or with world > 1, kernels
+ * are launched directly. */
+int ec_tables_use_graphs(ec_tables t, int enable);
 int ec_tables_profile_read(ec_tables t, double* ms_host, uint64_t* calls_host, uint64_t* launches,
                            int reset);
 /* Deterministic synthetic weights: row (t, id) element c =

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                                                     const int32_t* __restrict__ usrc, const float* __restrict__ urows,
                                                     const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
-                                                    int rank, int world) {
+                                                    int misses_local, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
       float* dst = nullptr;
       if (s >= 0) {
         dst = cache + static_cast<int64_t>(s) * D;
-      } else {
+      } else if (misses_local) {
         const uint32_t id = uniq[g];
         if (static_cast<int>(id % world) == rank) dst = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
       }
@@ -448,6 +448,35 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
       const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
       st4(dst + m.c * 4, make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+    }
+  }
+}
+
+// SGD for cold rows held in pinned host memory (miss queue, side stream).
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                         const uint32_t* __restrict__ missq,
+                                                         const uint32_t* __restrict__ uniq,
+                                                         const uint16_t* __restrict__ utab, const float* __restrict__ urows,
+                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      if (q >= nm) continue;
+      const uint32_t g = missq[q];
+      const uint32_t id = uniq[g];
+      if (static_cast<int>(id % world) != rank) continue;
+      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
+      st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4,
+          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
     }
   }
 }
@@ -531,6 +560,7 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
 
 // ------------------------------------------------------------ host side
 static int persistent_grid(int device) { return sm_count(device) * 8; }
+int Engine::host_grid() const { return sm_count(device) * 2; }
 
 static uint32_t log2_ceil(uint64_t x) {
   uint32_t l = 0;
@@ -539,6 +569,7 @@ static uint32_t log2_ceil(uint64_t x) {
 }
 
 Engine::~Engine() {
+  clear_graphs();
   if (ev_part) cudaEventDestroy(ev_part);
   if (ev_side) cudaEventDestroy(ev_side);
   if (side) cudaStreamDestroy(side);
@@ -694,6 +725,7 @@ void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
     EC_LAUNCH();
   }
   EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
+  clear_graphs();
   cache_k_total = all_ids.size();
   cache_k.resize(T);
   for (uint32_t t = 0; t < T; ++t) cache_k[t] = koff[t + 1] - koff[t];
@@ -742,6 +774,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   bool same = have_geom && b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed;
   for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
   if (same) return;
+  clear_graphs();
   geom_off.assign(b.table_offsets_host, b.table_offsets_host + T + 1);
   std::vector<Tile> tl;
   std::vector<int> ft(T + 1);
@@ -773,7 +806,10 @@ void Engine::launch_row_kernels_fwd(cudaStream_t st) {
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
     PhaseScope ph(prof, kPhaseGatherHost, side);
-    k_gather_host<VEC, 4><<<grid, kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank, world);
+    // few CTAs: the host link, not the SMs, bounds this kernel, and a full
+    // persistent grid would hold every SM slot while it waits on PCIe reads
+    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                               world);
     launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
@@ -810,9 +846,19 @@ void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st
     exchange_bwd(lr, st);
   }
   PhaseScope ph(prof, kPhaseApply, st);
+  const bool host = storage == EC_STORAGE_HOST;
+  if (host) {  // cold rows written back over the host link on the side stream
+    EC_CUDA(cudaEventRecord(ev_part, st));
+    EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p,
+                                                              lr, rank, world);
+    launched();
+    EC_CUDA(cudaEventRecord(ev_side, side));
+  }
   k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
-                                             rank, world);
+                                             host ? 0 : 1, rank, world);
   launched();
+  if (host) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
 }
 
 #define EC_DISPATCH_VEC(FN, ...)                                                  \
@@ -842,11 +888,65 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   set_geometry(b, st);
   bag_off = b.bag_offsets_dev;
   out_ptr = out;
+  const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
+  run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
+  have_fwd = true;
+}
+
+// Replay a captured CUDA graph of the per-batch kernel sequence when the
+// stream allows it (launch gaps dominate these short kernels); capture on
+// first use of a (kind, pointers) key.  Profiling, the legacy stream, an
+// outer capture and the multi-rank exchange (host syncs) launch directly.
+template <class F>
+void Engine::run_maybe_graphed(const GraphKey& key, cudaStream_t st, F&& enqueue) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  bool direct = !use_graphs || prof.on || world > 1 || st == nullptr || st == cudaStreamLegacy ||
+                st == cudaStreamPerThread;
+  if (!direct) {
+    EC_CUDA(cudaStreamIsCapturing(st, &cs));
+    direct = cs != cudaStreamCaptureStatusNone;
+  }
+  if (direct) {
+    enqueue();
+    return;
+  }
+  auto it = graphs.find(key);
+  if (it == graphs.end()) {
+    if (graphs.size() >= 64) clear_graphs();
+    const uint64_t before = launches;
+    cudaGraph_t g = nullptr;
+    EC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      launches = before;
+      throw;
+    }
+    EC_CUDA(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    EC_CUDA(e);
+    it = graphs.emplace(key, GraphEntry{ex, launches - before}).first;
+    launches = before;
+  }
+  EC_CUDA(cudaGraphLaunch(it->second.exec, st));
+  launches += it->second.kernels;
+}
+
+void Engine::clear_graphs() {
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+  graphs.clear();
+}
+
+void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
   const int grid = persistent_grid(device);
   {
   PhaseScope ph(prof, kPhaseDedup, st);
   if (ntiles) {
-    k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, counters(ctr.p, T).err);
+    k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, counters(ctr.p, T).err);
     launched();
     k_count<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, tile_cnt.p);
     launched();
@@ -854,7 +954,7 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   k_scan<<<1, 1024, 0, st>>>(tile_cnt.p, ntiles, first_tile.p, static_cast<int>(T), ctr.p);
   launched();
   if (ntiles) {
-    k_emit<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, b.indices_dev, slot_of.p, tile_cnt.p, uniq.p, uslot.p, utab.p);
+    k_emit<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, tile_cnt.p, uniq.p, uslot.p, utab.p);
     launched();
     k_inverse<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p);
     launched();
@@ -866,14 +966,16 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   launched();
   }
   EC_DISPATCH_VEC(launch_row_kernels_fwd, st);
-  have_fwd = true;
 }
 
 void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   if (!have_fwd) invalid("ec_lookup_bwd needs a preceding ec_lookup_fwd");
   if (!grad) invalid("null gradient");
   use_device(device);
-  EC_DISPATCH_VEC(launch_row_kernels_bwd, grad, lr, st);
+  uint32_t lr_bits;
+  std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
+  const GraphKey key{1, grad, bag_off, out_ptr, lr_bits};
+  run_maybe_graphed(key, st, [&] { EC_DISPATCH_VEC(launch_row_kernels_bwd, grad, lr, st); });
 }
 
 void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
@@ -993,6 +1095,14 @@ int ec_tables_profile_read(ec_tables t, double* ms, uint64_t* calls, uint64_t* l
       for (int i = 0; i < kNumPhases; ++i) e.prof.ms_[i] = 0.0, e.prof.calls_[i] = 0;
       e.launches = 0;
     }
+  });
+}
+
+int ec_tables_use_graphs(ec_tables t, int enable) {
+  return guard([&] {
+    Engine& e = E(t);
+    e.use_graphs = enable != 0;
+    if (!e.use_graphs) e.clear_graphs();
   });
 }
 

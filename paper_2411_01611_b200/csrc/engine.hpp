@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "common.hpp"
@@ -64,6 +66,22 @@ struct PhaseScope {
   cudaEvent_t a_ = nullptr;
 };
 
+struct GraphKey {
+  int kind;  // 0 forward, 1 backward
+  const void* a;
+  const void* b;
+  const void* c;
+  uint32_t lr_bits;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(kind, a, b, c, lr_bits) < std::tie(o.kind, o.a, o.b, o.c, o.lr_bits);
+  }
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  uint64_t kernels;
+};
+
 struct Engine {
   int device = 0;
   uint32_t T = 0, D = 0;
@@ -115,12 +133,19 @@ struct Engine {
     ++launches;
   }
 
+  bool use_graphs = true;
+  std::map<GraphKey, GraphEntry> graphs;
+  template <class F> void run_maybe_graphed(const GraphKey& key, cudaStream_t st, F&& enqueue);
+  void clear_graphs();
+  void enqueue_forward(const uint32_t* indices, cudaStream_t st);
+
   Exchange* ex = nullptr;
   uint64_t last_wire_rows = 0, last_wire_bytes = 0;
 
   ~Engine();
   void create(const ec_tables_config& c);
   uint64_t device_bytes() const;
+  int host_grid() const;
   void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
   void fill_cache(cudaStream_t st, bool from_store);
   void place_cache(const uint32_t* const* ids, const uint64_t* k);

@@ -67,6 +67,10 @@ class EmbeddingTables:
 
     PHASES = ("dedup", "partition", "gather_hbm", "gather_host", "exchange", "pool", "grad_scatter", "sgd_apply")
 
+    def use_graphs(self, enable: bool = True):
+        """CUDA-graph replay of forward/backward (needs a non-default stream)."""
+        check(N.lib().ec_tables_use_graphs(self._h, 1 if enable else 0))
+
     def profile(self, enable: bool = True):
         """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""
         check(N.lib().ec_tables_profile(self._h, 1 if enable else 0))

@@ -70,12 +70,21 @@ def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=
     return stats
 
 
-@pytest.mark.parametrize("storage", ["hbm", "host"])
-def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage):
+@pytest.mark.parametrize("storage,graphs", [("hbm", False), ("host", False), ("hbm", True), ("host", True)])
+def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs):
+    if graphs:  # CUDA-graph capture/replay needs a non-default stream
+        with torch.cuda.stream(torch.cuda.Stream()):
+            _small_fixed_pooling(ec, torch, ref, storage, True)
+    else:
+        _small_fixed_pooling(ec, torch, ref, storage, False)
+
+
+def _small_fixed_pooling(ec, torch, ref, storage, graphs):
     rows, D, B, P = [1000, 37, 5000, 1], 16, 64, 7
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
     caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, [50, 0, 500, 1])]
     tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
+    tab.use_graphs(graphs)
     seed, scale = 1234, 0.05
     tab.init_synthetic(seed, scale)
     tab.place_cache(caches)
@@ -109,6 +118,13 @@ def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage):
         u, _ = O.dedup(seg)
         assert (tab.export_unique(t) == u).all()
         assert (tab.export_rows(t) == tab.read_rows(t, u)).all()
+    # same buffers, new contents: a replayed graph must see the new ids
+    ids.copy_(ids2)
+    tab.forward(ids, offs, B, P)
+    for t in range(len(rows)):
+        u, inv = O.dedup(ids2_h[offs[t]:offs[t + 1]])
+        assert (tab.export_unique(t) == u).all()
+        assert (tab.export_inverse(t) == inv[:B * P]).all()
     tab.close()
 
 
