@@ -75,6 +75,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -100,7 +103,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "window": "warm-up (>=0.5 s) + timed steps"}
 
 
 # ------------------------------------------------------------ our arm
@@ -182,18 +185,26 @@ def run_ours(args, wl):
     for j in range(N_BATCHES):
         step(j)
         stats.append(tab.stats(per_table=True))
-    for w in range(args.warmup):
-        step(w % N_BATCHES)
-    torch.cuda.synchronize()
-
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    # ---- timed region: K steps, L2 flushed between steps (outside the events).
+    # Clocks are sampled from the start of warm-up (which runs >= 0.5 s so the
+    # 100 ms nvidia-smi sampler sees the GPU under this load) to the end of
+    # the timed steps.
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        t_w = time.time()
+        w = 0
+        while w < args.warmup or time.time() - t_w < 0.5:
+            flush.fill_(float(w))
+            step(w % N_BATCHES)
+            w += 1
+            if w % 50 == 0:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):

@@ -1,13 +1,16 @@
 // Lookup engine: row-sharded fp32 tables, replicated HBM hot-row cache, and
 // the per-batch forward/backward pipeline (K1..K6).
 //
-//   forward  K1 dedup      k_insert -> k_count -> k_scan -> k_emit -> k_inverse
-//            K2 partition  k_partition  (hit/miss per unique, miss queue, hash reset)
-//            K3 gather     k_gather (HBM: cache hits and local-HBM misses)
+//   forward  K1 dedup      k_insert -> k_compact (single-pass look-back scan + emit)
+//            K2 partition  k_inverse_partition (inverse | hit/miss per unique, miss queue)
+//            K3 gather     k_gather (HBM: cache hits and local-HBM misses; resets the
+//                          hash slot, zeroes the gradient row)
 //                          k_gather_host (pinned host misses, side stream)
 //            K4 exchange   exchange.cu (world > 1)
 //            K5 pool       k_pool (EmbeddingBag sum through inverse indices)
-//   backward K6            k_zero -> k_scatter (grad -> unique rows) -> k_apply (SGD)
+//   backward K6            k_scatter (bag grads -> unique rows, smem aggregation)
+//                          -> k_apply (SGD; k_apply_host for pinned-host rows)
+// Kernels live in lookup_kernels.cuh.
 //
 // Reference anchors: the dedup reproduces count_batch_unique's distinct and
 // non-cached distinct counts (core/src/simulator.cpp:85-106) per table batch
@@ -61,425 +64,11 @@ void use_device(int device) {
   EC_CUDA(cudaSetDevice(device));
 }
 
-// ------------------------------------------------------------------ K1
-constexpr int kThreads = 256;
-constexpr int kItems = 4;
-constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
+}  // namespace ec
 
-__device__ __forceinline__ uint32_t hash_insert(unsigned long long* tab, uint32_t mask, uint32_t shift,
-                                                uint32_t id, uint32_t lpos) {
-  const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
-  uint32_t h = hash_slot(id, shift);
-  for (;;) {
-    unsigned long long cur = __ldcg(tab + h);
-    if (cur == kEmptySlot) {
-      cur = atomicCAS(tab + h, kEmptySlot, mine);
-      if (cur == kEmptySlot) return h;
-    }
-    if (static_cast<uint32_t>(cur >> 32) == id) {
-      // same key: keep the smallest position (high words equal -> packed min)
-      if (static_cast<uint32_t>(cur) > lpos) atomicMin(tab + h, mine);
-      return h;
-    }
-    h = (h + 1) & mask;
-  }
-}
+#include "lookup_kernels.cuh"
 
-// Insert every lookup of a tile; warp lanes holding the same id collapse to
-// their lowest lane (= smallest position) before touching the table.
-__global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
-                                                     const uint32_t* __restrict__ indices,
-                                                     uint32_t* __restrict__ slot_of, int* __restrict__ err) {
-  const Tile tile = tiles[blockIdx.x];
-  const TableDev t = td[tile.table];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t off = j * kThreads + threadIdx.x;
-    bool live = off < tile.count;
-    const int64_t p = tile.start + off;
-    uint32_t id = live ? __ldcs(indices + p) : kEmptyKey;
-    if (live && id >= t.rows) {
-      atomicExch(err, 1);
-      live = false;
-      id = kEmptyKey;
-    }
-    const unsigned peers = __match_any_sync(kFull, id);
-    const int leader = __ffs(peers) - 1;
-    uint32_t h = 0;
-    if (live && leader == lane_id()) h = hash_insert(t.hash, t.mask, t.shift, id, static_cast<uint32_t>(p - t.base));
-    h = __shfl_sync(kFull, h, leader);
-    if (live) slot_of[p] = h;
-    else if (off < tile.count) slot_of[p] = kInvalidSlot;  // out-of-range id: skipped downstream
-  }
-}
-
-// First-occurrence flags per tile: lookup p is first iff the slot's packed
-// minimum position is p.
-__device__ __forceinline__ bool is_first(const TableDev& t, const uint32_t* slot_of, int64_t p, uint32_t* h) {
-  *h = slot_of[p];
-  return *h != kInvalidSlot && static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
-}
-
-__global__ void __launch_bounds__(kThreads) k_count(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
-                                                    const uint32_t* __restrict__ slot_of, int* __restrict__ tile_cnt) {
-  const Tile tile = tiles[blockIdx.x];
-  const TableDev t = td[tile.table];
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t off = j * kThreads + threadIdx.x;
-    uint32_t h;
-    if (off < tile.count && is_first(t, slot_of, tile.start + off, &h)) ++c;
-  }
-  __shared__ int w[kThreads / 32];
-  const int s = __reduce_add_sync(kFull, c);
-  if (lane_id() == 0) w[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int k = 0; k < kThreads / 32; ++k) tot += w[k];
-    tile_cnt[blockIdx.x] = tot;
-  }
-}
-
-// Single block: exclusive scan of tile counts in (table, position) order ->
-// global unique index base of each tile; per-table U and ubase; resets the
-// per-batch miss counters.
-__global__ void __launch_bounds__(1024) k_scan(int* __restrict__ tile_cnt, int ntiles, const int* __restrict__ first_tile,
-                                               int T, int* __restrict__ ctr) {
-  __shared__ int sw[32];
-  int carry = 0;
-  for (int base = 0; base < ntiles; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int v = i < ntiles ? tile_cnt[i] : 0;
-    int tot;
-    const int ex = block_exclusive_scan<1024>(v, sw, &tot);
-    if (i < ntiles) tile_cnt[i] = carry + ex;  // in place: now tile bases
-    carry += tot;
-  }
-  __syncthreads();
-  Counters c = counters(ctr, T);
-  for (int t = threadIdx.x; t <= T; t += blockDim.x) {
-    const int ft = first_tile[t];
-    c.ubase[t] = ft < ntiles ? tile_cnt[ft] : carry;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {
-    c.U[t] = c.ubase[t + 1] - c.ubase[t];
-    c.M[t] = 0;
-  }
-  if (threadIdx.x == 0) *c.miss_total = 0;
-}
-
-// Emit unique ids in first-occurrence order and tag each slot with the
-// unique's global index (low word | kRankTag, so no later flag test can
-// mistake it for a position).
-__global__ void __launch_bounds__(kThreads) k_emit(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
-                                                   const uint32_t* __restrict__ indices,
-                                                   const uint32_t* __restrict__ slot_of, const int* __restrict__ tile_base,
-                                                   uint32_t* __restrict__ uniq, uint32_t* __restrict__ uslot,
-                                                   uint16_t* __restrict__ utab) {
-  __shared__ int sw[kThreads / 32];
-  const Tile tile = tiles[blockIdx.x];
-  const TableDev t = td[tile.table];
-  int run = tile_base[blockIdx.x];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t off = j * kThreads + threadIdx.x;
-    uint32_t h = 0;
-    const bool first = off < tile.count && is_first(t, slot_of, tile.start + off, &h);
-    int tot;
-    const int ex = block_exclusive_scan<kThreads>(first ? 1 : 0, sw, &tot);
-    if (first) {
-      const uint32_t g = static_cast<uint32_t>(run + ex);
-      const uint32_t id = indices[tile.start + off];
-      uniq[g] = id;
-      uslot[g] = h;
-      utab[g] = static_cast<uint16_t>(tile.table);
-      t.hash[h] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
-    }
-    run += tot;
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_inverse(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
-                                                      const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ inv) {
-  const Tile tile = tiles[blockIdx.x];
-  const TableDev t = td[tile.table];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const uint32_t off = j * kThreads + threadIdx.x;
-    if (off < tile.count) {
-      const int64_t p = tile.start + off;
-      const uint32_t h = slot_of[p];
-      inv[p] = h == kInvalidSlot ? kInvalidSlot : static_cast<uint32_t>(__ldcg(t.hash + h)) & ~kRankTag;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K2
-// Per unique row: cache slot or miss; per-table miss counts; miss queue
-// (rows the GPU must fetch from the cold tier / owner); hash slot reset.
-__global__ void __launch_bounds__(kThreads) k_partition(const TableDev* __restrict__ td, int T, int* __restrict__ ctr,
-                                                        const uint32_t* __restrict__ uniq,
-                                                        const uint16_t* __restrict__ utab,
-                                                        const uint32_t* __restrict__ uslot, int32_t* __restrict__ usrc,
-                                                        uint32_t* __restrict__ missq) {
-  Counters c = counters(ctr, T);
-  const int U = c.ubase[T];
-  for (int base = blockIdx.x * blockDim.x; base < U; base += gridDim.x * blockDim.x) {
-    const int g = base + threadIdx.x;
-    const bool live = g < U;
-    int tab = -1;
-    bool miss = false;
-    if (live) {
-      tab = utab[g];
-      const TableDev t = td[tab];
-      const int32_t s = __ldg(t.remap + uniq[g]);
-      usrc[g] = s;
-      miss = s < 0;
-      t.hash[uslot[g]] = kEmptySlot;
-    }
-    const unsigned peers = __match_any_sync(kFull, tab);
-    const int nm = group_count(peers, miss);
-    if (live && nm && (__ffs(peers) - 1) == lane_id()) atomicAdd(c.M + tab, nm);
-    const unsigned mb = __ballot_sync(kFull, miss);
-    int qbase = 0;
-    if (mb && lane_id() == __ffs(mb) - 1) qbase = atomicAdd(c.miss_total, __popc(mb));
-    qbase = __shfl_sync(kFull, qbase, __ffs(mb ? mb : 1u) - 1);
-    if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
-  }
-}
-
-// ------------------------------------------------------------------ K3
-// VEC = D/4 lanes per row, 128-bit loads; each thread keeps R rows in flight.
-template <int VEC>
-struct RowMap {
-  static constexpr int kRowsPerWarp = 32 / VEC;
-  int sub, c;
-  __device__ RowMap() : sub(lane_id() / VEC), c(lane_id() % VEC) {}
-};
-
-template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
-                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
-                                                     const int32_t* __restrict__ usrc, const float* __restrict__ cache,
-                                                     float* __restrict__ urows, int local_hbm, int rank, int world) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
-    float4 v[R];
-    int dst[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int g = g0 + r * RPW + m.sub;
-      dst[r] = -1;
-      if (g < U) {
-        const int32_t s = usrc[g];
-        const float* src = nullptr;
-        if (s >= 0) {
-          src = cache + static_cast<int64_t>(s) * D;
-        } else if (local_hbm) {
-          const uint32_t id = uniq[g];
-          if (static_cast<int>(id % world) == rank) src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
-        }
-        if (src) {
-          v[r] = ldg4(src + m.c * 4);
-          dst[r] = g;
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
-  }
-}
-
-// Misses served from pinned host memory (UVA-mapped shard), side stream.
-template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
-                                                          const uint32_t* __restrict__ missq,
-                                                          const uint32_t* __restrict__ uniq,
-                                                          const uint16_t* __restrict__ utab, float* __restrict__ urows,
-                                                          int rank, int world) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
-    float4 v[R];
-    int dst[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = q0 + r * RPW + m.sub;
-      dst[r] = -1;
-      if (q < nm) {
-        const uint32_t g = missq[q];
-        const uint32_t id = uniq[g];
-        if (static_cast<int>(id % world) == rank) {
-          const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
-          v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
-          dst[r] = static_cast<int>(g);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
-  }
-}
-
-// ------------------------------------------------------------------ K5
-// Bags are visited sample-major (q = s*T + t) so each warp writes a
-// contiguous stretch of the [B, T*D] output.
-__device__ __forceinline__ void bag_range(const TableDev* td, const int64_t* bag_off, int T, int B, int P, int s,
-                                          int t, int64_t* lo, int64_t* hi) {
-  if (bag_off) {
-    *lo = bag_off[static_cast<int64_t>(t) * B + s];
-    *hi = bag_off[static_cast<int64_t>(t) * B + s + 1];
-  } else {
-    *lo = td[t].base + static_cast<int64_t>(s) * P;
-    *hi = *lo + P;
-  }
-}
-
-// Row u's float4 #c of the compact unique-row buffer; invalid lookups read 0.
-__device__ __forceinline__ float4 load_row(const float* urows, uint32_t u, int D, int c) {
-  if (u == kInvalidSlot) return make_float4(0.f, 0.f, 0.f, 0.f);
-  return ldg4(urows + static_cast<int64_t>(u) * D + c * 4);
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
-                                                   const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
-                                                   const float* __restrict__ urows, float* __restrict__ out) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int nbags = T * B;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW; q0 < nbags; q0 += nwarps * RPW) {
-    const int q = q0 + m.sub;
-    if (q >= nbags) continue;
-    const int s = q / T, t = q - s * T;
-    int64_t lo, hi;
-    bag_range(td, bag_off, T, B, P, s, t, &lo, &hi);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int64_t i = lo;
-    for (; i + 4 <= hi; i += 4) {  // 4 rows in flight, summed in lookup order
-      const float4 a = load_row(urows, inv[i], D, m.c);
-      const float4 b = load_row(urows, inv[i + 1], D, m.c);
-      const float4 c = load_row(urows, inv[i + 2], D, m.c);
-      const float4 d = load_row(urows, inv[i + 3], D, m.c);
-      acc = add4(add4(add4(add4(acc, a), b), c), d);
-    }
-    for (; i < hi; ++i) acc = add4(acc, load_row(urows, inv[i], D, m.c));
-    st4(out + (static_cast<int64_t>(s) * T + t) * D + m.c * 4, acc);
-  }
-}
-
-// ------------------------------------------------------------------ K6
-__global__ void k_zero(float4* __restrict__ p, const int* __restrict__ ctr, int T, int vec_per_row) {
-  const int64_t n = static_cast<int64_t>(counters(const_cast<int*>(ctr), T).ubase[T]) * vec_per_row;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
-// grad of bag (s, t) is added to the unique row of every lookup in the bag.
-template <int VEC>
-__global__ void __launch_bounds__(kThreads) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
-                                                      const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
-                                                      const float* __restrict__ grad, float* __restrict__ ugrad) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int nbags = T * B;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW; q0 < nbags; q0 += nwarps * RPW) {
-    const int q = q0 + m.sub;
-    if (q >= nbags) continue;
-    const int s = q / T, t = q - s * T;
-    int64_t lo, hi;
-    bag_range(td, bag_off, T, B, P, s, t, &lo, &hi);
-    const float4 gv = ld_stream4(grad + (static_cast<int64_t>(s) * T + t) * D + m.c * 4);
-    for (int64_t i = lo; i < hi; ++i) {
-      const uint32_t u = inv[i];
-      if (u != kInvalidSlot) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + m.c * 4), gv);
-    }
-  }
-}
-
-// SGD on every unique row: w = w_gathered - lr * g, written to the cache copy
-// (hits) or the owning local shard (misses, HBM or mapped host).
-template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
-                                                    const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
-                                                    const int32_t* __restrict__ usrc, const float* __restrict__ urows,
-                                                    const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
-                                                    int misses_local, int rank, int world) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int g = g0 + r * RPW + m.sub;
-      if (g >= U) continue;
-      const int32_t s = usrc[g];
-      float* dst = nullptr;
-      if (s >= 0) {
-        dst = cache + static_cast<int64_t>(s) * D;
-      } else if (misses_local) {
-        const uint32_t id = uniq[g];
-        if (static_cast<int>(id % world) == rank) dst = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
-      }
-      if (!dst) continue;
-      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
-      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
-      st4(dst + m.c * 4, make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
-    }
-  }
-}
-
-// SGD for cold rows held in pinned host memory (miss queue, side stream).
-template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
-                                                         const uint32_t* __restrict__ missq,
-                                                         const uint32_t* __restrict__ uniq,
-                                                         const uint16_t* __restrict__ utab, const float* __restrict__ urows,
-                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
-  constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
-  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = q0 + r * RPW + m.sub;
-      if (q >= nm) continue;
-      const uint32_t g = missq[q];
-      const uint32_t id = uniq[g];
-      if (static_cast<int>(id % world) != rank) continue;
-      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
-      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
-      st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4,
-          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
-    }
-  }
-}
+namespace ec {
 
 // -------------------------------------------------- table maintenance
 __device__ __forceinline__ float synth_value(uint64_t seed, float scale, uint32_t t, uint64_t id, uint32_t D,
@@ -560,7 +149,10 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
 
 // ------------------------------------------------------------ host side
 static int persistent_grid(int device) { return sm_count(device) * 8; }
-int Engine::host_grid() const { return sm_count(device) * 2; }
+// Row kernels share the SMs with the side-stream host-link kernels (1 CTA/SM,
+// ~48 regs x 256 threads each): size the main grids so every CTA is resident.
+int Engine::host_grid() const { return sm_count(device); }
+int Engine::row_grid() const { return sm_count(device) * (storage == EC_STORAGE_HOST ? 3 : 4); }
 
 static uint32_t log2_ceil(uint64_t x) {
   uint32_t l = 0;
@@ -635,8 +227,7 @@ void Engine::create(const ec_tables_config& c) {
   ugrad.alloc(N * D);
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
   tiles.alloc(max_tiles);
-  tile_cnt.alloc(max_tiles);
-  first_tile.alloc(T + 1);
+  status.alloc(max_tiles + 1);
   ctr.alloc(counters_size(T));
   EC_CUDA(cudaMemset(ctr.p, 0, ctr.bytes()));
   tdev.alloc(T);
@@ -662,7 +253,7 @@ void Engine::create(const ec_tables_config& c) {
 uint64_t Engine::device_bytes() const {
   return store_dev.bytes() + remap.bytes() + hash.bytes() + cache.bytes() + slot_of.bytes() + inv.bytes() +
          uniq.bytes() + uslot.bytes() + usrc.bytes() + missq.bytes() + utab.bytes() + urows.bytes() +
-         ugrad.bytes() + tiles.bytes() + tile_cnt.bytes() + ctr.bytes() + cache_ids.bytes() + cache_tab.bytes() +
+         ugrad.bytes() + tiles.bytes() + status.bytes() + stiles.bytes() + ctr.bytes() + cache_ids.bytes() + cache_tab.bytes() +
          exch_bytes();
 }
 
@@ -769,7 +360,9 @@ void Engine::rw_rows(uint32_t t, const uint32_t* ids, uint64_t n, float* buf_hos
   if (!write) EC_CUDA(cudaMemcpy(buf_host, dbuf.p, n * D * sizeof(float), cudaMemcpyDeviceToHost));
 }
 
-// Per-batch geometry: tiles never straddle tables; uploaded only on change.
+// Per-batch geometry (uploaded only on change): dedup tiles never straddle
+// tables; each tile knows which tables' ubase it publishes; scatter tiles are
+// runs of bags of one table.
 void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   bool same = have_geom && b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed;
   for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
@@ -782,15 +375,33 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
     const int64_t lo = geom_off[t], n = geom_off[t + 1] - geom_off[t];
     ft[t] = static_cast<int>(tl.size());
     for (int64_t s = 0; s < n; s += kTile)
-      tl.push_back(Tile{t, static_cast<uint32_t>(std::min<int64_t>(kTile, n - s)), lo + s});
+      tl.push_back(Tile{t, static_cast<uint32_t>(std::min<int64_t>(kTile, n - s)), lo + s, 0, 0});
     td_host[t].base = lo;
     td_host[t].n = n;
   }
-  ft[T] = static_cast<int>(tl.size());
   ntiles = static_cast<int>(tl.size());
+  tail_lo = static_cast<int>(T);
+  for (int t = static_cast<int>(T) - 1; t >= 0 && ft[t] == ntiles; --t) tail_lo = t;  // trailing empty tables
+  for (uint32_t t = 0; t < static_cast<uint32_t>(tail_lo); ++t) {
+    Tile& x = tl[ft[t]];
+    if (x.ub_hi == 0) x.ub_lo = t;
+    x.ub_hi = t + 1;
+  }
+  // scatter tiles: ~kTile lookups of one table each (bag count for fixed
+  // pooling; 256 bags for CSR)
+  std::vector<int4> sc;
+  const int per = b.bag_offsets_dev ? 256 : static_cast<int>(std::max<int64_t>(1, kTile / std::max<uint32_t>(1, b.pooling)));
+  for (uint32_t t = 0; t < T; ++t) {
+    if (geom_off[t + 1] == geom_off[t]) continue;
+    for (int s0 = 0; s0 < static_cast<int>(b.batch_size); s0 += per)
+      sc.push_back(make_int4(static_cast<int>(t), s0, std::min<int>(b.batch_size, s0 + per), 0));
+  }
+  nstiles = static_cast<int>(sc.size());
   EC_CUDA(cudaStreamSynchronize(st));
   if (ntiles) EC_CUDA(cudaMemcpy(tiles.p, tl.data(), tl.size() * sizeof(Tile), cudaMemcpyHostToDevice));
-  EC_CUDA(cudaMemcpy(first_tile.p, ft.data(), (T + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  if (status.n < static_cast<size_t>(ntiles) + 1) status.alloc(ntiles + 1);
+  if (stiles.n < sc.size()) stiles.alloc(sc.size());
+  if (nstiles) EC_CUDA(cudaMemcpy(stiles.p, sc.data(), sc.size() * sizeof(int4), cudaMemcpyHostToDevice));
   EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
   geom_b = b.batch_size;
   geom_p = b.pooling;
@@ -800,7 +411,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
 
 template <int VEC>
 void Engine::launch_row_kernels_fwd(cudaStream_t st) {
-  const int grid = persistent_grid(device);
+  const int grid = row_grid();
   if (storage == EC_STORAGE_HOST) {
     // host misses on the side stream, overlapping the HBM hit gather
     EC_CUDA(cudaEventRecord(ev_part, st));
@@ -815,8 +426,8 @@ void Engine::launch_row_kernels_fwd(cudaStream_t st) {
   }
   {
   PhaseScope ph(prof, kPhaseGather, st);
-  k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, cache.p, urows.p,
-                                              storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+  k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
+                                              ugrad.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
   launched();
   }
   if (world > 1) {
@@ -825,20 +436,21 @@ void Engine::launch_row_kernels_fwd(cudaStream_t st) {
   }
   if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PhaseScope ph(prof, kPhasePool, st);
-  k_pool<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, inv.p,
-                                         urows.p, out_ptr);
+  k_pool<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
+                                            inv.p, urows.p, out_ptr);
   launched();
 }
 
 template <int VEC>
 void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st) {
-  const int grid = persistent_grid(device);
+  const int grid = row_grid();
   {
   PhaseScope ph(prof, kPhaseScatter, st);
-  k_zero<<<grid, kThreads, 0, st>>>(reinterpret_cast<float4*>(ugrad.p), ctr.p, T, VEC);
-  launched();
-  k_scatter<VEC><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
-                                            inv.p, grad, ugrad.p);
+  // ugrad rows were zeroed by k_gather
+  if (nstiles) {
+    k_scatter<VEC><<<std::min(nstiles, sm_count(device) * 4), kThreads, 0, st>>>(
+        tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, stiles.p, nstiles, inv.p, grad, ugrad.p);
+  }
   launched();
   }
   if (world > 1) {
@@ -883,6 +495,7 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     if (!b.bag_offsets_dev && n != static_cast<int64_t>(b.batch_size) * b.pooling)
       invalid("table " + std::to_string(t) + ": fixed pooling needs batch_size*pooling lookups");
   }
+  if (b.table_offsets_host[T] >= (int64_t{1} << 31)) invalid("a batch holds at most 2^31-1 lookups");
   if (world > 1 && !comm_ready()) invalid("world > 1 needs ec_tables_attach_comm");
   use_device(device);
   set_geometry(b, st);
@@ -942,28 +555,24 @@ void Engine::clear_graphs() {
 }
 
 void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
-  const int grid = persistent_grid(device);
   {
-  PhaseScope ph(prof, kPhaseDedup, st);
-  if (ntiles) {
-    k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, counters(ctr.p, T).err);
-    launched();
-    k_count<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, tile_cnt.p);
-    launched();
-  }
-  k_scan<<<1, 1024, 0, st>>>(tile_cnt.p, ntiles, first_tile.p, static_cast<int>(T), ctr.p);
-  launched();
-  if (ntiles) {
-    k_emit<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, tile_cnt.p, uniq.p, uslot.p, utab.p);
-    launched();
-    k_inverse<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p);
-    launched();
-  }
+    PhaseScope ph(prof, kPhaseDedup, st);
+    if (ntiles) {
+      k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T));
+      launched();
+      k_compact<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T),
+                                             ntiles, tail_lo, uniq.p, uslot.p, utab.p);
+      launched();
+    } else {
+      EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
+    }
   }
   {
-  PhaseScope ph(prof, kPhasePartition, st);
-  k_partition<<<grid, kThreads, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, uslot.p, usrc.p, missq.p);
-  launched();
+    PhaseScope ph(prof, kPhasePartition, st);
+    k_inverse_partition<<<ntiles + sm_count(device) * 2, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p, ntiles,
+                                                                          static_cast<int>(T), ctr.p, uniq.p, utab.p,
+                                                                          usrc.p, missq.p);
+    launched();
   }
   EC_DISPATCH_VEC(launch_row_kernels_fwd, st);
 }
@@ -1152,10 +761,11 @@ int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* u_p
     s.lookups = static_cast<uint64_t>(e.geom_off[e.T]);
     s.index_units = s.lookups;
     for (uint32_t i = 0; i < e.T; ++i) {
-      s.unique_rows += c.U[i];
+      const int Ui = c.ubase[i + 1] - c.ubase[i];
+      s.unique_rows += Ui;
       s.miss_rows += c.M[i];
       s.hot_tables += c.M[i] == 0;
-      if (u_per) u_per[i] = c.U[i];
+      if (u_per) u_per[i] = Ui;
       if (m_per) m_per[i] = c.M[i];
     }
     s.hit_rows = s.unique_rows - s.miss_rows;
@@ -1172,7 +782,7 @@ static void table_span(Engine& e, uint32_t table, std::vector<int>& h, int* lo, 
   e.read_counters(nullptr, h);
   Counters c = counters(h.data(), e.T);
   *lo = c.ubase[table];
-  *n = c.U[table];
+  *n = c.ubase[table + 1] - c.ubase[table];
 }
 
 int ec_export_unique(ec_tables t, uint32_t table, uint32_t* out, uint64_t cap, uint64_t* count) {

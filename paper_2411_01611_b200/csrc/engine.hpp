@@ -25,16 +25,18 @@ struct Tile {
   uint32_t table;
   uint32_t count;
   int64_t start;
+  uint32_t ub_lo, ub_hi;  // tables whose first tile this is (k_compact writes their ubase)
 };
 
-// Per-batch device counters, one int array: U[T] M[T] ubase[T+1] miss_total err
+// Per-batch device counters, one int array:
+//   M[T] ubase[T+1] miss_total tile_counter err   (err last: survives resets)
 struct Counters {
-  int *U, *M, *ubase, *miss_total, *err;
+  int *M, *ubase, *miss_total, *tile_counter, *err;
 };
 __host__ __device__ inline Counters counters(int* p, int T) {
-  return Counters{p, p + T, p + 2 * T, p + 3 * T + 1, p + 3 * T + 2};
+  return Counters{p, p + T, p + 2 * T + 1, p + 2 * T + 2, p + 2 * T + 3};
 }
-inline size_t counters_size(int T) { return 3 * static_cast<size_t>(T) + 3; }
+inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 4; }
 
 struct Exchange;  // exchange.cu
 
@@ -111,10 +113,12 @@ struct Engine {
   DevBuf<uint16_t> utab;
   DevBuf<float> urows, ugrad;
   DevBuf<Tile> tiles;
-  DevBuf<int> tile_cnt, first_tile, ctr;
+  DevBuf<unsigned long long> status;  // decoupled look-back words, one per tile
+  DevBuf<int4> stiles;                // scatter tiles (table, bag lo, bag hi, -)
+  DevBuf<int> ctr;
   DevBuf<TableDev> tdev;
   std::vector<TableDev> td_host;
-  int ntiles = 0;
+  int ntiles = 0, nstiles = 0, tail_lo = 0;
 
   // geometry of the last batch
   bool have_geom = false, geom_fixed = true, have_fwd = false;
@@ -146,6 +150,7 @@ struct Engine {
   void create(const ec_tables_config& c);
   uint64_t device_bytes() const;
   int host_grid() const;
+  int row_grid() const;
   void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
   void fill_cache(cudaStream_t st, bool from_store);
   void place_cache(const uint32_t* const* ids, const uint64_t* k);

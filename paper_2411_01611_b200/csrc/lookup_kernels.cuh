@@ -1,0 +1,540 @@
+// sm_100a kernels of the lookup engine (K1 dedup, K2 hit/miss, K3 gather,
+// K5 pool, K6 backward).  Included by engine.cu; see the pipeline and HBM
+// layout described there.
+//
+// Per batch (fixed kernel sequence, no host synchronisation, CUDA-graph
+// capturable):
+//   k_insert           lookup -> hash slot (warp match-any collapse, packed
+//                      atomicMin keeps each id's first position); resets the
+//                      look-back status words and per-batch counters
+//   k_compact          first-occurrence flags, single-pass decoupled
+//                      look-back scan over tiles (table-major) -> global unique
+//                      index, unique ids emitted, slot tagged with the index
+//   k_inverse_partition  lookup -> unique index (inverse) | unique -> cache slot
+//                      or miss (per-table miss counts, miss queue)
+//   k_gather           cache/HBM rows -> compact unique rows; also clears the
+//                      hash slot and zeroes the unique's gradient row
+//   k_gather_host      pinned-host misses (side stream)
+//   k_pool             EmbeddingBag sum through inverse indices
+//   k_scatter          bag gradients -> unique rows, block-local shared-memory
+//                      aggregation (hot rows), global float4 atomics otherwise
+//   k_apply(_host)     SGD into cache rows / owning shard
+#pragma once
+
+#include "device_util.cuh"
+#include "engine.hpp"
+
+namespace ec {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 4;
+constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
+
+// ------------------------------------------------------------------ K1
+__device__ __forceinline__ uint32_t hash_insert(unsigned long long* tab, uint32_t mask, uint32_t shift,
+                                                uint32_t id, uint32_t lpos) {
+  const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
+  uint32_t h = hash_slot(id, shift);
+  for (;;) {
+    unsigned long long cur = __ldcg(tab + h);
+    if (cur == kEmptySlot) {
+      cur = atomicCAS(tab + h, kEmptySlot, mine);
+      if (cur == kEmptySlot) return h;
+    }
+    if (static_cast<uint32_t>(cur >> 32) == id) {
+      // same key: keep the smallest position (high words equal -> packed min)
+      if (static_cast<uint32_t>(cur) > lpos) atomicMin(tab + h, mine);
+      return h;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                     const uint32_t* __restrict__ indices,
+                                                     uint32_t* __restrict__ slot_of,
+                                                     unsigned long long* __restrict__ status, int* __restrict__ ctr,
+                                                     int T) {
+  const Tile tile = tiles[blockIdx.x];
+  const TableDev t = td[tile.table];
+  Counters c = counters(ctr, T);
+  if (threadIdx.x == 0) status[blockIdx.x] = 0;  // look-back word of this tile, read by k_compact
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < T; i += blockDim.x) c.M[i] = 0;
+    if (threadIdx.x == 0) {
+      *c.miss_total = 0;
+      *c.tile_counter = 0;
+    }
+  }
+  uint32_t id[kItems];
+  bool live[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {  // all loads first: kItems independent requests in flight
+    const uint32_t off = j * kThreads + threadIdx.x;
+    live[j] = off < tile.count;
+    id[j] = live[j] ? __ldcs(indices + tile.start + off) : kEmptyKey;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    const int64_t p = tile.start + off;
+    if (live[j] && id[j] >= t.rows) {
+      atomicExch(c.err, 1);
+      live[j] = false;
+      id[j] = kEmptyKey;
+    }
+    // lanes holding the same id collapse to their lowest lane (= smallest position)
+    const unsigned peers = __match_any_sync(kFull, id[j]);
+    const int leader = __ffs(peers) - 1;
+    uint32_t h = 0;
+    if (live[j] && leader == lane_id()) h = hash_insert(t.hash, t.mask, t.shift, id[j], static_cast<uint32_t>(p - t.base));
+    h = __shfl_sync(kFull, h, leader);
+    if (live[j]) slot_of[p] = h;
+    else if (off < tile.count) slot_of[p] = kInvalidSlot;  // out-of-range id: skipped downstream
+  }
+}
+
+// Lookup p is its id's first occurrence iff the slot's packed minimum is p.
+__device__ __forceinline__ bool is_first(const TableDev& t, const uint32_t* slot_of, int64_t p, uint32_t* h) {
+  *h = slot_of[p];
+  return *h != kInvalidSlot && static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
+}
+
+constexpr unsigned long long kStatAgg = 1ull << 32;  // status word: (flag << 32) | value
+constexpr unsigned long long kStatInc = 2ull << 32;
+
+__device__ __forceinline__ void publish(unsigned long long* p, unsigned long long v) {
+  __threadfence();
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+// Flags + single-pass scan (decoupled look-back over tiles claimed in order
+// through an atomic counter) + emission.  Tiles are table-major, so the
+// global exclusive prefix is the unique index in (table, first occurrence)
+// order and the prefix at a table's first tile is that table's ubase.
+__global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
+                                                      const uint32_t* __restrict__ indices,
+                                                      const uint32_t* __restrict__ slot_of,
+                                                      unsigned long long* __restrict__ status, int* __restrict__ ctr,
+                                                      int T, int ntiles, int tail_lo, uint32_t* __restrict__ uniq,
+                                                      uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab) {
+  __shared__ int s_tile, s_excl;
+  __shared__ int sw[kThreads / 32];
+  Counters c = counters(ctr, T);
+  if (threadIdx.x == 0) s_tile = atomicAdd(c.tile_counter, 1);
+  __syncthreads();
+  const int ti = s_tile;
+  const Tile tile = tiles[ti];
+  const TableDev t = td[tile.table];
+  bool first[kItems];
+  uint32_t h[kItems];
+  int ex[kItems], count = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    first[j] = off < tile.count && is_first(t, slot_of, tile.start + off, &h[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {  // position order within the tile: j-major, then thread
+    int tot;
+    ex[j] = count + block_exclusive_scan<kThreads>(first[j] ? 1 : 0, sw, &tot);
+    count += tot;
+  }
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int excl = 0;
+    if (ti == 0) {
+      if (lane == 0) publish(status, kStatInc | static_cast<uint32_t>(count));
+    } else {
+      if (lane == 0) publish(status + ti, kStatAgg | static_cast<uint32_t>(count));
+      for (int k = ti - 1;; k -= 32) {
+        const int idx = k - lane;
+        unsigned long long v = kStatInc;  // before tile 0: an inclusive zero ends the walk
+        if (idx >= 0) {
+          do {
+            v = *reinterpret_cast<volatile unsigned long long*>(status + idx);
+          } while ((v >> 32) == 0);
+        }
+        const unsigned inc = __ballot_sync(kFull, (v >> 32) == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        excl += __reduce_add_sync(kFull, lane <= stop ? static_cast<int>(static_cast<uint32_t>(v)) : 0);
+        if (inc) break;
+      }
+      if (lane == 0) publish(status + ti, kStatInc | static_cast<uint32_t>(excl + count));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      for (uint32_t tb = tile.ub_lo; tb < tile.ub_hi; ++tb) c.ubase[tb] = excl;  // tables starting here
+      if (ti == ntiles - 1)
+        for (int tb = tail_lo; tb <= T; ++tb) c.ubase[tb] = excl + count;  // trailing empty tables + total
+    }
+  }
+  __syncthreads();
+  const int base = s_excl;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (!first[j]) continue;
+    const uint32_t off = j * kThreads + threadIdx.x;
+    const uint32_t g = static_cast<uint32_t>(base + ex[j]);
+    const uint32_t id = indices[tile.start + off];
+    uniq[g] = id;
+    uslot[g] = h[j];
+    utab[g] = static_cast<uint16_t>(tile.table);
+    // only this thread writes this slot; concurrent flag tests never match a tagged value
+    t.hash[h[j]] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
+  }
+}
+
+// Blocks [0, ntiles): inverse of each lookup (the slot now holds its tagged
+// unique index).  Blocks [ntiles, ...): hit/miss partition of the uniques.
+__global__ void __launch_bounds__(kThreads) k_inverse_partition(const Tile* __restrict__ tiles,
+                                                                const TableDev* __restrict__ td,
+                                                                const uint32_t* __restrict__ slot_of,
+                                                                uint32_t* __restrict__ inv, int ntiles, int T,
+                                                                int* __restrict__ ctr, const uint32_t* __restrict__ uniq,
+                                                                const uint16_t* __restrict__ utab,
+                                                                int32_t* __restrict__ usrc,
+                                                                uint32_t* __restrict__ missq) {
+  if (static_cast<int>(blockIdx.x) < ntiles) {
+    const Tile tile = tiles[blockIdx.x];
+    const TableDev t = td[tile.table];
+    uint32_t hs[kItems];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint32_t off = j * kThreads + threadIdx.x;
+      hs[j] = off < tile.count ? slot_of[tile.start + off] : kInvalidSlot;
+    }
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint32_t off = j * kThreads + threadIdx.x;
+      if (off < tile.count)
+        inv[tile.start + off] = hs[j] == kInvalidSlot ? kInvalidSlot
+                                                      : static_cast<uint32_t>(__ldcg(t.hash + hs[j])) & ~kRankTag;
+    }
+    return;
+  }
+  // K2: cache slot (>= 0) or miss (-1) per unique; a lookup misses iff its id
+  // is not cached (core/src/simulator.cpp:99)
+  Counters c = counters(ctr, T);
+  const int U = c.ubase[T];
+  const int nb = gridDim.x - ntiles, b = blockIdx.x - ntiles;
+  for (int base = b * blockDim.x; base < U; base += nb * blockDim.x) {
+    const int g = base + threadIdx.x;
+    const bool live = g < U;
+    int tab = -1;
+    bool miss = false;
+    if (live) {
+      tab = utab[g];
+      const int32_t s = __ldg(td[tab].remap + uniq[g]);
+      usrc[g] = s;
+      miss = s < 0;
+    }
+    const unsigned peers = __match_any_sync(kFull, tab);
+    const int nm = group_count(peers, miss);
+    if (live && nm && (__ffs(peers) - 1) == lane_id()) atomicAdd(c.M + tab, nm);
+    const unsigned mb = __ballot_sync(kFull, miss);
+    int qbase = 0;
+    if (mb && lane_id() == __ffs(mb) - 1) qbase = atomicAdd(c.miss_total, __popc(mb));
+    qbase = __shfl_sync(kFull, qbase, __ffs(mb ? mb : 1u) - 1);
+    if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
+  }
+}
+
+// ------------------------------------------------------------------ K3
+// VEC = D/4 lanes per row, 128-bit accesses; R rows in flight per thread.
+template <int VEC>
+struct RowMap {
+  static constexpr int kRowsPerWarp = 32 / VEC;
+  int sub, c;
+  __device__ RowMap() : sub(lane_id() / VEC), c(lane_id() % VEC) {}
+};
+
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                                                     const uint32_t* __restrict__ uslot,
+                                                     const int32_t* __restrict__ usrc, const float* __restrict__ cache,
+                                                     float* __restrict__ urows, float* __restrict__ ugrad, int local_hbm,
+                                                     int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
+    float4 v[R];
+    int dst[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      dst[r] = -1;
+      if (g < U) {
+        const int32_t s = usrc[g];
+        const float* src = nullptr;
+        const uint32_t tab = utab[g];
+        if (s >= 0) {
+          src = cache + static_cast<int64_t>(s) * D;
+        } else if (local_hbm) {
+          const uint32_t id = uniq[g];
+          if (static_cast<int>(id % world) == rank) src = td[tab].store + static_cast<int64_t>(id / world) * D;
+        }
+        if (src) {
+          v[r] = ldg4(src + m.c * 4);
+          dst[r] = g;
+        }
+        if (m.c == 0) td[tab].hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
+        st4(ugrad + static_cast<int64_t>(g) * D + m.c * 4, zero);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+}
+
+// Misses served from pinned host memory (UVA-mapped shard), side stream.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                          const uint32_t* __restrict__ missq,
+                                                          const uint32_t* __restrict__ uniq,
+                                                          const uint16_t* __restrict__ utab, float* __restrict__ urows,
+                                                          int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+    float4 v[R];
+    int dst[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      dst[r] = -1;
+      if (q < nm) {
+        const uint32_t g = missq[q];
+        const uint32_t id = uniq[g];
+        if (static_cast<int>(id % world) == rank) {
+          const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+          v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
+          dst[r] = static_cast<int>(g);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+}
+
+// ------------------------------------------------------------------ K5
+__device__ __forceinline__ void bag_range(const TableDev* td, const int64_t* bag_off, int B, int P, int s, int t,
+                                          int64_t* lo, int64_t* hi) {
+  if (bag_off) {
+    *lo = bag_off[static_cast<int64_t>(t) * B + s];
+    *hi = bag_off[static_cast<int64_t>(t) * B + s + 1];
+  } else {
+    *lo = td[t].base + static_cast<int64_t>(s) * P;
+    *hi = *lo + P;
+  }
+}
+
+// Row u's float4 #c of the compact unique-row buffer; invalid lookups read 0.
+__device__ __forceinline__ float4 load_row(const float* urows, uint32_t u, int D, int c) {
+  if (u == kInvalidSlot) return make_float4(0.f, 0.f, 0.f, 0.f);
+  return ldg4(urows + static_cast<int64_t>(u) * D + c * 4);
+}
+
+// Bags visited sample-major (q = s*T + t) so a warp writes a contiguous
+// stretch of the [B, T*D] output; R bags in flight per thread; each bag is
+// summed in lookup order.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
+                                                   const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
+                                                   const float* __restrict__ urows, float* __restrict__ out) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nbags = T * B;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
+    int lo[R], len[R];  // batch positions < 2^31 (checked by Engine::forward)
+    int maxlen = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      lo[r] = 0;
+      len[r] = 0;
+      if (q < nbags) {
+        const int s = q / T, t = q - s * T;
+        int64_t l64, h64;
+        bag_range(td, bag_off, B, P, s, t, &l64, &h64);
+        lo[r] = static_cast<int>(l64);
+        len[r] = static_cast<int>(h64 - l64);
+        maxlen = max(maxlen, len[r]);
+      }
+    }
+    float4 acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < maxlen; ++i) {
+      uint32_t u[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = add4(acc[r], load_row(urows, u[r], D, m.c));
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      if (q < nbags) st4(out + static_cast<int64_t>(q) * D + m.c * 4, acc[r]);  // q = s*T + t
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K6
+// Scatter tiles: a run of bags of one table (table-major).  Each block
+// aggregates the gradients of the tile's lookups per unique row in a shared
+// memory hash (kSlots rows) — hot rows (tiny tables, Zipf heads) collapse to
+// one global atomic per block — and sends rows that do not fit straight to
+// global float4 atomics.
+template <int VEC>
+struct ScatterSmem {
+  static constexpr int kFloats = 8192;  // 32 KB of fp32 accumulators
+  static constexpr int kSlots = kFloats / (VEC * 4);
+  uint32_t keys[kSlots];
+  float acc[kFloats];
+};
+
+template <int VEC>
+__device__ __forceinline__ int smem_slot(ScatterSmem<VEC>& sm, uint32_t u) {
+  constexpr int S = ScatterSmem<VEC>::kSlots;
+  uint32_t h = (u * 0x9E3779B1u) & (S - 1);
+  for (int probe = 0; probe < S / 2; ++probe) {
+    const uint32_t cur = atomicCAS(&sm.keys[h], kEmptyKey, u);
+    if (cur == kEmptyKey || cur == u) return static_cast<int>(h);
+    h = (h + 1) & (S - 1);
+  }
+  return -1;  // table full: caller falls back to a global atomic
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
+                                                      const int64_t* __restrict__ bag_off,
+                                                      const int4* __restrict__ stiles, int nstiles,
+                                                      const uint32_t* __restrict__ inv, const float* __restrict__ grad,
+                                                      float* __restrict__ ugrad) {
+  constexpr int D = VEC * 4;
+  constexpr int S = ScatterSmem<VEC>::kSlots;
+  constexpr int BAGS = kThreads / VEC;  // bags per block pass
+  __shared__ ScatterSmem<VEC> sm;
+  const int sub = threadIdx.x / VEC, c = threadIdx.x % VEC;
+  for (int st = blockIdx.x; st < nstiles; st += gridDim.x) {
+    const int4 tl = stiles[st];  // (table, first bag, end bag, -)
+    for (int i = threadIdx.x; i < S; i += kThreads) sm.keys[i] = kEmptyKey;
+    for (int i = threadIdx.x; i < ScatterSmem<VEC>::kFloats; i += kThreads) sm.acc[i] = 0.f;
+    __syncthreads();
+    for (int s = tl.y + sub; s < tl.z; s += BAGS) {
+      int64_t lo, hi;
+      bag_range(td, bag_off, B, P, s, tl.x, &lo, &hi);
+      const float4 gv = ld_stream4(grad + (static_cast<int64_t>(s) * T + tl.x) * D + c * 4);
+      for (int64_t i = lo; i < hi; ++i) {
+        const uint32_t u = inv[i];
+        if (u == kInvalidSlot) continue;
+        // the group's lane 0 claims the shared slot; the group shares it
+        const int lead = (threadIdx.x & 31) - c;
+        const unsigned gmask = VEC == 32 ? kFull : (((1u << VEC) - 1u) << lead);  // this bag's lanes
+        int slot = 0;
+        if (c == 0) slot = smem_slot(sm, u);
+        slot = __shfl_sync(gmask, slot, lead);
+        if (slot >= 0) {
+          float* a = sm.acc + slot * D + c * 4;
+          atomicAdd(a + 0, gv.x);
+          atomicAdd(a + 1, gv.y);
+          atomicAdd(a + 2, gv.z);
+          atomicAdd(a + 3, gv.w);
+        } else {
+          atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + c * 4), gv);
+        }
+      }
+    }
+    __syncthreads();
+    for (int r = sub; r < S; r += BAGS) {
+      const uint32_t u = sm.keys[r];
+      if (u == kEmptyKey) continue;
+      const float* a = sm.acc + r * D + c * 4;
+      atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + c * 4), make_float4(a[0], a[1], a[2], a[3]));
+    }
+    __syncthreads();
+  }
+}
+
+// SGD on every unique row: w = w_gathered - lr * g, written to the cache copy
+// (hits) or, for misses whose shard is in HBM, to the owning local shard.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                    const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                                                    const int32_t* __restrict__ usrc, const float* __restrict__ urows,
+                                                    const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
+                                                    int misses_local, int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      if (g >= U) continue;
+      const int32_t s = usrc[g];
+      float* dst = nullptr;
+      if (s >= 0) {
+        dst = cache + static_cast<int64_t>(s) * D;
+      } else if (misses_local) {
+        const uint32_t id = uniq[g];
+        if (static_cast<int>(id % world) == rank) dst = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+      }
+      if (!dst) continue;
+      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
+      st4(dst + m.c * 4, make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+    }
+  }
+}
+
+// SGD for cold rows held in pinned host memory (miss queue, side stream).
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                         const uint32_t* __restrict__ missq,
+                                                         const uint32_t* __restrict__ uniq,
+                                                         const uint16_t* __restrict__ utab, const float* __restrict__ urows,
+                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      if (q >= nm) continue;
+      const uint32_t g = missq[q];
+      const uint32_t id = uniq[g];
+      if (static_cast<int>(id % world) != rank) continue;
+      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
+      st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4,
+          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+    }
+  }
+}
+
+}  // namespace ec
