@@ -352,7 +352,7 @@ __device__ __forceinline__ float4 load_row(const float* urows, uint32_t u, int D
 // stretch of the [B, T*D] output; R bags in flight per thread; each bag is
 // summed in lookup order.
 template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
+__global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
                                                    const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
                                                    const float* __restrict__ urows, float* __restrict__ out) {
   constexpr int D = VEC * 4;
