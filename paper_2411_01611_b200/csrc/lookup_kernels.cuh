@@ -414,7 +414,7 @@ template <int VEC>
 __device__ __forceinline__ int smem_slot(ScatterSmem<VEC>& sm, uint32_t u) {
   constexpr int S = ScatterSmem<VEC>::kSlots;
   uint32_t h = (u * 0x9E3779B1u) & (S - 1);
-  for (int probe = 0; probe < S / 2; ++probe) {
+  for (int probe = 0; probe < 8; ++probe) {  // short probe: a full table must not serialise the block
     const uint32_t cur = atomicCAS(&sm.keys[h], kEmptyKey, u);
     if (cur == kEmptyKey || cur == u) return static_cast<int>(h);
     h = (h + 1) & (S - 1);
