@@ -447,10 +447,8 @@ void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st
   {
   PhaseScope ph(prof, kPhaseScatter, st);
   // ugrad rows were zeroed by k_gather
-  if (nstiles) {
-    k_scatter<VEC><<<std::min(nstiles, sm_count(device) * 4), kThreads, 0, st>>>(
-        tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, stiles.p, nstiles, inv.p, grad, ugrad.p);
-  }
+  k_scatter<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
+                                               inv.p, grad, ugrad.p);
   launched();
   }
   if (world > 1) {

@@ -16,8 +16,8 @@
 //                      hash slot and zeroes the unique's gradient row
 //   k_gather_host      pinned-host misses (side stream)
 //   k_pool             EmbeddingBag sum through inverse indices
-//   k_scatter          bag gradients -> unique rows, block-local shared-memory
-//                      aggregation (hot rows), global float4 atomics otherwise
+//   k_scatter          bag gradients -> unique rows: float4 REDG per distinct row
+//                      of a warp (equal rows pre-summed with shuffles)
 //   k_apply(_host)     SGD into cache rows / owning shard
 #pragma once
 
@@ -31,22 +31,23 @@ constexpr int kItems = 4;
 constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
 
 // ------------------------------------------------------------------ K1
-__device__ __forceinline__ uint32_t hash_insert(unsigned long long* tab, uint32_t mask, uint32_t shift,
-                                                uint32_t id, uint32_t lpos) {
+// Insert (id, lpos) starting at slot h whose current content `cur` was
+// already loaded; returns the slot holding id.  Packed words (id << 32 | pos)
+// make "keep the first position" a 64-bit atomicMin on an existing key.
+__device__ __forceinline__ uint32_t hash_insert_from(unsigned long long* tab, uint32_t mask, uint32_t h,
+                                                     unsigned long long cur, uint32_t id, uint32_t lpos) {
   const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
-  uint32_t h = hash_slot(id, shift);
   for (;;) {
-    unsigned long long cur = __ldcg(tab + h);
     if (cur == kEmptySlot) {
       cur = atomicCAS(tab + h, kEmptySlot, mine);
       if (cur == kEmptySlot) return h;
     }
     if (static_cast<uint32_t>(cur >> 32) == id) {
-      // same key: keep the smallest position (high words equal -> packed min)
       if (static_cast<uint32_t>(cur) > lpos) atomicMin(tab + h, mine);
       return h;
     }
     h = (h + 1) & mask;
+    cur = __ldcg(tab + h);
   }
 }
 
@@ -74,22 +75,33 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     live[j] = off < tile.count;
     id[j] = live[j] ? __ldcs(indices + tile.start + off) : kEmptyKey;
   }
+  unsigned peers[kItems];
+  uint32_t h[kItems];
+  unsigned long long cur[kItems];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    const uint32_t off = j * kThreads + threadIdx.x;
-    const int64_t p = tile.start + off;
     if (live[j] && id[j] >= t.rows) {
       atomicExch(c.err, 1);
       live[j] = false;
       id[j] = kEmptyKey;
     }
     // lanes holding the same id collapse to their lowest lane (= smallest position)
-    const unsigned peers = __match_any_sync(kFull, id[j]);
-    const int leader = __ffs(peers) - 1;
-    uint32_t h = 0;
-    if (live[j] && leader == lane_id()) h = hash_insert(t.hash, t.mask, t.shift, id[j], static_cast<uint32_t>(p - t.base));
-    h = __shfl_sync(kFull, h, leader);
-    if (live[j]) slot_of[p] = h;
+    peers[j] = __match_any_sync(kFull, id[j]);
+    h[j] = hash_slot(id[j], t.shift);
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j)  // home-slot probes of all items in flight together
+    cur[j] = (live[j] && __ffs(peers[j]) - 1 == lane_id()) ? __ldcg(t.hash + h[j]) : 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    const int64_t p = tile.start + off;
+    const int leader = __ffs(peers[j]) - 1;
+    uint32_t slot = 0;
+    if (live[j] && leader == lane_id())
+      slot = hash_insert_from(t.hash, t.mask, h[j], cur[j], id[j], static_cast<uint32_t>(p - t.base));
+    slot = __shfl_sync(kFull, slot, leader);
+    if (live[j]) slot_of[p] = slot;
     else if (off < tile.count) slot_of[p] = kInvalidSlot;  // out-of-range id: skipped downstream
   }
 }
@@ -132,7 +144,13 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t off = j * kThreads + threadIdx.x;
-    first[j] = off < tile.count && is_first(t, slot_of, tile.start + off, &h[j]);
+    h[j] = off < tile.count ? slot_of[tile.start + off] : kInvalidSlot;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint32_t off = j * kThreads + threadIdx.x;
+    first[j] = h[j] != kInvalidSlot &&
+               static_cast<uint32_t>(__ldcg(t.hash + h[j])) == static_cast<uint32_t>(tile.start + off - t.base);
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {  // position order within the tile: j-major, then thread
@@ -140,34 +158,37 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
     ex[j] = count + block_exclusive_scan<kThreads>(first[j] ? 1 : 0, sw, &tot);
     count += tot;
   }
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int excl = 0;
-    if (ti == 0) {
-      if (lane == 0) publish(status, kStatInc | static_cast<uint32_t>(count));
-    } else {
-      if (lane == 0) publish(status + ti, kStatAgg | static_cast<uint32_t>(count));
-      for (int k = ti - 1;; k -= 32) {
-        const int idx = k - lane;
-        unsigned long long v = kStatInc;  // before tile 0: an inclusive zero ends the walk
-        if (idx >= 0) {
-          do {
-            v = *reinterpret_cast<volatile unsigned long long*>(status + idx);
-          } while ((v >> 32) == 0);
-        }
-        const unsigned inc = __ballot_sync(kFull, (v >> 32) == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 31;
-        excl += __reduce_add_sync(kFull, lane <= stop ? static_cast<int>(static_cast<uint32_t>(v)) : 0);
-        if (inc) break;
-      }
-      if (lane == 0) publish(status + ti, kStatInc | static_cast<uint32_t>(excl + count));
+  // Block-wide decoupled look-back: each thread watches one predecessor per
+  // round; the walk stops at the nearest tile with an inclusive prefix.
+  if (threadIdx.x == 0) publish(status + ti, (ti == 0 ? kStatInc : kStatAgg) | static_cast<uint32_t>(count));
+  __shared__ int s_stop, s_sum;
+  int excl = 0;
+  for (int k = ti - 1; k >= 0; k -= kThreads) {
+    const int idx = k - static_cast<int>(threadIdx.x);
+    unsigned long long v = kStatInc;  // before tile 0: an inclusive zero ends the walk
+    if (idx >= 0) {
+      do {
+        v = *reinterpret_cast<volatile unsigned long long*>(status + idx);
+      } while ((v >> 32) == 0);
     }
-    if (lane == 0) {
-      s_excl = excl;
-      for (uint32_t tb = tile.ub_lo; tb < tile.ub_hi; ++tb) c.ubase[tb] = excl;  // tables starting here
-      if (ti == ntiles - 1)
-        for (int tb = tail_lo; tb <= T; ++tb) c.ubase[tb] = excl + count;  // trailing empty tables + total
-    }
+    if (threadIdx.x == 0) { s_stop = kThreads; s_sum = 0; }
+    __syncthreads();
+    if ((v >> 32) == 2) atomicMin(&s_stop, static_cast<int>(threadIdx.x));
+    __syncthreads();
+    const int stop = s_stop;
+    const int part = __reduce_add_sync(kFull, static_cast<int>(threadIdx.x) <= stop ? static_cast<int>(static_cast<uint32_t>(v)) : 0);
+    if (lane_id() == 0 && part) atomicAdd(&s_sum, part);
+    __syncthreads();
+    excl += s_sum;
+    __syncthreads();
+    if (stop < kThreads) break;
+  }
+  if (threadIdx.x == 0) {
+    if (ti > 0) publish(status + ti, kStatInc | static_cast<uint32_t>(excl + count));
+    s_excl = excl;
+    for (uint32_t tb = tile.ub_lo; tb < tile.ub_hi; ++tb) c.ubase[tb] = excl;  // tables starting here
+    if (ti == ntiles - 1)
+      for (int tb = tail_lo; tb <= T; ++tb) c.ubase[tb] = excl + count;  // trailing empty tables + total
   }
   __syncthreads();
   const int base = s_excl;
@@ -397,79 +418,66 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
 }
 
 // ------------------------------------------------------------------ K6
-// Scatter tiles: a run of bags of one table (table-major).  Each block
-// aggregates the gradients of the tile's lookups per unique row in a shared
-// memory hash (kSlots rows) — hot rows (tiny tables, Zipf heads) collapse to
-// one global atomic per block — and sends rows that do not fit straight to
-// global float4 atomics.
-template <int VEC>
-struct ScatterSmem {
-  static constexpr int kFloats = 8192;  // 32 KB of fp32 accumulators
-  static constexpr int kSlots = kFloats / (VEC * 4);
-  uint32_t keys[kSlots];
-  float acc[kFloats];
-};
-
-template <int VEC>
-__device__ __forceinline__ int smem_slot(ScatterSmem<VEC>& sm, uint32_t u) {
-  constexpr int S = ScatterSmem<VEC>::kSlots;
-  uint32_t h = (u * 0x9E3779B1u) & (S - 1);
-  for (int probe = 0; probe < 8; ++probe) {  // short probe: a full table must not serialise the block
-    const uint32_t cur = atomicCAS(&sm.keys[h], kEmptyKey, u);
-    if (cur == kEmptyKey || cur == u) return static_cast<int>(h);
-    h = (h + 1) & (S - 1);
-  }
-  return -1;  // table full: caller falls back to a global atomic
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(kThreads) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
-                                                      const int64_t* __restrict__ bag_off,
-                                                      const int4* __restrict__ stiles, int nstiles,
-                                                      const uint32_t* __restrict__ inv, const float* __restrict__ grad,
-                                                      float* __restrict__ ugrad) {
+// Bags visited table-major (q = t*B + s): the 32/VEC bags a warp holds are
+// consecutive samples of one table, so hot rows repeat inside the warp; lanes
+// with equal (row, component) are summed with shuffles first and one float4
+// REDG per distinct row goes to L2.  R bags in flight per thread.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
+                                                         const int64_t* __restrict__ bag_off,
+                                                         const uint32_t* __restrict__ inv, const float* __restrict__ grad,
+                                                         float* __restrict__ ugrad) {
   constexpr int D = VEC * 4;
-  constexpr int S = ScatterSmem<VEC>::kSlots;
-  constexpr int BAGS = kThreads / VEC;  // bags per block pass
-  __shared__ ScatterSmem<VEC> sm;
-  const int sub = threadIdx.x / VEC, c = threadIdx.x % VEC;
-  for (int st = blockIdx.x; st < nstiles; st += gridDim.x) {
-    const int4 tl = stiles[st];  // (table, first bag, end bag, -)
-    for (int i = threadIdx.x; i < S; i += kThreads) sm.keys[i] = kEmptyKey;
-    for (int i = threadIdx.x; i < ScatterSmem<VEC>::kFloats; i += kThreads) sm.acc[i] = 0.f;
-    __syncthreads();
-    for (int s = tl.y + sub; s < tl.z; s += BAGS) {
-      int64_t lo, hi;
-      bag_range(td, bag_off, B, P, s, tl.x, &lo, &hi);
-      const float4 gv = ld_stream4(grad + (static_cast<int64_t>(s) * T + tl.x) * D + c * 4);
-      for (int64_t i = lo; i < hi; ++i) {
-        const uint32_t u = inv[i];
-        if (u == kInvalidSlot) continue;
-        // the group's lane 0 claims the shared slot; the group shares it
-        const int lead = (threadIdx.x & 31) - c;
-        const unsigned gmask = VEC == 32 ? kFull : (((1u << VEC) - 1u) << lead);  // this bag's lanes
-        int slot = 0;
-        if (c == 0) slot = smem_slot(sm, u);
-        slot = __shfl_sync(gmask, slot, lead);
-        if (slot >= 0) {
-          float* a = sm.acc + slot * D + c * 4;
-          atomicAdd(a + 0, gv.x);
-          atomicAdd(a + 1, gv.y);
-          atomicAdd(a + 2, gv.z);
-          atomicAdd(a + 3, gv.w);
-        } else {
-          atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + c * 4), gv);
-        }
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nbags = T * B;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
+    int lo[R], len[R], maxlen = 0;
+    float4 gv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      lo[r] = 0;
+      len[r] = 0;
+      gv[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < nbags) {
+        const int t = q / B, s = q - t * B;
+        int64_t l64, h64;
+        bag_range(td, bag_off, B, P, s, t, &l64, &h64);
+        lo[r] = static_cast<int>(l64);
+        len[r] = static_cast<int>(h64 - l64);
+        maxlen = max(maxlen, len[r]);
+        gv[r] = ld_stream4(grad + (static_cast<int64_t>(s) * T + t) * D + m.c * 4);
       }
     }
-    __syncthreads();
-    for (int r = sub; r < S; r += BAGS) {
-      const uint32_t u = sm.keys[r];
-      if (u == kEmptyKey) continue;
-      const float* a = sm.acc + r * D + c * 4;
-      atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u) * D + c * 4), make_float4(a[0], a[1], a[2], a[3]));
+    maxlen = __reduce_max_sync(kFull, maxlen);
+    for (int i = 0; i < maxlen; ++i) {
+      uint32_t u[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float4 v = gv[r];
+        bool lead = u[r] != kInvalidSlot;
+        if (RPW > 1 && __any_sync(kFull, __popc(__match_any_sync(kFull, u[r])) > VEC)) {
+          // some row repeats in this warp: rotate by whole bags (same component c)
+#pragma unroll
+          for (int k = 1; k < RPW; ++k) {
+            const int src = (lane_id() + k * VEC) & 31;
+            const uint32_t uo = __shfl_sync(kFull, u[r], src);
+            const float4 o = make_float4(__shfl_sync(kFull, gv[r].x, src), __shfl_sync(kFull, gv[r].y, src),
+                                         __shfl_sync(kFull, gv[r].z, src), __shfl_sync(kFull, gv[r].w, src));
+            if (uo == u[r]) {
+              if (src < lane_id()) lead = false;  // a lower bag owns this row
+              else v = add4(v, o);
+            }
+          }
+        }
+        if (lead) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u[r]) * D + m.c * 4), v);
+      }
     }
-    __syncthreads();
   }
 }
 
