@@ -36,6 +36,8 @@ TB = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546,
 WORKLOADS = {
     "kaggle": dict(rows=KAGGLE, dim=16, batch=16384, pooling=1, alpha=1.05, cache_bytes=256 << 20,
                    storage="host", name="criteo-kaggle-shaped (BASELINE configs[1])"),
+    "kaggle_hbm": dict(rows=KAGGLE, dim=16, batch=16384, pooling=1, alpha=1.05, cache_bytes=256 << 20,
+                       storage="hbm", name="criteo-kaggle-shaped, cold rows in HBM (configs[1] variant)"),
     "cfg1": dict(rows=[1_000_000] * 8, dim=64, batch=4096, pooling=20, alpha=1.05, cache_bytes=0,
                  storage="hbm", name="8x1M zipf1.05 D64 b4096 P20 (BASELINE configs[0] shape)"),
     "tb": dict(rows=TB, dim=64, batch=65536, pooling=1, alpha=1.05, cache_bytes=1 << 30, storage="hbm",
