@@ -31,7 +31,10 @@
 //            cap_t = pow2 >= 2*min(max lookups, E_t); self-cleaning per batch
 //   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
 //            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
+#include <sys/mman.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -160,12 +163,54 @@ static uint32_t log2_ceil(uint64_t x) {
   return l;
 }
 
+// Pinned, GPU-mapped host tier.  Backed by 2 MiB pages where the kernel
+// allows (explicit hugetlb, else transparent huge pages via madvise) and then
+// registered with CUDA: random GPU reads of 64-256 B rows over the host link
+// then touch far fewer page translations than with 4 KiB pages, which
+// otherwise throttle the HBM kernels running beside them.  EC_HOST_ALLOC=cuda
+// selects plain cudaHostAlloc.
+void* alloc_host_tier(uint64_t bytes, bool* mmapped) {
+  const char* mode = std::getenv("EC_HOST_ALLOC");
+  void* p = nullptr;
+  *mmapped = false;
+  if (!mode || std::strcmp(mode, "cuda") != 0) {
+    const uint64_t huge = 2ull << 20;
+    const uint64_t len = (bytes + huge - 1) / huge * huge;
+    p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_HUGETLB, -1, 0);
+    if (p == MAP_FAILED) {
+      p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+      if (p != MAP_FAILED) madvise(p, len, MADV_HUGEPAGE);
+    }
+    if (p != MAP_FAILED) {
+      if (cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+        *mmapped = true;
+        return p;
+      }
+      cudaGetLastError();
+      munmap(p, len);
+    }
+    p = nullptr;
+  }
+  EC_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  return p;
+}
+
+void free_host_tier(void* p, uint64_t bytes, bool mmapped) {
+  if (!mmapped) {
+    cudaFreeHost(p);
+    return;
+  }
+  const uint64_t huge = 2ull << 20;
+  cudaHostUnregister(p);
+  munmap(p, (bytes + huge - 1) / huge * huge);
+}
+
 Engine::~Engine() {
   clear_graphs();
   if (ev_part) cudaEventDestroy(ev_part);
   if (ev_side) cudaEventDestroy(ev_side);
   if (side) cudaStreamDestroy(side);
-  if (store_host) cudaFreeHost(store_host);
+  if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
 }
 
@@ -207,8 +252,8 @@ void Engine::create(const ec_tables_config& c) {
     store_dev.alloc(store_elems);
     store_base = store_dev.p;
   } else {
-    EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&store_host), std::max<uint64_t>(store_elems, 1) * sizeof(float),
-                          cudaHostAllocMapped | cudaHostAllocPortable));
+    store_host_bytes = std::max<uint64_t>(store_elems, 1) * sizeof(float);
+    store_host = static_cast<float*>(alloc_host_tier(store_host_bytes, &store_host_mmapped));
     EC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&store_base), store_host, 0));
   }
   remap.alloc(remap_off[T]);

@@ -96,6 +96,8 @@ struct Engine {
 
   DevBuf<float> store_dev;
   float* store_host = nullptr;  // pinned, mapped
+  uint64_t store_host_bytes = 0;
+  bool store_host_mmapped = false;
   float* store_base = nullptr;  // device-visible base of the shard
   DevBuf<int32_t> remap;
   DevBuf<unsigned long long> hash;
