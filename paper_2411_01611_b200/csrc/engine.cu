@@ -154,7 +154,13 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
 static int persistent_grid(int device) { return sm_count(device) * 8; }
 // Row kernels share the SMs with the side-stream host-link kernels (1 CTA/SM,
 // ~48 regs x 256 threads each): size the main grids so every CTA is resident.
-int Engine::host_grid() const { return sm_count(device); }
+int Engine::host_grid() const {
+  static const int env = [] {
+    const char* v = std::getenv("EC_HOST_CTAS");
+    return v ? std::atoi(v) : 0;
+  }();
+  return env > 0 ? env : sm_count(device);
+}
 int Engine::row_grid() const { return sm_count(device) * (storage == EC_STORAGE_HOST ? 3 : 4); }
 
 static uint32_t log2_ceil(uint64_t x) {
