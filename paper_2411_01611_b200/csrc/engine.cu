@@ -152,14 +152,18 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
 
 // ------------------------------------------------------------ host side
 static int persistent_grid(int device) { return sm_count(device) * 8; }
-// Row kernels share the SMs with the side-stream host-link kernels (1 CTA/SM,
-// ~48 regs x 256 threads each): size the main grids so every CTA is resident.
+// Row kernels share the SMs with the side-stream host-link kernels: size the
+// main grids so every CTA stays resident beside them.
 int Engine::host_grid() const {
   static const int env = [] {
     const char* v = std::getenv("EC_HOST_CTAS");
     return v ? std::atoi(v) : 0;
   }();
-  return env > 0 ? env : sm_count(device);
+  // 32 CTAs x 256 threads keep ~8k row reads in flight, enough to saturate the
+  // host link for 64-256 B rows, while leaving the L2/HBM request queues to the
+  // main-stream kernels (measured: 8 CTAs starve the link, >= 148 slow the
+  // concurrent HBM gather 4x)
+  return env > 0 ? env : 32;
 }
 int Engine::row_grid() const { return sm_count(device) * (storage == EC_STORAGE_HOST ? 3 : 4); }
 
