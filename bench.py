@@ -141,21 +141,25 @@ def gen_batches(ec, torch, dists, wl, rank, nb):
 
 
 def phase_bytes(st, wl, T):
-    """Algorithmic bytes per step by phase (SURVEY §8d definitions; i = s = 4 B)."""
+    """Algorithmic bytes per launch of each kernel (i = s = 4 B; definitions in
+    DESIGN.md §4 following SURVEY.md §8d).  n lookups, U unique rows, H cache
+    hits, M misses, row = D*4 bytes."""
     D, B, P = wl["dim"], wl["batch"], wl["pooling"]
     n = st["lookups"]
     U, H, M = st["unique_rows"], st["hit_rows"], st["miss_rows"]
     row = D * 4
-    hbm_rows = U if wl["storage"] == "hbm" else H
+    hbm_src = U if wl["storage"] == "hbm" else H      # rows k_gather reads from HBM
     host_rows = 0 if wl["storage"] == "hbm" else M
     return {
-        "dedup": n * 4 + n * 4 + U * 4,
-        "partition": U * 4 * 3,
-        "gather_hbm": hbm_rows * row * 2 + U * 4,
-        "gather_host": host_rows * row * 2 + host_rows * 4,
-        "pool": n * 4 + n * row + B * T * row,
-        "grad_scatter": U * row + B * T * row + n * 4 + n * row,
-        "sgd_apply": U * row * 3 + U * 4,
+        "k_insert": n * 4 + n * 4,                     # ids in, slot_of out
+        "k_compact": n * 4 + U * (4 + 4 + 2),          # slot_of in; uniq, uslot, utab out
+        "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out
+        "k_gather": U * 4 + hbm_src * row + U * row + U * row,       # usrc in, rows in, urows out, ugrad zeroed
+        "k_gather_host": host_rows * (4 + row + row),  # missq in, host rows in (host link), urows out
+        "k_pool": n * 4 + n * row + B * T * row,       # inverse, rows, pooled out
+        "k_scatter": B * T * row + n * 4 + n * row,    # grads in, inverse in, row-grad reductions
+        "k_apply": (U - host_rows) * (4 + row * 3),    # usrc, urows, ugrad in, rows out
+        "k_apply_host": host_rows * (4 + row * 3),
     }
 
 
@@ -278,7 +282,7 @@ def run_ours(args, wl):
     tot_ms = sum(p["ms_per_call"] for p in phases.values())
     for p in phases.values():
         p["share"] = round(p["ms_per_call"] / tot_ms, 3)
-    hbm_phases = {k: v for k, v in phases.items() if k not in ("gather_host", "exchange")}
+    hbm_phases = {k: v for k, v in phases.items() if k not in ("k_gather_host", "k_apply_host", "exchange")}
     dom = max(hbm_phases, key=lambda k: hbm_phases[k]["ms_per_call"])
     dom_gbs = hbm_phases[dom]["gbs"]
     step_alg = sum(mean_bytes.values())

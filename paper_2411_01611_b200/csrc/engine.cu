@@ -510,19 +510,22 @@ void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st
     PhaseScope ph(prof, kPhaseExchange, st);
     exchange_bwd(lr, st);
   }
-  PhaseScope ph(prof, kPhaseApply, st);
   const bool host = storage == EC_STORAGE_HOST;
   if (host) {  // cold rows written back over the host link on the side stream
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    PhaseScope ph(prof, kPhaseApplyHost, side);
     k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p,
                                                               lr, rank, world);
     launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
-  k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
-                                             host ? 0 : 1, rank, world);
-  launched();
+  {
+    PhaseScope ph(prof, kPhaseApply, st);
+    k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
+                                               host ? 0 : 1, rank, world);
+    launched();
+  }
   if (host) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
 }
 
@@ -609,10 +612,13 @@ void Engine::clear_graphs() {
 
 void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
   {
-    PhaseScope ph(prof, kPhaseDedup, st);
     if (ntiles) {
-      k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T));
-      launched();
+      {
+        PhaseScope ph(prof, kPhaseInsert, st);
+        k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T));
+        launched();
+      }
+      PhaseScope ph(prof, kPhaseCompact, st);
       k_compact<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T),
                                              ntiles, tail_lo, uniq.p, uslot.p, utab.p);
       launched();
@@ -621,7 +627,7 @@ void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
     }
   }
   {
-    PhaseScope ph(prof, kPhasePartition, st);
+    PhaseScope ph(prof, kPhaseInversePartition, st);
     k_inverse_partition<<<ntiles + sm_count(device) * 2, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p, ntiles,
                                                                           static_cast<int>(T), ctr.p, uniq.p, utab.p,
                                                                           usrc.p, missq.p);

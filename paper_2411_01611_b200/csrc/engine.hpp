@@ -40,8 +40,9 @@ inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 4; }
 
 struct Exchange;  // exchange.cu
 
-enum { kPhaseDedup = 0, kPhasePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange, kPhasePool,
-       kPhaseScatter, kPhaseApply, kNumPhases };
+// One timing slot per kernel of the batch pipeline (ec_tables_profile_read order).
+enum { kPhaseInsert = 0, kPhaseCompact, kPhaseInversePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange,
+       kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kNumPhases };
 
 // Optional per-phase CUDA-event timing on the launching streams.
 struct Profiler {

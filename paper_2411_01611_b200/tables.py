@@ -65,7 +65,8 @@ class EmbeddingTables:
         check(N.lib().ec_tables_memory(self._h, C.byref(d), C.byref(h)))
         return {"device_bytes": d.value, "host_bytes": h.value}
 
-    PHASES = ("dedup", "partition", "gather_hbm", "gather_host", "exchange", "pool", "grad_scatter", "sgd_apply")
+    PHASES = ("k_insert", "k_compact", "k_inverse_partition", "k_gather", "k_gather_host", "exchange", "k_pool",
+              "k_scatter", "k_apply", "k_apply_host")
 
     def use_graphs(self, enable: bool = True):
         """CUDA-graph replay of forward/backward (needs a non-default stream)."""
@@ -76,8 +77,8 @@ class EmbeddingTables:
         check(N.lib().ec_tables_profile(self._h, 1 if enable else 0))
 
     def profile_read(self, reset: bool = True):
-        ms = np.zeros(8, np.float64)
-        calls = np.zeros(8, np.uint64)
+        ms = np.zeros(len(self.PHASES), np.float64)
+        calls = np.zeros(len(self.PHASES), np.uint64)
         launches = C.c_uint64()
         check(N.lib().ec_tables_profile_read(self._h, ms.ctypes.data, calls.ctypes.data, C.byref(launches),
                                              1 if reset else 0))
