@@ -319,6 +319,25 @@ int ec_export_rows(ec_tables t, uint32_t table, float* rows_host);
 int ec_comm_unique_id(uint8_t* id128_host);
 int ec_tables_attach_comm(ec_tables t, const uint8_t* id128_host);
 
+/* Host-side sharding math (no GPU): rows of each table owned by `rank`
+ * (owner(id) = id % world), and the per-batch exchange plan of `rank` from the
+ * all-gathered count matrix counts[r*(world+1) + o] = requests rank r sends to
+ * owner o (o < world) and rank r's cache-hit count (o = world): send/recv
+ * counts and offsets per peer, and every rank's hit-list count and offset. */
+int ec_shard_rows(const uint64_t* rows_host, uint32_t num_tables, int world, int rank, uint64_t* local_rows_host);
+int ec_exchange_plan(const int* counts_host, int world, int rank, int64_t* send_cnt, int64_t* send_off,
+                     int64_t* recv_cnt, int64_t* recv_off, int64_t* hot_cnt, int64_t* hot_off);
+
+/* In-process loopback group: `n` ranks (member r has rank r of world n) on one
+ * device, driven in lock step with device-to-device copies in place of NCCL.
+ * Same routing, owner serve, gradient return and rank-ordered replica update
+ * as the NCCL path; used to exercise the sharded data path on one GPU. */
+typedef struct ec_group_s* ec_group;
+int ec_group_create(ec_tables* members, int n, ec_group* out);
+void ec_group_destroy(ec_group g);
+int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs_dev, void* stream);
+int ec_group_lookup_bwd(ec_group g, const float* const* grads_dev, float lr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

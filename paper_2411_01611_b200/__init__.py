@@ -37,7 +37,7 @@ __all__ = [
     "delta_comm", "CachePlan", "optimal_cache_size_scan", "optimal_cache_size_search", "memory_io_proxy",
     "place_topk_global", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
     "SimResult", "measure_unique", "simulate_epoch", "Trace", "classify_samples", "build_schedule",
-    "SampleClasses", "BatchSchedule", "EmbeddingTables",
+    "SampleClasses", "BatchSchedule", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
 ]
 
 kCostUnitsNote = "one unit = one embedding vector = one transmitted index"
@@ -520,4 +520,4 @@ def build_schedule(trace: Trace, cache_ids, batch_size: int, shuffle_seed: Optio
     return BatchSchedule(pack(order[:h]), pack(order[h:]), batch_size)
 
 
-from .tables import EmbeddingTables  # noqa: E402
+from .tables import EmbeddingGroup, EmbeddingTables, exchange_plan, shard_rows  # noqa: E402

@@ -157,11 +157,17 @@ _SIGS = {
     "ec_export_rows": [vp, u32, vp],
     "ec_comm_unique_id": [vp],
     "ec_tables_attach_comm": [vp, vp],
+    "ec_shard_rows": [vp, u32, C.c_int, C.c_int, vp],
+    "ec_exchange_plan": [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp],
+    "ec_group_create": [vp, C.c_int, P(vp)],
+    "ec_group_destroy": [vp],
+    "ec_group_lookup_fwd": [vp, P(Batch), vp, vp],
+    "ec_group_lookup_bwd": [vp, vp, f32, vp],
 }
 _RESTYPE = {
     "ec_last_error": C.c_char_p, "ec_version": C.c_char_p, "ec_cost_units_note": C.c_char_p,
     "ec_rng_algorithm": C.c_char_p, "ec_substream_seed": u64, "ec_dist_size": u64,
-    "ec_dist_destroy": None, "ec_sampler_destroy": None, "ec_tables_destroy": None,
+    "ec_dist_destroy": None, "ec_sampler_destroy": None, "ec_tables_destroy": None, "ec_group_destroy": None,
 }
 
 _lib = None

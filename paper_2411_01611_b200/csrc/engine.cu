@@ -464,8 +464,21 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   have_geom = true;
 }
 
+#define EC_DISPATCH_VEC(FN, ...)                                                  \
+  switch (D / 4) {                                                                \
+    case 1: FN<1>(__VA_ARGS__); break;                                            \
+    case 2: FN<2>(__VA_ARGS__); break;                                            \
+    case 4: FN<4>(__VA_ARGS__); break;                                            \
+    case 8: FN<8>(__VA_ARGS__); break;                                            \
+    case 16: FN<16>(__VA_ARGS__); break;                                          \
+    case 32: FN<32>(__VA_ARGS__); break;                                          \
+    default: invalid("dim must be 4, 8, 16, 32, 64 or 128 for the lookup kernels"); \
+  }
+
+// K3 for rows this rank holds: pinned-host misses on the side stream, cache
+// hits and local-HBM misses on the main stream.
 template <int VEC>
-void Engine::launch_row_kernels_fwd(cudaStream_t st) {
+void Engine::fwd_gather_local(cudaStream_t st) {
   const int grid = row_grid();
   if (storage == EC_STORAGE_HOST) {
     // host misses on the side stream, overlapping the HBM hit gather
@@ -479,37 +492,36 @@ void Engine::launch_row_kernels_fwd(cudaStream_t st) {
     launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
-  {
   PhaseScope ph(prof, kPhaseGather, st);
   k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
                                               ugrad.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
   launched();
-  }
-  if (world > 1) {
-    PhaseScope ph(prof, kPhaseExchange, st);
-    exchange_fwd(st);
-  }
+}
+
+// K5 once every unique row is present (side stream joined).
+template <int VEC>
+void Engine::fwd_pool(cudaStream_t st) {
   if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PhaseScope ph(prof, kPhasePool, st);
-  k_pool<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
-                                            inv.p, urows.p, out_ptr);
+  k_pool<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
+                                                  inv.p, urows.p, out_ptr);
   launched();
 }
 
 template <int VEC>
-void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st) {
-  const int grid = row_grid();
-  {
+void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
   // ugrad rows were zeroed by k_gather
-  k_scatter<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
-                                               inv.p, grad, ugrad.p);
+  k_scatter<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+                                                     bag_off, inv.p, grad, ugrad.p);
   launched();
-  }
-  if (world > 1) {
-    PhaseScope ph(prof, kPhaseExchange, st);
-    exchange_bwd(lr, st);
-  }
+}
+
+// K6b for rows this rank applies itself: misses it owns (HBM, or pinned host
+// on the side stream) and — single rank only — cache hits.  With world > 1
+// the replicated hot rows are updated by the rank-ordered exchange instead.
+template <int VEC>
+void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
   if (host) {  // cold rows written back over the host link on the side stream
     EC_CUDA(cudaEventRecord(ev_part, st));
@@ -522,26 +534,17 @@ void Engine::launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st
   }
   {
     PhaseScope ph(prof, kPhaseApply, st);
-    k_apply<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr, cache.p,
-                                               host ? 0 : 1, rank, world);
+    k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
+                                                     cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
     launched();
   }
   if (host) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
 }
 
-#define EC_DISPATCH_VEC(FN, ...)                                                  \
-  switch (D / 4) {                                                                \
-    case 1: FN<1>(__VA_ARGS__); break;                                            \
-    case 2: FN<2>(__VA_ARGS__); break;                                            \
-    case 4: FN<4>(__VA_ARGS__); break;                                            \
-    case 8: FN<8>(__VA_ARGS__); break;                                            \
-    case 16: FN<16>(__VA_ARGS__); break;                                          \
-    case 32: FN<32>(__VA_ARGS__); break;                                          \
-    default: invalid("dim must be 4, 8, 16, 32, 64 or 128 for the lookup kernels"); \
-  }
 
-void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
+void Engine::forward_prologue(const ec_batch& b, float* out, cudaStream_t st) {
   if (!b.table_offsets_host || !b.indices_dev) invalid("batch needs indices and table offsets");
+  if (!out) invalid("null output");
   if (b.batch_size < 1 || b.batch_size > max_b) invalid("batch_size out of [1, max_batch_size]");
   if (b.table_offsets_host[0] != 0) invalid("table_offsets[0] must be 0");
   for (uint32_t t = 0; t < T; ++t) {
@@ -552,14 +555,35 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
       invalid("table " + std::to_string(t) + ": fixed pooling needs batch_size*pooling lookups");
   }
   if (b.table_offsets_host[T] >= (int64_t{1} << 31)) invalid("a batch holds at most 2^31-1 lookups");
-  if (world > 1 && !comm_ready()) invalid("world > 1 needs ec_tables_attach_comm");
+  if (world > 1 && !comm_ready()) invalid("world > 1 needs ec_tables_attach_comm (or a loopback group)");
   use_device(device);
   set_geometry(b, st);
   bag_off = b.bag_offsets_dev;
   out_ptr = out;
-  const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
-  run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
+}
+
+void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
+  if (in_group) invalid("this rank belongs to a loopback group: use ec_group_lookup_fwd");
+  forward_prologue(b, out, st);
+  if (world == 1) {
+    const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
+    run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
+  } else {
+    enqueue_dedup_partition(b.indices_dev, st);
+    gather_local(st);
+    exchange_fwd(st);  // K4: remote misses fetched from their owners
+    pool(st);
+  }
   have_fwd = true;
+}
+
+void Engine::gather_local(cudaStream_t st) { EC_DISPATCH_VEC(fwd_gather_local, st); }
+void Engine::pool(cudaStream_t st) { EC_DISPATCH_VEC(fwd_pool, st); }
+void Engine::scatter_and_apply_local(const float* grad, float lr, cudaStream_t st) {
+  if (!grad) invalid("null gradient");
+  use_device(device);
+  EC_DISPATCH_VEC(bwd_scatter, grad, st);
+  EC_DISPATCH_VEC(bwd_apply_local, lr, st);
 }
 
 // Replay a captured CUDA graph of the per-batch kernel sequence when the
@@ -611,6 +635,12 @@ void Engine::clear_graphs() {
 }
 
 void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
+  enqueue_dedup_partition(indices, st);
+  gather_local(st);
+  pool(st);
+}
+
+void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   {
     if (ntiles) {
       {
@@ -633,17 +663,22 @@ void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
                                                                           usrc.p, missq.p);
     launched();
   }
-  EC_DISPATCH_VEC(launch_row_kernels_fwd, st);
 }
 
 void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   if (!have_fwd) invalid("ec_lookup_bwd needs a preceding ec_lookup_fwd");
+  if (in_group) invalid("this rank belongs to a loopback group: use ec_group_lookup_bwd");
   if (!grad) invalid("null gradient");
   use_device(device);
-  uint32_t lr_bits;
-  std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
-  const GraphKey key{1, grad, bag_off, out_ptr, lr_bits};
-  run_maybe_graphed(key, st, [&] { EC_DISPATCH_VEC(launch_row_kernels_bwd, grad, lr, st); });
+  if (world == 1) {
+    uint32_t lr_bits;
+    std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
+    const GraphKey key{1, grad, bag_off, out_ptr, lr_bits};
+    run_maybe_graphed(key, st, [&] { scatter_and_apply_local(grad, lr, st); });
+  } else {
+    scatter_and_apply_local(grad, lr, st);
+    exchange_bwd(lr, st);  // remote misses -> owners, replicated hot rows in rank order
+  }
 }
 
 void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
@@ -707,10 +742,6 @@ Profiler::~Profiler() {
 
 // ===================================================================== ABI
 using namespace ec;
-
-struct ec_tables_s {
-  Engine e;
-};
 
 static Engine& E(ec_tables t) {
   if (!t) invalid("null tables handle");

@@ -162,10 +162,25 @@ struct Engine {
   void forward(const ec_batch& b, float* out, cudaStream_t st);
   void backward(const float* grad, float lr, cudaStream_t st);
   void read_counters(cudaStream_t st, std::vector<int>& h);
-  template <int VEC> void launch_row_kernels_fwd(cudaStream_t st);
-  template <int VEC> void launch_row_kernels_bwd(const float* grad, float lr, cudaStream_t st);
+  template <int VEC> void fwd_gather_local(cudaStream_t st);
+  template <int VEC> void fwd_pool(cudaStream_t st);
+  template <int VEC> void bwd_scatter(const float* grad, cudaStream_t st);
+  template <int VEC> void bwd_apply_local(float lr, cudaStream_t st);
+  void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
+  void forward_prologue(const ec_batch& b, float* out, cudaStream_t st);
+  void gather_local(cudaStream_t st);
+  void pool(cudaStream_t st);
+  void scatter_and_apply_local(const float* grad, float lr, cudaStream_t st);
 
   // multi-GPU (exchange.cu)
+  bool in_group = false;  // member of an in-process loopback group
+  void ex_init(int W);
+  void ex_route(cudaStream_t st);
+  void ex_plan();
+  void ex_serve(cudaStream_t st);
+  void ex_unpack(cudaStream_t st);
+  void ex_pack_bwd(cudaStream_t st);
+  void ex_apply_bwd(float lr, cudaStream_t st);
   bool comm_ready() const;
   void attach_comm(const uint8_t* id128);
   void destroy_comm();
@@ -175,3 +190,8 @@ struct Engine {
 };
 
 }  // namespace ec
+
+// Opaque ABI handle (include/embcomm_gpu.h).
+struct ec_tables_s {
+  ec::Engine e;
+};

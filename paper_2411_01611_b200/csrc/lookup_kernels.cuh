@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                                                     const int32_t* __restrict__ usrc, const float* __restrict__ urows,
                                                     const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
-                                                    int misses_local, int rank, int world) {
+                                                    int hits, int misses_local, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
       const int32_t s = usrc[g];
       float* dst = nullptr;
       if (s >= 0) {
-        dst = cache + static_cast<int64_t>(s) * D;
+        if (hits) dst = cache + static_cast<int64_t>(s) * D;
       } else if (misses_local) {
         const uint32_t id = uniq[g];
         if (static_cast<int>(id % world) == rank) dst = td[utab[g]].store + static_cast<int64_t>(id / world) * D;

@@ -192,3 +192,64 @@ class EmbeddingTables:
         buf = (C.c_uint8 * 128)(*uid)
         check(N.lib().ec_tables_attach_comm(self._h, buf))
 
+
+
+def shard_rows(rows: Sequence[int], world: int, rank: int) -> list[int]:
+    """Rows of each table owned by `rank` under owner(id) = id % world."""
+    r = (C.c_uint64 * len(rows))(*rows)
+    out = np.zeros(len(rows), np.uint64)
+    check(N.lib().ec_shard_rows(r, len(rows), world, rank, out.ctypes.data))
+    return [int(x) for x in out]
+
+
+def exchange_plan(counts, world: int, rank: int) -> dict:
+    """Per-batch exchange plan of `rank` from the all-gathered count matrix
+    (world x (world+1): requests to each owner, then the hit count)."""
+    m = np.ascontiguousarray(counts, dtype=np.int32).reshape(world, world + 1)
+    outs = [np.zeros(world, np.int64) for _ in range(6)]
+    check(N.lib().ec_exchange_plan(m.ctypes.data, world, rank, *[o.ctypes.data for o in outs]))
+    return dict(zip(("send_cnt", "send_off", "recv_cnt", "recv_off", "hot_cnt", "hot_off"), outs))
+
+
+class EmbeddingGroup:
+    """In-process loopback group: ranks 0..n-1 of row-sharded tables on one
+    device, driven in lock step (same routing / serve / gradient return /
+    rank-ordered replica update as the NCCL path, device copies as transport)."""
+
+    def __init__(self, members: Sequence[EmbeddingTables]):
+        self.members = list(members)
+        arr = (C.c_void_p * len(self.members))(*[m._h.value for m in self.members])
+        h = C.c_void_p()
+        check(N.lib().ec_group_create(arr, len(self.members), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().ec_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, indices, table_offsets, batch_size: int, pooling: int):
+        """indices[r]: rank r's int32 CUDA ids; same geometry on every rank."""
+        torch = self.members[0].torch
+        n = len(self.members)
+        offs = np.ascontiguousarray(table_offsets, dtype=np.int64)
+        batches = (N.Batch * n)(*[N.Batch(indices[r].data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), None,
+                                          batch_size, pooling) for r in range(n)])
+        outs = [torch.empty((batch_size, m.T * m.D), dtype=torch.float32, device=indices[0].device)
+                for m in self.members]
+        optr = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+        for m in self.members:
+            m._offsets = offs
+        check(N.lib().ec_group_lookup_fwd(self._h, batches, optr, _stream_ptr(torch, self.members[0].device)))
+        return outs
+
+    def backward(self, grads, lr: float):
+        torch = self.members[0].torch
+        gptr = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        check(N.lib().ec_group_lookup_bwd(self._h, gptr, lr, _stream_ptr(torch, self.members[0].device)))
