@@ -285,6 +285,11 @@ def run_ours(args, wl):
     hbm_phases = {k: v for k, v in phases.items() if k not in ("k_gather_host", "k_apply_host", "exchange")}
     dom = max(hbm_phases, key=lambda k: hbm_phases[k]["ms_per_call"])
     dom_gbs = hbm_phases[dom]["gbs"]
+    # dram bytes per launch of that kernel from the committed ncu --set full capture
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"r1_{args.workload}_traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(dom)
     step_alg = sum(mean_bytes.values())
 
     s0 = stats[0]
@@ -311,7 +316,10 @@ def run_ours(args, wl):
                 "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int(T * 8 * 2 + 72)},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": round(dom_gbs / peak, 4), "traffic": None,
+                     "frac": round(dom_gbs / peak, 4), "traffic": traffic,
+                     "alg_bytes_per_launch": hbm_phases[dom]["alg_bytes"],
+                     "traffic_source": (f"profiles/r1_{args.workload}_traffic.json (ncu --set full, dram read+write "
+                                        "bytes per launch)") if traffic else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
         "step_alg_bytes": int(step_alg),
         "step_alg_gbs": round(step_alg / (ms * 1e-3) / 1e9, 1),
