@@ -285,6 +285,14 @@ typedef struct {
  * K1..K5 on `stream` (host misses on an internal side stream joined by an
  * event).  No host synchronisation unless world > 1. */
 int ec_lookup_fwd(ec_tables t, const ec_batch* batch, float* out_dev, void* stream);
+/* Start the next batch while the current one finishes (single rank): its
+ * dedup, hit/miss partition and pinned-host miss gather run on internal
+ * streams into a second buffer set, overlapping the current backward; the
+ * next ec_lookup_fwd with the same indices_dev consumes them.  Host-tier rows
+ * the current backward updates are refreshed in the prefetched copy, so
+ * results equal the unpipelined sequence.  Same geometry as the last forward
+ * required. */
+int ec_lookup_prefetch(ec_tables t, const ec_batch* batch, void* stream);
 /* Backward of the last forward: grad_dev laid out like out_dev; applies
  * w <- w - lr * (sum of grads of every lookup of the row) to the cache copy
  * of cached rows and to the owning shard of the others (K6). */

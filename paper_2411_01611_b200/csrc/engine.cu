@@ -220,6 +220,9 @@ Engine::~Engine() {
   if (ev_part) cudaEventDestroy(ev_part);
   if (ev_side) cudaEventDestroy(ev_side);
   if (side) cudaStreamDestroy(side);
+  if (pstream) cudaStreamDestroy(pstream);
+  if (ev_fwd) cudaEventDestroy(ev_fwd);
+  if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
 }
@@ -271,20 +274,23 @@ void Engine::create(const ec_tables_config& c) {
   hash.alloc(hash_off[T]);
   EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
   const uint64_t N = max_n * T;
-  slot_of.alloc(N);
-  inv.alloc(N);
-  uniq.alloc(N);
-  uslot.alloc(N);
-  usrc.alloc(N);
-  missq.alloc(N);
-  utab.alloc(N);
-  urows.alloc(N * D);
-  ugrad.alloc(N * D);
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
+  for (BatchBufs& b : bb) {
+    b.slot_of.alloc(N);
+    b.inv.alloc(N);
+    b.uniq.alloc(N);
+    b.uslot.alloc(N);
+    b.usrc.alloc(N);
+    b.missq.alloc(N);
+    b.utab.alloc(N);
+    b.urows.alloc(N * D);
+    b.ugrad.alloc(N * D);
+    b.status.alloc(max_tiles + 1);
+    b.ctr.alloc(counters_size(T));
+    EC_CUDA(cudaMemset(b.ctr.p, 0, b.ctr.bytes()));
+  }
+  select(0);
   tiles.alloc(max_tiles);
-  status.alloc(max_tiles + 1);
-  ctr.alloc(counters_size(T));
-  EC_CUDA(cudaMemset(ctr.p, 0, ctr.bytes()));
   tdev.alloc(T);
   td_host.resize(T);
   for (uint32_t t = 0; t < T; ++t) {
@@ -300,15 +306,33 @@ void Engine::create(const ec_tables_config& c) {
   }
   EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
   EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  EC_CUDA(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
 }
 
+void Engine::select(int i) {
+  cur = i;
+  BatchBufs& b = bb[i];
+  slot_of = view(b.slot_of);
+  inv = view(b.inv);
+  uniq = view(b.uniq);
+  uslot = view(b.uslot);
+  missq = view(b.missq);
+  usrc = view(b.usrc);
+  utab = view(b.utab);
+  urows = view(b.urows);
+  ugrad = view(b.ugrad);
+  status = view(b.status);
+  ctr = view(b.ctr);
+}
+
 uint64_t Engine::device_bytes() const {
-  return store_dev.bytes() + remap.bytes() + hash.bytes() + cache.bytes() + slot_of.bytes() + inv.bytes() +
-         uniq.bytes() + uslot.bytes() + usrc.bytes() + missq.bytes() + utab.bytes() + urows.bytes() +
-         ugrad.bytes() + tiles.bytes() + status.bytes() + stiles.bytes() + ctr.bytes() + cache_ids.bytes() + cache_tab.bytes() +
+  return store_dev.bytes() + remap.bytes() + hash.bytes() + cache.bytes() + bb[0].bytes() + bb[1].bytes() +
+         tiles.bytes() + stiles.bytes() + cache_ids.bytes() + cache_tab.bytes() +
          exch_bytes();
 }
 
@@ -422,7 +446,9 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   bool same = have_geom && b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed;
   for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
   if (same) return;
+  if (bb[cur ^ 1].pending) drop_prefetch(st);
   clear_graphs();
+  ++geom_version;
   geom_off.assign(b.table_offsets_host, b.table_offsets_host + T + 1);
   std::vector<Tile> tl;
   std::vector<int> ft(T + 1);
@@ -454,7 +480,9 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   nstiles = static_cast<int>(sc.size());
   EC_CUDA(cudaStreamSynchronize(st));
   if (ntiles) EC_CUDA(cudaMemcpy(tiles.p, tl.data(), tl.size() * sizeof(Tile), cudaMemcpyHostToDevice));
-  if (status.n < static_cast<size_t>(ntiles) + 1) status.alloc(ntiles + 1);
+  for (BatchBufs& bs : bb)
+    if (bs.status.n < static_cast<size_t>(ntiles) + 1) bs.status.alloc(ntiles + 1);
+  select(cur);
   if (stiles.n < sc.size()) stiles.alloc(sc.size());
   if (nstiles) EC_CUDA(cudaMemcpy(stiles.p, sc.data(), sc.size() * sizeof(int4), cudaMemcpyHostToDevice));
   EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
@@ -480,7 +508,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
 template <int VEC>
 void Engine::fwd_gather_local(cudaStream_t st) {
   const int grid = row_grid();
-  if (storage == EC_STORAGE_HOST) {
+  if (storage == EC_STORAGE_HOST && !consuming_prefetch) {
     // host misses on the side stream, overlapping the HBM hit gather
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
@@ -501,7 +529,7 @@ void Engine::fwd_gather_local(cudaStream_t st) {
 // K5 once every unique row is present (side stream joined).
 template <int VEC>
 void Engine::fwd_pool(cudaStream_t st) {
-  if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  if (storage == EC_STORAGE_HOST && !consuming_prefetch) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PhaseScope ph(prof, kPhasePool, st);
   k_pool<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
                                                   inv.p, urows.p, out_ptr);
@@ -526,9 +554,12 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   if (host) {  // cold rows written back over the host link on the side stream
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    const BatchBufs& nx = bb[cur ^ 1];
+    if (nx.pending) EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cudaEventWaitExternal));  // its gather precedes our patch
     PhaseScope ph(prof, kPhaseApplyHost, side);
     k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p,
-                                                              lr, rank, world);
+                                                              lr, rank, world, nx.pending ? nx.usrc.p : nullptr,
+                                                              nx.pending ? nx.urows.p : nullptr);
     launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
@@ -565,6 +596,30 @@ void Engine::forward_prologue(const ec_batch& b, float* out, cudaStream_t st) {
 void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   if (in_group) invalid("this rank belongs to a loopback group: use ec_group_lookup_fwd");
   forward_prologue(b, out, st);
+  BatchBufs& nx = bb[cur ^ 1];
+  if (nx.pending) {
+    if (nx.indices == b.indices_dev && nx.geom_version == geom_version) {
+      // dedup, hit/miss and host-miss gather already ran (ec_lookup_prefetch)
+      nx.pending = false;
+      select(cur ^ 1);
+      EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
+      consuming_prefetch = true;
+      try {
+        const GraphKey key{2, b.indices_dev, b.bag_offsets_dev, out, 0};
+        run_maybe_graphed(key, st, [&] {
+          gather_local(st);
+          pool(st);
+        });
+      } catch (...) {
+        consuming_prefetch = false;
+        throw;
+      }
+      consuming_prefetch = false;
+      have_fwd = true;
+      return;
+    }
+    drop_prefetch(st);
+  }
   if (world == 1) {
     const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
     run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
@@ -575,6 +630,62 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     pool(st);
   }
   have_fwd = true;
+}
+
+// Start the next batch early: dedup, hit/miss partition and (pinned-host
+// tier) the miss gather run on the prefetch/side streams into the other
+// buffer set, overlapping the current batch's backward.  Rows the current
+// backward then writes to the host tier are patched into the prefetched copy
+// (k_apply_host).  Single rank only; needs the current batch geometry.
+void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
+  if (in_group || world > 1) invalid("prefetch is single-rank only");
+  if (!have_geom || !b.indices_dev || !b.table_offsets_host) invalid("prefetch needs a batch with the current geometry");
+  bool same = b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed &&
+              b.bag_offsets_dev == bag_off;
+  for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
+  if (!same) invalid("prefetch needs the geometry (offsets, batch size, pooling, bag offsets) of the last forward");
+  use_device(device);
+  if (bb[cur ^ 1].pending) drop_prefetch(st);
+  // the shared hash is clean once the current forward's k_gather ran
+  EC_CUDA(cudaEventRecord(ev_fwd, st));
+  EC_CUDA(cudaStreamWaitEvent(pstream, ev_fwd, 0));
+  const int saved = cur;
+  select(cur ^ 1);
+  try {
+    enqueue_dedup_partition(b.indices_dev, pstream);
+    if (storage == EC_STORAGE_HOST) {
+      EC_CUDA(cudaEventRecord(ev_part, pstream));
+      EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+      EC_DISPATCH_VEC(launch_gather_host, side);
+      EC_CUDA(cudaEventRecord(ev_pf, side));
+    } else {
+      EC_CUDA(cudaEventRecord(ev_pf, pstream));
+    }
+  } catch (...) {
+    select(saved);
+    throw;
+  }
+  bb[cur].pending = true;
+  bb[cur].indices = b.indices_dev;
+  bb[cur].geom_version = geom_version;
+  select(saved);
+}
+
+void Engine::drop_prefetch(cudaStream_t st) {
+  BatchBufs& nx = bb[cur ^ 1];
+  if (!nx.pending) return;
+  EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
+  k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev.p, T, nx.ctr.p, nx.utab.p, nx.uslot.p);
+  launched();
+  nx.pending = false;
+}
+
+template <int VEC>
+void Engine::launch_gather_host(cudaStream_t s) {
+  PhaseScope ph(prof, kPhaseGatherHost, s);
+  k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                          world);
+  launched();
 }
 
 void Engine::gather_local(cudaStream_t st) { EC_DISPATCH_VEC(fwd_gather_local, st); }
@@ -603,7 +714,9 @@ void Engine::run_maybe_graphed(const GraphKey& key, cudaStream_t st, F&& enqueue
     enqueue();
     return;
   }
-  auto it = graphs.find(key);
+  GraphKey k = key;
+  k.set = cur;
+  auto it = graphs.find(k);
   if (it == graphs.end()) {
     if (graphs.size() >= 64) clear_graphs();
     const uint64_t before = launches;
@@ -622,7 +735,7 @@ void Engine::run_maybe_graphed(const GraphKey& key, cudaStream_t st, F&& enqueue
     const cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     EC_CUDA(e);
-    it = graphs.emplace(key, GraphEntry{ex, launches - before}).first;
+    it = graphs.emplace(k, GraphEntry{ex, launches - before}).first;
     launches = before;
   }
   EC_CUDA(cudaGraphLaunch(it->second.exec, st));
@@ -673,7 +786,7 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   if (world == 1) {
     uint32_t lr_bits;
     std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
-    const GraphKey key{1, grad, bag_off, out_ptr, lr_bits};
+    const GraphKey key{bb[cur ^ 1].pending ? 3 : 1, grad, bag_off, out_ptr, lr_bits};
     run_maybe_graphed(key, st, [&] { scatter_and_apply_local(grad, lr, st); });
   } else {
     scatter_and_apply_local(grad, lr, st);
@@ -686,6 +799,7 @@ void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
   h.resize(counters_size(T));
   EC_CUDA(cudaStreamSynchronize(st));
   EC_CUDA(cudaStreamSynchronize(side));
+  EC_CUDA(cudaStreamSynchronize(pstream));
   EC_CUDA(cudaMemcpy(h.data(), ctr.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
   Counters c = counters(h.data(), T);
   if (*c.err) {
@@ -833,6 +947,13 @@ int ec_lookup_fwd(ec_tables t, const ec_batch* b, float* out, void* stream) {
   return guard([&] {
     if (!b || !out) invalid("null argument");
     E(t).forward(*b, out, as_stream(stream));
+  });
+}
+
+int ec_lookup_prefetch(ec_tables t, const ec_batch* b, void* stream) {
+  return guard([&] {
+    if (!b) invalid("null batch");
+    E(t).prefetch(*b, as_stream(stream));
   });
 }
 

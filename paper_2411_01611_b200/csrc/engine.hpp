@@ -40,6 +40,33 @@ inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 4; }
 
 struct Exchange;  // exchange.cu
 
+template <class T>
+struct View {
+  T* p = nullptr;
+  size_t n = 0;
+  size_t bytes() const { return n * sizeof(T); }
+};
+template <class T>
+View<T> view(DevBuf<T>& b) {
+  return View<T>{b.p, b.n};
+}
+
+struct BatchBufs {
+  DevBuf<uint32_t> slot_of, inv, uniq, uslot, missq;
+  DevBuf<int32_t> usrc;
+  DevBuf<uint16_t> utab;
+  DevBuf<float> urows, ugrad;
+  DevBuf<unsigned long long> status;
+  DevBuf<int> ctr;
+  const uint32_t* indices = nullptr;  // batch held by a pending prefetch
+  uint64_t geom_version = 0;
+  bool pending = false;               // prefetched, not yet consumed by forward
+  uint64_t bytes() const {
+    return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
+           utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + ctr.bytes();
+  }
+};
+
 // One timing slot per kernel of the batch pipeline (ec_tables_profile_read order).
 enum { kPhaseInsert = 0, kPhaseCompact, kPhaseInversePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange,
        kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kNumPhases };
@@ -70,13 +97,14 @@ struct PhaseScope {
 };
 
 struct GraphKey {
-  int kind;  // 0 forward, 1 backward
+  int kind;  // 0 forward, 1 backward, 2 forward of a prefetched batch, 3 backward patching a prefetch
   const void* a;
   const void* b;
   const void* c;
   uint32_t lr_bits;
+  int set = 0;  // per-batch buffer set the captured kernels point at
   bool operator<(const GraphKey& o) const {
-    return std::tie(kind, a, b, c, lr_bits) < std::tie(o.kind, o.a, o.b, o.c, o.lr_bits);
+    return std::tie(kind, a, b, c, lr_bits, set) < std::tie(o.kind, o.a, o.b, o.c, o.lr_bits, o.set);
   }
 };
 
@@ -111,14 +139,20 @@ struct Engine {
   float synth_scale = 0.f;
   bool synth_valid = false;
 
-  DevBuf<uint32_t> slot_of, inv, uniq, uslot, missq;
-  DevBuf<int32_t> usrc;
-  DevBuf<uint16_t> utab;
-  DevBuf<float> urows, ugrad;
+  // Per-batch state, double-buffered so the next batch can be prefetched
+  // (dedup, hit/miss, host-miss gather) while the current one runs backward.
+  // The View members below point at the selected set (select()).
+  BatchBufs bb[2];
+  int cur = 0;
+  View<uint32_t> slot_of, inv, uniq, uslot, missq;
+  View<int32_t> usrc;
+  View<uint16_t> utab;
+  View<float> urows, ugrad;
+  View<unsigned long long> status;  // decoupled look-back words, one per tile
+  View<int> ctr;
+  void select(int i);
   DevBuf<Tile> tiles;
-  DevBuf<unsigned long long> status;  // decoupled look-back words, one per tile
   DevBuf<int4> stiles;                // scatter tiles (table, bag lo, bag hi, -)
-  DevBuf<int> ctr;
   DevBuf<TableDev> tdev;
   std::vector<TableDev> td_host;
   int ntiles = 0, nstiles = 0, tail_lo = 0;
@@ -130,8 +164,13 @@ struct Engine {
   const int64_t* bag_off = nullptr;
   float* out_ptr = nullptr;
 
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_part = nullptr, ev_side = nullptr;
+  cudaStream_t side = nullptr, pstream = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_fwd = nullptr, ev_pf = nullptr;
+  uint64_t geom_version = 0;
+  bool consuming_prefetch = false;
+  void prefetch(const ec_batch& b, cudaStream_t st);
+  void drop_prefetch(cudaStream_t st);
+  template <int VEC> void launch_gather_host(cudaStream_t s);
 
   Profiler prof;
   uint64_t launches = 0;

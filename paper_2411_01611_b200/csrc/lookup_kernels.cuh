@@ -522,7 +522,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
                                                          const uint32_t* __restrict__ missq,
                                                          const uint32_t* __restrict__ uniq,
                                                          const uint16_t* __restrict__ utab, const float* __restrict__ urows,
-                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
+                                                         const float* __restrict__ ugrad, float lr, int rank, int world,
+                                                         const int32_t* __restrict__ nxt_usrc,
+                                                         float* __restrict__ nxt_urows) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -539,10 +541,35 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
       if (static_cast<int>(id % world) != rank) continue;
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
       const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
-      st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4,
-          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+      const float4 nw = make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      const TableDev tb = td[utab[g]];
+      st4(tb.store + static_cast<int64_t>(id / world) * D + m.c * 4, nw);
+      if (nxt_urows) {
+        // A prefetched next batch may already hold this row (gathered before
+        // this update): its dedup left id -> tagged unique index in the
+        // hash; refresh that copy with the new value.
+        uint32_t h = hash_slot(id, tb.shift);
+        for (;;) {
+          const unsigned long long v = __ldcg(tb.hash + h);
+          if (v == kEmptySlot) break;
+          if (static_cast<uint32_t>(v >> 32) == id) {
+            const uint32_t g2 = static_cast<uint32_t>(v) & ~kRankTag;
+            if (nxt_usrc[g2] < 0) st4(nxt_urows + static_cast<int64_t>(g2) * D + m.c * 4, nw);
+            break;
+          }
+          h = (h + 1) & tb.mask;
+        }
+      }
     }
   }
+}
+
+// Drop the hash entries of a prefetched batch that will not be consumed.
+__global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                             const uint16_t* __restrict__ utab, const uint32_t* __restrict__ uslot) {
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x)
+    td[utab[g]].hash[uslot[g]] = kEmptySlot;
 }
 
 }  // namespace ec

@@ -137,6 +137,16 @@ class EmbeddingTables:
         self._out = out
         return out
 
+    def prefetch(self, indices, table_offsets: Sequence[int], batch_size: int, pooling: int = 0, bag_offsets=None):
+        """Start the next batch (dedup, hit/miss, host-miss gather) while the
+        current one finishes; the next forward() with the same `indices`
+        tensor consumes it.  Same geometry as the last forward."""
+        offs = np.ascontiguousarray(table_offsets, dtype=np.int64)
+        bo = bag_offsets.data_ptr() if bag_offsets is not None else None
+        self._pf_offs = offs  # keep alive for the call
+        b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo, batch_size, pooling)
+        check(N.lib().ec_lookup_prefetch(self._h, C.byref(b), _stream_ptr(self.torch, self.device)))
+
     def backward(self, grad, lr: float):
         torch = self.torch
         if grad.dtype != torch.float32 or not grad.is_cuda or not grad.is_contiguous():

@@ -201,3 +201,51 @@ def test_config2_kaggle_shape_host_tier(ec, torch, ref):
                      out=out, ref=ref)
     assert st["miss_rows"] > 0 and st["hit_rows"] > 0
     tab.close()
+
+
+@pytest.mark.parametrize("storage,graphs", [("host", False), ("host", True), ("hbm", True)])
+def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
+    """fwd(j) -> prefetch(j+1) -> bwd(j) gives the same outputs and final rows
+    as the unpipelined fwd/bwd sequence (cold rows updated by bwd(j) that
+    batch j+1 already gathered are refreshed)."""
+    rows, D, B, P = [3000, 800, 50], 8, 128, 3
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.0)) for r in rows]
+    caches = [d.top_ids(k) for d, k in zip(dists, [30, 10, 5])]
+    n = B * P
+    offs = np.arange(len(rows) + 1, dtype=np.int64) * n
+    nb = 6
+    batches = [make_ids(ec, torch, dists, [n] * len(rows), 500 + j)[0] for j in range(nb)]
+    grads = [torch.randn(B, len(rows) * D, device="cuda") for _ in range(nb)]
+
+    def run(pipelined):
+        tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=n, max_batch_size=B)
+        tab.use_graphs(graphs)
+        tab.init_synthetic(4, 0.2)
+        tab.place_cache(caches)
+        outs = []
+        for j in range(nb):
+            o = tab.forward(batches[j], offs, B, P)
+            outs.append(o.clone())
+            if pipelined and j + 1 < nb:
+                tab.prefetch(batches[j + 1], offs, B, P)
+            tab.backward(grads[j], 0.5)
+        torch.cuda.synchronize()
+        final = [tab.read_rows(t, np.arange(rows[t])) for t in range(len(rows))]
+        st = tab.stats(per_table=True)
+        tab.close()
+        return [o.cpu().numpy() for o in outs], final, st
+
+    def body():
+        o1, f1, s1 = run(False)
+        o2, f2, s2 = run(True)
+        for a, b in zip(o1, o2):
+            np.testing.assert_allclose(b, a, rtol=RTOL, atol=ATOL)
+        for a, b in zip(f1, f2):
+            np.testing.assert_allclose(b, a, rtol=RTOL, atol=ATOL)
+        assert (s1["miss_per_table"] == s2["miss_per_table"]).all()
+
+    if graphs:
+        with torch.cuda.stream(torch.cuda.Stream()):
+            body()
+    else:
+        body()
