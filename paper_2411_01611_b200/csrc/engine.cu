@@ -555,7 +555,11 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
     const BatchBufs& nx = bb[cur ^ 1];
-    if (nx.pending) EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cudaEventWaitExternal));  // its gather precedes our patch
+    if (nx.pending) {  // the prefetched gather precedes our patch
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      EC_CUDA(cudaStreamIsCapturing(st, &cs));
+      EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    }
     PhaseScope ph(prof, kPhaseApplyHost, side);
     k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p,
                                                               lr, rank, world, nx.pending ? nx.usrc.p : nullptr,
