@@ -238,10 +238,13 @@ def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
     def body():
         o1, f1, s1 = run(False)
         o2, f2, s2 = run(True)
+        # both runs sum gradients with float atomics (order-of-summation
+        # noise compounds over the steps); a stale prefetched row would be
+        # off by lr*grad = O(0.1), five orders above this bound
         for a, b in zip(o1, o2):
-            np.testing.assert_allclose(b, a, rtol=RTOL, atol=ATOL)
+            np.testing.assert_allclose(b, a, rtol=RTOL, atol=1e-5 * np.abs(a).max())
         for a, b in zip(f1, f2):
-            np.testing.assert_allclose(b, a, rtol=RTOL, atol=ATOL)
+            np.testing.assert_allclose(b, a, rtol=RTOL, atol=1e-5 * np.abs(a).max())
         assert (s1["miss_per_table"] == s2["miss_per_table"]).all()
 
     if graphs:
