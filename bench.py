@@ -183,8 +183,16 @@ def run_ours(args, wl):
     stream = torch.cuda.current_stream()
 
     def step(j):
+        # pipelined training step: forward of batch j (its dedup, hit/miss and
+        # host-miss gather were prefetched during step j-1), prefetch of batch
+        # j+1 overlapping the backward of j, then a join so the step's window
+        # holds all of its work
         o = tab.forward(ids[j], offs, B, P, out=out)
+        if args.prefetch:
+            tab.prefetch(ids[(j + 1) % N_BATCHES], offs, B, P)
         tab.backward(o, LR)  # loss = 0.5*||pooled||^2  ->  d loss / d pooled = pooled
+        if args.prefetch:
+            tab.prefetch_wait()
 
     # per-batch stats (deterministic per batch; outside any timed region)
     stats = []
@@ -242,16 +250,24 @@ def run_ours(args, wl):
 
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
-    dev_ids = torch.empty_like(ids[0])
+    dev_ids = [torch.empty_like(ids[0]), torch.empty_like(ids[0])]
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
     e2e_end = torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     e2e_start.record(stream)
+    dev_ids[0].copy_(host_ids[0], non_blocking=True)
+    if args.prefetch:
+        tab.prefetch(dev_ids[0], offs, B, P)
     for k in range(args.steps):
-        dev_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
-        o = tab.forward(dev_ids, offs, B, P, out=out)
+        cur_ids, nxt_ids = dev_ids[k % 2], dev_ids[(k + 1) % 2]
+        if not args.prefetch:
+            cur_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
+        o = tab.forward(cur_ids, offs, B, P, out=out)
+        if args.prefetch:  # H2D of the next step's ids, then its prefetch
+            nxt_ids.copy_(host_ids[(k + 1) % N_BATCHES], non_blocking=True)
+            tab.prefetch(nxt_ids, offs, B, P)
         tab.backward(o, LR)
         counters = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
     e2e_end.record(stream)
@@ -309,7 +325,10 @@ def run_ours(args, wl):
         "config": {"workload": wl["name"], "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
                    "cache_rows": int(sum(ks)), "cache_bytes": int(sum(ks)) * D * 4, "cold_tier": wl["storage"],
                    "l2": "flushed between timed steps (256 MiB write outside the per-step events)",
-                   "step": "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD)",
+                   "step": ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD); pipelined: the next "
+                            "batch's dedup/hit-miss/host gather (ec_lookup_prefetch) overlaps this backward and "
+                            "is inside this step's window") if args.prefetch else
+                           "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
                    "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5),
@@ -441,6 +460,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="kaggle")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
+                    help="unpipelined steps (no ec_lookup_prefetch of the next batch)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -293,6 +293,8 @@ int ec_lookup_fwd(ec_tables t, const ec_batch* batch, float* out_dev, void* stre
  * results equal the unpipelined sequence.  Same geometry as the last forward
  * required. */
 int ec_lookup_prefetch(ec_tables t, const ec_batch* batch, void* stream);
+/* Make `stream` wait for a pending prefetch (no-op without one). */
+int ec_lookup_prefetch_wait(ec_tables t, void* stream);
 /* Backward of the last forward: grad_dev laid out like out_dev; applies
  * w <- w - lr * (sum of grads of every lookup of the row) to the cache copy
  * of cached rows and to the owning shard of the others (K6). */

@@ -961,6 +961,14 @@ int ec_lookup_prefetch(ec_tables t, const ec_batch* b, void* stream) {
   });
 }
 
+int ec_lookup_prefetch_wait(ec_tables t, void* stream) {
+  return guard([&] {
+    Engine& e = E(t);
+    use_device(e.device);
+    if (e.bb[e.cur ^ 1].pending) EC_CUDA(cudaStreamWaitEvent(as_stream(stream), e.ev_pf, 0));
+  });
+}
+
 int ec_lookup_bwd(ec_tables t, const float* grad, float lr, void* stream) {
   return guard([&] { E(t).backward(grad, lr, as_stream(stream)); });
 }

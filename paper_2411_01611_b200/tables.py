@@ -147,6 +147,10 @@ class EmbeddingTables:
         b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo, batch_size, pooling)
         check(N.lib().ec_lookup_prefetch(self._h, C.byref(b), _stream_ptr(self.torch, self.device)))
 
+    def prefetch_wait(self):
+        """Make the current stream wait for a pending prefetch."""
+        check(N.lib().ec_lookup_prefetch_wait(self._h, _stream_ptr(self.torch, self.device)))
+
     def backward(self, grad, lr: float):
         torch = self.torch
         if grad.dtype != torch.float32 or not grad.is_cuda or not grad.is_contiguous():
