@@ -254,22 +254,28 @@ def run_ours(args, wl):
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
     e2e_end = torch.cuda.Event(enable_timing=True)
+    def e2e_steps(nsteps):
+        dev_ids[0].copy_(host_ids[0], non_blocking=True)
+        if args.prefetch:
+            tab.prefetch(dev_ids[0], offs, B, P)
+        res = None
+        for k in range(nsteps):
+            cur_ids, nxt_ids = dev_ids[k % 2], dev_ids[(k + 1) % 2]
+            if not args.prefetch:
+                cur_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
+            o = tab.forward(cur_ids, offs, B, P, out=out)
+            if args.prefetch:  # H2D of the next step's ids, then its prefetch
+                nxt_ids.copy_(host_ids[(k + 1) % N_BATCHES], non_blocking=True)
+                tab.prefetch(nxt_ids, offs, B, P)
+            tab.backward(o, LR)
+            res = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
+        return res
+
+    e2e_steps(max(args.warmup, 8))  # untimed: captures the graphs of this buffer rotation
     barrier()
     torch.cuda.synchronize()
     e2e_start.record(stream)
-    dev_ids[0].copy_(host_ids[0], non_blocking=True)
-    if args.prefetch:
-        tab.prefetch(dev_ids[0], offs, B, P)
-    for k in range(args.steps):
-        cur_ids, nxt_ids = dev_ids[k % 2], dev_ids[(k + 1) % 2]
-        if not args.prefetch:
-            cur_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
-        o = tab.forward(cur_ids, offs, B, P, out=out)
-        if args.prefetch:  # H2D of the next step's ids, then its prefetch
-            nxt_ids.copy_(host_ids[(k + 1) % N_BATCHES], non_blocking=True)
-            tab.prefetch(nxt_ids, offs, B, P)
-        tab.backward(o, LR)
-        counters = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
+    counters = e2e_steps(args.steps)
     e2e_end.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -221,6 +221,8 @@ Engine::~Engine() {
   if (ev_side) cudaEventDestroy(ev_side);
   if (side) cudaStreamDestroy(side);
   if (pstream) cudaStreamDestroy(pstream);
+  if (side2) cudaStreamDestroy(side2);
+  if (ev_side2) cudaEventDestroy(ev_side2);
   if (ev_fwd) cudaEventDestroy(ev_fwd);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
@@ -307,6 +309,8 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
   EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   EC_CUDA(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
+  EC_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
@@ -551,21 +555,32 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
-  if (host) {  // cold rows written back over the host link on the side stream
-    EC_CUDA(cudaEventRecord(ev_part, st));
-    EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
-    const BatchBufs& nx = bb[cur ^ 1];
-    if (nx.pending) {  // the prefetched gather precedes our patch
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      EC_CUDA(cudaStreamIsCapturing(st, &cs));
-      EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+  if (host) {
+    EC_CUDA(cudaEventRecord(ev_part, st));  // gradients complete
+    // cold rows written back over the host link on their own stream
+    // (full duplex with the host reads of a prefetched batch)
+    EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
+    {
+      PhaseScope ph(prof, kPhaseApplyHost, side2);
+      k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                                 ugrad.p, lr, rank, world);
+      launched();
     }
-    PhaseScope ph(prof, kPhaseApplyHost, side);
-    k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p,
-                                                              lr, rank, world, nx.pending ? nx.usrc.p : nullptr,
-                                                              nx.pending ? nx.urows.p : nullptr);
-    launched();
-    EC_CUDA(cudaEventRecord(ev_side, side));
+    EC_CUDA(cudaEventRecord(ev_side2, side2));
+    const BatchBufs& nx = bb[cur ^ 1];
+    if (nx.pending) {
+      // refresh the prefetched batch's copies of rows updated here; after its
+      // host gather (FIFO on the side stream) and after our gradients
+      EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      EC_CUDA(cudaStreamIsCapturing(st, &cs));  // replayed graphs are not FIFO with the prefetch's launches
+      EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+      k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+                                                                        urows.p, ugrad.p, lr, rank, world, nx.usrc.p,
+                                                                        nx.urows.p);
+      launched();
+      EC_CUDA(cudaEventRecord(ev_side, side));
+    }
   }
   {
     PhaseScope ph(prof, kPhaseApply, st);
@@ -573,7 +588,10 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
     launched();
   }
-  if (host) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  if (host) {
+    EC_CUDA(cudaStreamWaitEvent(st, ev_side2, 0));
+    if (bb[cur ^ 1].pending) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+  }
 }
 
 
@@ -804,6 +822,7 @@ void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
   EC_CUDA(cudaStreamSynchronize(st));
   EC_CUDA(cudaStreamSynchronize(side));
   EC_CUDA(cudaStreamSynchronize(pstream));
+  EC_CUDA(cudaStreamSynchronize(side2));
   EC_CUDA(cudaMemcpy(h.data(), ctr.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
   Counters c = counters(h.data(), T);
   if (*c.err) {

@@ -164,8 +164,8 @@ struct Engine {
   const int64_t* bag_off = nullptr;
   float* out_ptr = nullptr;
 
-  cudaStream_t side = nullptr, pstream = nullptr;
-  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_fwd = nullptr, ev_pf = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_fwd = nullptr, ev_pf = nullptr;
   uint64_t geom_version = 0;
   bool consuming_prefetch = false;
   void prefetch(const ec_batch& b, cudaStream_t st);

@@ -522,9 +522,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
                                                          const uint32_t* __restrict__ missq,
                                                          const uint32_t* __restrict__ uniq,
                                                          const uint16_t* __restrict__ utab, const float* __restrict__ urows,
-                                                         const float* __restrict__ ugrad, float lr, int rank, int world,
-                                                         const int32_t* __restrict__ nxt_usrc,
-                                                         float* __restrict__ nxt_urows) {
+                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -542,23 +540,55 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
       const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
       const float4 nw = make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4, nw);
+    }
+  }
+}
+
+// A prefetched next batch gathered its host rows before this batch's SGD
+// reached the host tier: for every row this batch updates, find it in the next
+// batch's hash (id -> tagged unique index, left by its dedup) and refresh the
+// copy with the new value.  On-device only; the host write-back runs apart.
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __restrict__ td, int T,
+                                                             const int* __restrict__ ctr,
+                                                             const uint32_t* __restrict__ missq,
+                                                             const uint32_t* __restrict__ uniq,
+                                                             const uint16_t* __restrict__ utab,
+                                                             const float* __restrict__ urows,
+                                                             const float* __restrict__ ugrad, float lr, int rank,
+                                                             int world, const int32_t* __restrict__ nxt_usrc,
+                                                             float* __restrict__ nxt_urows) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      if (q >= nm) continue;
+      const uint32_t g = missq[q];
+      const uint32_t id = uniq[g];
+      if (static_cast<int>(id % world) != rank) continue;
       const TableDev tb = td[utab[g]];
-      st4(tb.store + static_cast<int64_t>(id / world) * D + m.c * 4, nw);
-      if (nxt_urows) {
-        // A prefetched next batch may already hold this row (gathered before
-        // this update): its dedup left id -> tagged unique index in the
-        // hash; refresh that copy with the new value.
-        uint32_t h = hash_slot(id, tb.shift);
-        for (;;) {
-          const unsigned long long v = __ldcg(tb.hash + h);
-          if (v == kEmptySlot) break;
-          if (static_cast<uint32_t>(v >> 32) == id) {
-            const uint32_t g2 = static_cast<uint32_t>(v) & ~kRankTag;
-            if (nxt_usrc[g2] < 0) st4(nxt_urows + static_cast<int64_t>(g2) * D + m.c * 4, nw);
-            break;
+      uint32_t h = hash_slot(id, tb.shift);
+      for (;;) {
+        const unsigned long long v = __ldcg(tb.hash + h);
+        if (v == kEmptySlot) break;
+        if (static_cast<uint32_t>(v >> 32) == id) {
+          const uint32_t g2 = static_cast<uint32_t>(v) & ~kRankTag;
+          if (nxt_usrc[g2] < 0) {
+            const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+            const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
+            st4(nxt_urows + static_cast<int64_t>(g2) * D + m.c * 4,
+                make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
           }
-          h = (h + 1) & tb.mask;
+          break;
         }
+        h = (h + 1) & tb.mask;
       }
     }
   }
