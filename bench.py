@@ -466,8 +466,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="kaggle")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
-                    help="unpipelined steps (no ec_lookup_prefetch of the next batch)")
+    ap.add_argument("--prefetch", action="store_true",
+                    help="pipelined steps: ec_lookup_prefetch of the next batch overlaps this backward")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -246,6 +246,11 @@ int ec_tables_profile(ec_tables t, int enable);
  * stream, under profiling, inside an outer capture or with world > 1, kernels
  * are launched directly. */
 int ec_tables_use_graphs(ec_tables t, int enable);
+/* Dedup implementation: 0 (default) one thread-block cluster per table
+ * (insert, flags, scan, emit, inverse and hit/miss in one kernel) whenever
+ * every table's batch has <= 131072 lookups, else the tile path; 1 forces the
+ * tile path (k_insert -> k_compact -> k_inverse_partition).  Same results. */
+int ec_tables_dedup_mode(ec_tables t, int mode);
 int ec_tables_profile_read(ec_tables t, double* ms_host, uint64_t* calls_host, uint64_t* launches,
                            int reset);
 /* Deterministic synthetic weights: row (t, id) element c =

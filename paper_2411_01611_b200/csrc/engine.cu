@@ -291,6 +291,7 @@ void Engine::create(const ec_tables_config& c) {
     b.ctr.alloc(counters_size(T));
     EC_CUDA(cudaMemset(b.ctr.p, 0, b.ctr.bytes()));
   }
+  for (BatchBufs& b : bb) b.tstat.alloc(T);
   select(0);
   tiles.alloc(max_tiles);
   tdev.alloc(T);
@@ -331,6 +332,7 @@ void Engine::select(int i) {
   urows = view(b.urows);
   ugrad = view(b.ugrad);
   status = view(b.status);
+  tstat = view(b.tstat);
   ctr = view(b.ctr);
 }
 
@@ -465,6 +467,9 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
     td_host[t].n = n;
   }
   ntiles = static_cast<int>(tl.size());
+  int64_t nmax = 0;
+  for (uint32_t t = 0; t < T; ++t) nmax = std::max<int64_t>(nmax, geom_off[t + 1] - geom_off[t]);
+  cluster_ok = nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * kMaxItems;
   tail_lo = static_cast<int>(T);
   for (int t = static_cast<int>(T) - 1; t >= 0 && ft[t] == ntiles; --t) tail_lo = t;  // trailing empty tables
   for (uint32_t t = 0; t < static_cast<uint32_t>(tail_lo); ++t) {
@@ -776,6 +781,17 @@ void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
+  if (cluster_ok && dedup_mode != 1) {
+    // one thread-block cluster per table: K1 + K2 in a single kernel
+    EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
+    EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
+    PhaseScope ph(prof, kPhaseInsert, st);
+    k_dedup_cluster<<<kClusterCtas * T, kClusterThreads, 0, st>>>(tdev.p, static_cast<int>(T), indices, slot_of.p,
+                                                                 tstat.p, ctr.p, uniq.p, uslot.p, utab.p, inv.p,
+                                                                 usrc.p, missq.p);
+    launched();
+    return;
+  }
   {
     if (ntiles) {
       {
@@ -931,6 +947,15 @@ int ec_tables_profile_read(ec_tables t, double* ms, uint64_t* calls, uint64_t* l
       for (int i = 0; i < kNumPhases; ++i) e.prof.ms_[i] = 0.0, e.prof.calls_[i] = 0;
       e.launches = 0;
     }
+  });
+}
+
+int ec_tables_dedup_mode(ec_tables t, int mode) {
+  return guard([&] {
+    if (mode < 0 || mode > 1) invalid("dedup mode: 0 auto (cluster per table when it fits), 1 tiles");
+    Engine& e = E(t);
+    e.dedup_mode = mode;
+    e.clear_graphs();
   });
 }
 

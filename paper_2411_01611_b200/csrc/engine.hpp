@@ -56,14 +56,14 @@ struct BatchBufs {
   DevBuf<int32_t> usrc;
   DevBuf<uint16_t> utab;
   DevBuf<float> urows, ugrad;
-  DevBuf<unsigned long long> status;
+  DevBuf<unsigned long long> status, tstat;  // tile / table look-back words
   DevBuf<int> ctr;
   const uint32_t* indices = nullptr;  // batch held by a pending prefetch
   uint64_t geom_version = 0;
   bool pending = false;               // prefetched, not yet consumed by forward
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
-           utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + ctr.bytes();
+           utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + tstat.bytes() + ctr.bytes();
   }
 };
 
@@ -149,6 +149,9 @@ struct Engine {
   View<uint16_t> utab;
   View<float> urows, ugrad;
   View<unsigned long long> status;  // decoupled look-back words, one per tile
+  View<unsigned long long> tstat;   // one per table (cluster dedup)
+  bool cluster_ok = false;          // every table's batch fits one cluster
+  int dedup_mode = 0;               // 0 auto, 1 tile path
   View<int> ctr;
   void select(int i);
   DevBuf<Tile> tiles;

@@ -21,6 +21,8 @@
 //   k_apply(_host)     SGD into cache rows / owning shard
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "device_util.cuh"
 #include "engine.hpp"
 
@@ -600,6 +602,189 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x)
     td[utab[g]].hash[uslot[g]] = kEmptySlot;
+}
+
+}  // namespace ec
+
+// ===================================================================
+// K1 + K2 in one kernel: one thread-block cluster per table.
+//
+// The batch of a table is split into kClusterCtas contiguous chunks, one per
+// CTA; inside a CTA each thread owns kMaxItems-or-fewer consecutive positions
+// (thread-major), so the rank of a first occurrence is an exclusive scan of
+// per-thread counts plus a popcount inside the thread.  Phases are separated
+// by cluster barriers (release/acquire at cluster scope) instead of kernel
+// boundaries; the CTA totals are exchanged through distributed shared memory.
+// Tables take tickets in order and chain their unique bases with a short
+// look-back (one word per table), so the global unique index is in
+// (table, first occurrence) order exactly as the tile path produces it.
+// ===================================================================
+namespace ec {
+
+namespace cg = cooperative_groups;
+constexpr int kClusterCtas = 8;
+constexpr int kClusterThreads = 512;
+constexpr int kMaxItems = 32;  // per thread -> n_t <= 8 * 512 * 32 = 131072
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads)
+    k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
+                    uint32_t* __restrict__ slot_of, unsigned long long* __restrict__ tstatus, int* __restrict__ ctr,
+                    uint32_t* __restrict__ uniq, uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab,
+                    uint32_t* __restrict__ inv, int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned crank = cluster.block_rank();
+  __shared__ int s_table, s_total, s_prefix, s_base;
+  __shared__ int sw[kClusterThreads / 32];
+  Counters c = counters(ctr, T);
+  if (crank == 0 && threadIdx.x == 0) s_table = atomicAdd(c.tile_counter, 1);  // ticket = table id
+  cluster.sync();
+  const int t = *cluster.map_shared_rank(&s_table, 0);
+  const TableDev tb = td[t];
+  const int64_t n = tb.n;
+  const int64_t chunk = (n + kClusterCtas - 1) / kClusterCtas;
+  const int64_t c0 = min(n, static_cast<int64_t>(crank) * chunk), c1 = min(n, c0 + chunk);
+  const int items = static_cast<int>((c1 - c0 + kClusterThreads - 1) / kClusterThreads);
+  const int64_t p0 = c0 + static_cast<int64_t>(threadIdx.x) * items;  // this thread's first position
+  const int my = static_cast<int>(max(int64_t{0}, min(static_cast<int64_t>(items), c1 - p0)));
+
+  // ---- P1: insert (packed atomicMin keeps each id's first position)
+  for (int j0 = 0; j0 < items; j0 += 4) {
+    uint32_t id[4], h[4];
+    unsigned long long cur[4];
+    bool live[4];
+    unsigned peers[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      live[k] = j < my;
+      id[k] = live[k] ? __ldcs(indices + tb.base + p0 + j) : kEmptyKey;
+      if (live[k] && id[k] >= tb.rows) {
+        atomicExch(c.err, 1);
+        live[k] = false;
+        id[k] = kEmptyKey;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      peers[k] = __match_any_sync(kFull, id[k]);
+      h[k] = hash_slot(id[k], tb.shift);
+      cur[k] = (live[k] && __ffs(peers[k]) - 1 == lane_id()) ? __ldcg(tb.hash + h[k]) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = j0 + k;
+      const int leader = __ffs(peers[k]) - 1;
+      uint32_t slot = 0;
+      if (live[k] && leader == lane_id())
+        slot = hash_insert_from(tb.hash, tb.mask, h[k], cur[k], id[k], static_cast<uint32_t>(p0 + j));
+      slot = __shfl_sync(kFull, slot, leader);
+      if (j < my) slot_of[tb.base + p0 + j] = live[k] ? slot : kInvalidSlot;
+    }
+  }
+  cluster.sync();  // every insert of this table is done
+
+  // ---- P2: first-occurrence flags, CTA scan, cluster prefix via DSMEM
+  uint32_t mask = 0;
+  for (int j0 = 0; j0 < items; j0 += 4) {
+    uint32_t hs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hs[k] = (j0 + k) < my ? slot_of[tb.base + p0 + j0 + k] : kInvalidSlot;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (hs[k] != kInvalidSlot &&
+          static_cast<uint32_t>(__ldcg(tb.hash + hs[k])) == static_cast<uint32_t>(p0 + j0 + k))
+        mask |= 1u << (j0 + k);
+  }
+  int total;
+  const int ex = block_exclusive_scan<kClusterThreads>(__popc(mask), sw, &total);
+  if (threadIdx.x == 0) s_total = total;
+  cluster.sync();
+  if (threadIdx.x == 0) {
+    int before = 0, all = 0;
+    for (unsigned r = 0; r < kClusterCtas; ++r) {
+      const int v = *cluster.map_shared_rank(&s_total, r);
+      if (r < crank) before += v;
+      all += v;
+    }
+    s_prefix = before;
+    if (crank == 0) {
+      // table-level look-back: tickets are taken in order, so every lower
+      // table is running or done; its word becomes inclusive soon
+      int excl = 0;
+      if (t > 0) {
+        publish(tstatus + t, kStatAgg | static_cast<uint32_t>(all));
+        for (int k = t - 1; k >= 0; --k) {
+          unsigned long long v;
+          do {
+            v = *reinterpret_cast<volatile unsigned long long*>(tstatus + k);
+          } while ((v >> 32) == 0);
+          excl += static_cast<int>(static_cast<uint32_t>(v));
+          if ((v >> 32) == 2) break;
+        }
+      }
+      publish(tstatus + t, kStatInc | static_cast<uint32_t>(excl + all));
+      c.ubase[t] = excl;
+      if (t == T - 1) c.ubase[T] = excl + all;
+      s_base = excl;
+    }
+  }
+  cluster.sync();
+  const int base = *cluster.map_shared_rank(&s_base, 0) + s_prefix + ex;
+
+  // ---- P3: emit unique ids in first-occurrence order, tag their slots
+  {
+    uint32_t m = mask;
+    int r = 0;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t p = tb.base + p0 + j;
+      const uint32_t g = static_cast<uint32_t>(base + r++);
+      const uint32_t id = indices[p];
+      const uint32_t h = slot_of[p];
+      uniq[g] = id;
+      uslot[g] = h;
+      utab[g] = static_cast<uint16_t>(t);
+      tb.hash[h] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
+    }
+  }
+  cluster.sync();  // all tags of this table visible
+
+  // ---- P4: inverse
+  for (int j0 = 0; j0 < my; j0 += 4) {
+    uint32_t hs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hs[k] = (j0 + k) < my ? slot_of[tb.base + p0 + j0 + k] : kInvalidSlot;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (j0 + k < my)
+        inv[tb.base + p0 + j0 + k] = hs[k] == kInvalidSlot ? kInvalidSlot
+                                                           : static_cast<uint32_t>(__ldcg(tb.hash + hs[k])) & ~kRankTag;
+  }
+
+  // ---- P5: hit/miss partition of this table's uniques (K2)
+  const int ub = *cluster.map_shared_rank(&s_base, 0);
+  int U = 0;
+  for (unsigned r = 0; r < kClusterCtas; ++r) U += *cluster.map_shared_rank(&s_total, r);
+  for (int b0 = crank * kClusterThreads; b0 < U; b0 += kClusterCtas * kClusterThreads) {
+    const int g = ub + b0 + static_cast<int>(threadIdx.x);
+    const bool live = b0 + static_cast<int>(threadIdx.x) < U;
+    bool miss = false;
+    if (live) {
+      const int32_t s = __ldg(tb.remap + uniq[g]);
+      usrc[g] = s;
+      miss = s < 0;
+    }
+    const unsigned mb = __ballot_sync(kFull, miss);
+    int qbase = 0;
+    if (mb && lane_id() == __ffs(mb) - 1) {
+      qbase = atomicAdd(c.miss_total, __popc(mb));
+      atomicAdd(c.M + t, __popc(mb));
+    }
+    qbase = __shfl_sync(kFull, qbase, __ffs(mb ? mb : 1u) - 1);
+    if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
+  }
+  cluster.sync();  // keep DSMEM of every CTA alive until all remote reads are done
 }
 
 }  // namespace ec

@@ -72,6 +72,10 @@ class EmbeddingTables:
         """CUDA-graph replay of forward/backward (needs a non-default stream)."""
         check(N.lib().ec_tables_use_graphs(self._h, 1 if enable else 0))
 
+    def dedup_mode(self, mode: str = "auto"):
+        """"auto": one thread-block cluster per table when it fits; "tiles": tile path."""
+        check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1}[mode]))
+
     def profile(self, enable: bool = True):
         """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""
         check(N.lib().ec_tables_profile(self._h, 1 if enable else 0))

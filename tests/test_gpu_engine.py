@@ -70,21 +70,24 @@ def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=
     return stats
 
 
-@pytest.mark.parametrize("storage,graphs", [("hbm", False), ("host", False), ("hbm", True), ("host", True)])
-def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs):
+@pytest.mark.parametrize("storage,graphs,mode", [("hbm", False, "auto"), ("host", False, "auto"),
+                                                 ("hbm", True, "auto"), ("host", True, "auto"),
+                                                 ("hbm", False, "tiles"), ("host", True, "tiles")])
+def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs, mode):
     if graphs:  # CUDA-graph capture/replay needs a non-default stream
         with torch.cuda.stream(torch.cuda.Stream()):
-            _small_fixed_pooling(ec, torch, ref, storage, True)
+            _small_fixed_pooling(ec, torch, ref, storage, True, mode)
     else:
-        _small_fixed_pooling(ec, torch, ref, storage, False)
+        _small_fixed_pooling(ec, torch, ref, storage, False, mode)
 
 
-def _small_fixed_pooling(ec, torch, ref, storage, graphs):
+def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
     rows, D, B, P = [1000, 37, 5000, 1], 16, 64, 7
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
     caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, [50, 0, 500, 1])]
     tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
     tab.use_graphs(graphs)
+    tab.dedup_mode(mode)
     seed, scale = 1234, 0.05
     tab.init_synthetic(seed, scale)
     tab.place_cache(caches)
@@ -166,13 +169,15 @@ def test_out_of_range_id_is_a_validation_error(ec, torch):
     tab.close()
 
 
-def test_config1_full_size_counts_and_sets(ec, torch, ref):
+@pytest.mark.parametrize("mode", ["auto", "tiles"])
+def test_config1_full_size_counts_and_sets(ec, torch, ref, mode):
     """Config 1 (BASELINE.json configs[0]): 8 tables x 1M rows, D=64, b=4096,
     P=20 (n = 81,920 per table); counts bit-exact vs the reference,
     unique/inverse/hit sets bit-exact vs the oracle, three cache sizes."""
     T, E, D, B, P = 8, 1_000_000, 64, 4096, 20
     dist = ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, E, 1.05))
     tab = ec.EmbeddingTables([E] * T, D, max_lookups_per_table=B * P, max_batch_size=B)
+    tab.dedup_mode(mode)
     tab.init_synthetic(9, 0.01)
     for k in (0, 10_000, 100_000):
         caches = [dist.top_ids(k)] * T
