@@ -111,7 +111,9 @@ def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
         _, want = O.backward_sgd(np.ascontiguousarray(gh[:, t * D:(t + 1) * D]), inv[:seg.size],
                                  np.arange(B + 1, dtype=np.int64) * P, w0, lr)
         got = tab.read_rows(t, u)
-        np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+        # fp32 sums of several O(1) gradients: absolute error scales with the
+        # row magnitude, so atol is 1e-5 of the largest |w| in the table
+        np.testing.assert_allclose(got, want, rtol=RTOL, atol=1e-5 * np.abs(want).max())
     # a second batch sees the updated rows and a clean hash table
     ids2, _ = make_ids(ec, torch, dists, [B * P] * len(rows), 78)
     tab.forward(ids2, offs, B, P)
