@@ -246,10 +246,12 @@ int ec_tables_profile(ec_tables t, int enable);
  * stream, under profiling, inside an outer capture or with world > 1, kernels
  * are launched directly. */
 int ec_tables_use_graphs(ec_tables t, int enable);
-/* Dedup implementation: 0 (default) one thread-block cluster per table
- * (insert, flags, scan, emit, inverse and hit/miss in one kernel) whenever
- * every table's batch has <= 131072 lookups, else the tile path; 1 forces the
- * tile path (k_insert -> k_compact -> k_inverse_partition).  Same results. */
+/* Dedup implementation: 0 (default, auto) one thread-block cluster per table
+ * (insert, flags, scan, emit, inverse and hit/miss in one kernel) when the
+ * tables fill the GPU (8*T >= SMs) and every table's batch has <= 32768
+ * lookups, else the tile path; 1 forces the tile path (k_insert -> k_compact
+ * -> k_inverse_partition); 2 forces the cluster kernel whenever every
+ * table's batch has <= 131072 lookups.  Identical results. */
 int ec_tables_dedup_mode(ec_tables t, int mode);
 int ec_tables_profile_read(ec_tables t, double* ms_host, uint64_t* calls_host, uint64_t* launches,
                            int reset);

@@ -150,8 +150,9 @@ struct Engine {
   View<float> urows, ugrad;
   View<unsigned long long> status;  // decoupled look-back words, one per tile
   View<unsigned long long> tstat;   // one per table (cluster dedup)
-  bool cluster_ok = false;          // every table's batch fits one cluster
-  int dedup_mode = 0;               // 0 auto, 1 tile path
+  bool cluster_fits = false;        // every table's batch fits one cluster
+  bool cluster_ok = false;          // ... and the cluster path is the faster one
+  int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr;
   void select(int i);
   DevBuf<Tile> tiles;

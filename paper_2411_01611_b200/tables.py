@@ -73,8 +73,8 @@ class EmbeddingTables:
         check(N.lib().ec_tables_use_graphs(self._h, 1 if enable else 0))
 
     def dedup_mode(self, mode: str = "auto"):
-        """"auto": one thread-block cluster per table when it fits; "tiles": tile path."""
-        check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1}[mode]))
+        """"auto" (cluster per table when the tables fill the GPU), "tiles", or "cluster"."""
+        check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1, "cluster": 2}[mode]))
 
     def profile(self, enable: bool = True):
         """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""

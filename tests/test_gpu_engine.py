@@ -72,7 +72,8 @@ def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=
 
 @pytest.mark.parametrize("storage,graphs,mode", [("hbm", False, "auto"), ("host", False, "auto"),
                                                  ("hbm", True, "auto"), ("host", True, "auto"),
-                                                 ("hbm", False, "tiles"), ("host", True, "tiles")])
+                                                 ("hbm", False, "tiles"), ("host", True, "tiles"),
+                                                 ("hbm", False, "cluster"), ("host", True, "cluster")])
 def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs, mode):
     if graphs:  # CUDA-graph capture/replay needs a non-default stream
         with torch.cuda.stream(torch.cuda.Stream()):
@@ -171,7 +172,7 @@ def test_out_of_range_id_is_a_validation_error(ec, torch):
     tab.close()
 
 
-@pytest.mark.parametrize("mode", ["auto", "tiles"])
+@pytest.mark.parametrize("mode", ["auto", "cluster"])
 def test_config1_full_size_counts_and_sets(ec, torch, ref, mode):
     """Config 1 (BASELINE.json configs[0]): 8 tables x 1M rows, D=64, b=4096,
     P=20 (n = 81,920 per table); counts bit-exact vs the reference,
