@@ -38,6 +38,13 @@ WORKLOADS = {
                    storage="host", name="criteo-kaggle-shaped (BASELINE configs[1])"),
     "kaggle_hbm": dict(rows=KAGGLE, dim=16, batch=16384, pooling=1, alpha=1.05, cache_bytes=256 << 20,
                        storage="hbm", name="criteo-kaggle-shaped, cold rows in HBM (configs[1] variant)"),
+    # BASELINE configs[3]: access-skew sweep at a fixed cache fraction (10% of
+    # rows), Kaggle-shaped tables in HBM.  "bagpipe": power law (alpha 0.95)
+    # over a seeded random permutation of each table's ids (hot ids anywhere).
+    **{f"skew_{name}": dict(rows=KAGGLE, dim=16, batch=16384, pooling=1, dist=dist, cache_frac=0.10,
+                            cache_bytes=0, storage="hbm", name=f"skew sweep {name}, 10% cache (configs[3] shape)")
+       for name, dist in [("uniform", ("uniform",)), ("zipf0.8", ("zipf", 0.8)), ("zipf1.05", ("zipf", 1.05)),
+                          ("zipf1.2", ("zipf", 1.2)), ("bagpipe", ("bagpipe", 0.95))]},
     "cfg1": dict(rows=[1_000_000] * 8, dim=64, batch=4096, pooling=20, alpha=1.05, cache_bytes=0,
                  storage="hbm", name="8x1M zipf1.05 D64 b4096 P20 (BASELINE configs[0] shape)"),
     "tb": dict(rows=TB, dim=64, batch=65536, pooling=1, alpha=1.05, cache_bytes=1 << 30, storage="hbm",
@@ -109,10 +116,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ our arm
+def make_dist(ec, wl, rows, t):
+    kind = wl.get("dist", ("zipf", wl.get("alpha", 1.05)))
+    if kind[0] == "uniform":
+        return ec.EmbeddingDistribution.uniform(rows)
+    if kind[0] == "zipf":
+        return ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, rows, kind[1]))
+    # bagpipe-style: Zipf weights dealt to a seeded permutation of the ids
+    w = np.arange(1, rows + 1, dtype=np.float64) ** -kind[1]
+    p = np.empty(rows)
+    p[np.random.default_rng(SEED + t).permutation(rows)] = w / w.sum()
+    return ec.EmbeddingDistribution.from_probabilities(p)
+
+
 def build_tables(ec, torch, wl, rank, world, device):
     rows, D, B, P = wl["rows"], wl["dim"], wl["batch"], wl["pooling"]
-    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, wl["alpha"])) for r in rows]
+    dists = [make_dist(ec, wl, r, t) for t, r in enumerate(rows)]
     budget = wl["cache_bytes"] // (D * 4)
+    if wl.get("cache_frac"):
+        budget = int(sum(rows) * wl["cache_frac"])
     ks = ec.place_topk_global(dists, budget) if budget else [0] * len(rows)
     caches = [d.top_ids(k) for d, k in zip(dists, ks)]
     tab = ec.EmbeddingTables(rows, D, storage=wl["storage"], rank=rank, world=world,
@@ -328,7 +350,8 @@ def run_ours(args, wl):
         "vs_baseline": None,
         "dtype": "fp32 rows, uint32 ids",
         "data": "synthetic: Zipf(1.05) ids from the reference sampler stream (GPU K0, bit-exact), synthetic rows",
-        "config": {"workload": wl["name"], "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
+        "config": {"workload": wl["name"], "distribution": list(wl.get("dist", ("zipf", wl.get("alpha")))),
+                   "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
                    "cache_rows": int(sum(ks)), "cache_bytes": int(sum(ks)) * D * 4, "cold_tier": wl["storage"],
                    "l2": "flushed between timed steps (256 MiB write outside the per-step events)",
                    "step": ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD); pipelined: the next "

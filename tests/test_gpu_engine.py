@@ -260,3 +260,40 @@ def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
             body()
     else:
         body()
+
+
+def test_skew_sweep_distributions(ec, torch, ref):
+    """BASELINE configs[3] distributions at small scale: uniform, Zipf 0.8/1.2
+    and a power law over a permuted id space (non-identity rank -> id map in
+    the sampler and in top-k placement); ids bit-exact vs the reference
+    sampler, counts vs the reference, sets vs the oracle."""
+    rows, D, B, P = [5000, 20000, 3000, 800], 8, 256, 4
+    rng = np.random.default_rng(7)
+    dists, rdists = [], []
+    for t, r in enumerate(rows):
+        if t == 0:
+            p = np.full(r, 1.0 / r)
+        elif t == 3:
+            w = np.arange(1, r + 1, dtype=np.float64) ** -0.95
+            p = np.empty(r)
+            p[rng.permutation(r)] = w / w.sum()
+        else:
+            a = 0.8 if t == 1 else 1.2
+            w = np.arange(1, r + 1, dtype=np.float64) ** -a
+            p = w / w.sum()
+        dists.append(ec.EmbeddingDistribution.from_probabilities(p))
+        rdists.append(ref.RefDist.from_probs(p))
+    caches = [d.top_ids(len(d) // 10) for d in dists]
+    for d, rd, c in zip(dists, rdists, caches):
+        assert (c == rd.top_ids(len(c))).all()  # placement == reference top_ids
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=B * P, max_batch_size=B)
+    tab.init_synthetic(11, 0.3)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B * P] * len(rows), 4242)
+    ids_h = ids.cpu().numpy().view(np.uint32)
+    for t, rd in enumerate(rdists):
+        want = ref.ref_sample_batch(rd, B, P, ec.substream_seed(4242, t))
+        assert (ids_h[offs[t]:offs[t + 1]] == want).all(), f"table {t}: sampler ids"
+    out = tab.forward(ids, offs, B, P)
+    check_batch(ec, tab, ids_h, offs, caches, rows, D, 11, 0.3, P=P, B=B, out=out, ref=ref)
+    tab.close()
