@@ -103,6 +103,9 @@ def test_group_forward_backward(ec, torch, ref, world, storage):
                         before[key] = _current_rows(members, t, [i], world, cached[t])[0].astype(np.float64)
         group.backward(grads, lr)
         torch.cuda.synchronize()
+        # fp32 atomics sum each row's gradients in a varying order: the bound
+        # is 1e-5 relative to the largest updated value
+        scale = max(np.abs(before[k] - lr * g).max() for k, g in acc.items())
         for (t, i), gsum in acc.items():
             exp = before[(t, i)] - lr * gsum
             if i in cached[t]:
@@ -112,7 +115,7 @@ def test_group_forward_backward(ec, torch, ref, world, storage):
                 got = reps[0]
             else:
                 got = members[i % world].read_rows(t, [i])[0]
-            np.testing.assert_allclose(got, exp, rtol=RTOL, atol=ATOL)
+            np.testing.assert_allclose(got, exp, rtol=RTOL, atol=1e-5 * scale)
     group.close()
     for m in members:
         m.close()
