@@ -144,6 +144,7 @@ _SIGS = {
     "ec_tables_profile": [vp, C.c_int],
     "ec_tables_use_graphs": [vp, C.c_int],
     "ec_tables_dedup_mode": [vp, C.c_int],
+    "ec_tables_scatter_mode": [vp, C.c_int],
     "ec_tables_profile_read": [vp, vp, vp, P(u64), C.c_int],
     "ec_tables_init_synthetic": [vp, u64, f32, vp],
     "ec_tables_place_cache": [vp, vp, vp],

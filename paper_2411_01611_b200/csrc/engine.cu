@@ -289,6 +289,11 @@ void Engine::create(const ec_tables_config& c) {
     b.ugrad.alloc(N * D);
     b.status.alloc(max_tiles + 1);
     b.ctr.alloc(counters_size(T));
+    b.cnt.alloc(N);
+    b.off.alloc(N + 1);
+    b.list_u.alloc(N);
+    b.list_g.alloc(N);
+    b.part.alloc((N + kScanTile) / kScanTile + 1);
     EC_CUDA(cudaMemset(b.ctr.p, 0, b.ctr.bytes()));
   }
   for (BatchBufs& b : bb) b.tstat.alloc(T);
@@ -334,6 +339,11 @@ void Engine::select(int i) {
   status = view(b.status);
   tstat = view(b.tstat);
   ctr = view(b.ctr);
+  cnt = view(b.cnt);
+  off = view(b.off);
+  part = view(b.part);
+  list_u = view(b.list_u);
+  list_g = view(b.list_g);
 }
 
 uint64_t Engine::device_bytes() const {
@@ -536,7 +546,7 @@ void Engine::fwd_gather_local(cudaStream_t st) {
   }
   PhaseScope ph(prof, kPhaseGather, st);
   k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
-                                              ugrad.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+                                              ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
   launched();
 }
 
@@ -553,9 +563,29 @@ void Engine::fwd_pool(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
-  // ugrad rows were zeroed by k_gather
-  k_scatter<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
-                                                     bag_off, inv.p, grad, ugrad.p);
+  // ugrad rows and occurrence counts were zeroed by k_gather
+  if (scatter_mode == 1) {
+    k_scatter<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+                                                       bag_off, inv.p, grad, ugrad.p);
+    launched();
+    return;
+  }
+  if (!ntiles) return;
+  const int tgrid = std::min(ntiles, sm_count(device) * 8);
+  k_bwd_count<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, inv.p, cnt.p);
+  launched();
+  const int nparts = static_cast<int>((max_n * T + kScanTile) / kScanTile);
+  k_uscan_reduce<<<nparts, kScanThreads, 0, st>>>(cnt.p, ctr.p, static_cast<int>(T), part.p);
+  launched();
+  k_scan_partials<<<1, 1024, 0, st>>>(part.p, nparts, nullptr);
+  launched();
+  k_uscan_apply<<<nparts, kScanThreads, 0, st>>>(cnt.p, ctr.p, static_cast<int>(T), part.p, off.p);
+  launched();
+  k_bwd_fill<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, tdev.p, bag_off, static_cast<int>(T), static_cast<int>(geom_b),
+                                         static_cast<int>(geom_p), inv.p, off.p, cnt.p, list_u.p, list_g.p);
+  launched();
+  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list_u.p, list_g.p, grad,
+                                                      ugrad.p);
   launched();
 }
 
@@ -960,6 +990,15 @@ int ec_tables_dedup_mode(ec_tables t, int mode) {
     if (mode < 0 || mode > 2) invalid("dedup mode: 0 auto, 1 tiles, 2 cluster per table (when it fits)");
     Engine& e = E(t);
     e.dedup_mode = mode;
+    e.clear_graphs();
+  });
+}
+
+int ec_tables_scatter_mode(ec_tables t, int mode) {
+  return guard([&] {
+    if (mode < 0 || mode > 1) invalid("scatter mode: 0 transpose + segmented reduction, 1 float4 atomics");
+    Engine& e = E(t);
+    e.scatter_mode = mode;
     e.clear_graphs();
   });
 }

@@ -25,6 +25,7 @@
 
 #include "device_util.cuh"
 #include "engine.hpp"
+#include "scan.cuh"
 
 namespace ec {
 
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
                                                      const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                                                      const uint32_t* __restrict__ uslot,
                                                      const int32_t* __restrict__ usrc, const float* __restrict__ cache,
-                                                     float* __restrict__ urows, float* __restrict__ ugrad, int local_hbm,
-                                                     int rank, int world) {
+                                                     float* __restrict__ urows, float* __restrict__ ugrad,
+                                                     int* __restrict__ cnt, int local_hbm, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -307,7 +308,10 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
           v[r] = ldg4(src + m.c * 4);
           dst[r] = g;
         }
-        if (m.c == 0) td[tab].hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
+        if (m.c == 0) {
+          td[tab].hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
+          cnt[g] = 0;                           // backward occurrence count
+        }
         st4(ugrad + static_cast<int64_t>(g) * D + m.c * 4, zero);
       }
     }
@@ -785,6 +789,179 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
     if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
   }
   cluster.sync();  // keep DSMEM of every CTA alive until all remote reads are done
+}
+
+}  // namespace ec
+
+// ===================================================================
+// K6a as a transpose: gradients of a unique row are summed in registers.
+//
+//   k_bwd_count   per lookup: cnt[inverse] += 1 (match-any warp aggregation)
+//   k_uscan_*     off = exclusive scan of cnt over the U uniques (device U)
+//   k_bwd_fill    per lookup: slot = off[u] + cursor[u]++ ; lists hold (u, grad row)
+//   k_bwd_reduce  fixed 32-entry chunks of the u-grouped list per lane group:
+//                 runs of one u are summed in registers; runs wholly inside a
+//                 chunk are stored, the two boundary runs add atomically
+// Hot rows of tiny tables no longer serialise on L2 atomics: every grad row
+// is read once and ~2 float4 REDs per chunk remain.
+// ===================================================================
+namespace ec {
+
+constexpr int kRunChunk = 32;
+
+// grad-row index (bag) of lookup p in table t
+__device__ __forceinline__ int bag_of(const TableDev& tb, const int64_t* bag_off, int B, int P, int t, int64_t p) {
+  if (!bag_off) return static_cast<int>((p - tb.base) / P);
+  const int64_t* b = bag_off + static_cast<int64_t>(t) * B;  // last s with b[s] <= p
+  int lo = 0, hi = B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (b[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) k_bwd_count(const Tile* __restrict__ tiles, int ntiles,
+                                                        const uint32_t* __restrict__ inv, int* __restrict__ cnt) {
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const Tile tile = tiles[ti];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint32_t off = j * kThreads + threadIdx.x;
+      const uint32_t u = off < tile.count ? inv[tile.start + off] : kInvalidSlot;
+      const unsigned peers = __match_any_sync(kFull, u);
+      if (u != kInvalidSlot && (__ffs(peers) - 1) == lane_id()) atomicAdd(cnt + u, __popc(peers));
+    }
+  }
+}
+
+// Exclusive scan of cnt[0, U) with U read on the device; cnt is reset to 0 so
+// it can serve as the fill cursor.  part needs ceil(N / kScanTile) + 1 ints.
+__global__ void k_uscan_reduce(const int* __restrict__ cnt, const int* __restrict__ ctr, int T, int* __restrict__ part) {
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int s = 0;
+  if (base < U) {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const int64_t i = base + j * kScanThreads + threadIdx.x;
+      if (i < U) s += cnt[i];
+    }
+  }
+  const int v = __reduce_add_sync(kFull, s);
+  __shared__ int w[kScanThreads / 32];
+  if (lane_id() == 0) w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < kScanThreads / 32; ++k) t += w[k];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_uscan_apply(int* __restrict__ cnt, const int* __restrict__ ctr, int T, const int* __restrict__ part,
+                              int* __restrict__ off) {
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  if (base > U) return;  // whole block past the end (block-uniform)
+  __shared__ int sw[kScanThreads / 32];
+  int run = part[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int64_t i = base + j * kScanThreads + threadIdx.x;
+    const int v = i < U ? cnt[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan<kScanThreads>(v, sw, &tot);
+    if (i < U) {
+      off[i] = run + ex;
+      cnt[i] = 0;
+    } else if (i == U) {
+      off[i] = run + ex;  // total
+    }
+    run += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ tiles, int ntiles,
+                                                       const TableDev* __restrict__ td, const int64_t* __restrict__ bag_off,
+                                                       int T, int B, int P, const uint32_t* __restrict__ inv,
+                                                       const int* __restrict__ off, int* __restrict__ cursor,
+                                                       uint32_t* __restrict__ list_u, uint32_t* __restrict__ list_g) {
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const Tile tile = tiles[ti];
+    const TableDev tb = td[tile.table];
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const uint32_t o = j * kThreads + threadIdx.x;
+      const int64_t p = tile.start + o;
+      const uint32_t u = o < tile.count ? inv[p] : kInvalidSlot;
+      const unsigned peers = __match_any_sync(kFull, u);
+      const int leader = __ffs(peers) - 1;
+      int b0 = 0;
+      if (u != kInvalidSlot && leader == lane_id()) b0 = atomicAdd(cursor + u, __popc(peers));
+      b0 = __shfl_sync(kFull, b0, leader);
+      if (u != kInvalidSlot) {
+        const int pos = off[u] + b0 + __popc(peers & ((1u << lane_id()) - 1));
+        list_u[pos] = u;
+        list_g[pos] = static_cast<uint32_t>(bag_of(tb, bag_off, B, P, static_cast<int>(tile.table), p)) * T +
+                      tile.table;  // row of grad viewed as [B*T, D]
+      }
+    }
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
+                                                         const uint32_t* __restrict__ list_u,
+                                                         const uint32_t* __restrict__ list_g,
+                                                         const float* __restrict__ grad, float* __restrict__ ugrad) {
+  constexpr int D = VEC * 4;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int n = off[U];
+  const int groups = (gridDim.x * blockDim.x) / VEC;
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / VEC;
+  for (int c0 = gid * kRunChunk; c0 < n; c0 += groups * kRunChunk) {
+    const int c1 = min(n, c0 + kRunChunk);
+    uint32_t cu = list_u[c0];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool first_run = true;  // the run containing c0 may start before the chunk
+    int i = c0;
+    while (i < c1) {
+      // 4 grad rows in flight, then fold them in list order
+      uint32_t u4[4], g4[4];
+      float4 v4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool ok = i + k < c1;
+        u4[k] = ok ? list_u[i + k] : kInvalidSlot;
+        g4[k] = ok ? list_g[i + k] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        v4[k] = u4[k] != kInvalidSlot ? ld_stream4(grad + static_cast<int64_t>(g4[k]) * D + m.c * 4)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (u4[k] == kInvalidSlot) continue;
+        if (u4[k] != cu) {
+          // run of cu ends inside this chunk: sole owner unless it began before c0
+          float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
+          if (first_run && off[cu] < c0) atomicAdd(reinterpret_cast<float4*>(dst), acc);
+          else st4(dst, acc);
+          first_run = false;
+          cu = u4[k];
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        acc = add4(acc, v4[k]);
+      }
+      i += 4;
+    }
+    // last run: it may continue past the chunk, or began before it
+    float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
+    if ((first_run && off[cu] < c0) || off[cu + 1] > c1) atomicAdd(reinterpret_cast<float4*>(dst), acc);
+    else st4(dst, acc);
+  }
 }
 
 }  // namespace ec

@@ -13,7 +13,7 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void k_scan_reduce(const int* __restrict__ in, int64_t n, int* __restrict__ part) {
+static __global__ void k_scan_reduce(const int* __restrict__ in, int64_t n, int* __restrict__ part) {
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
   int s = 0;
 #pragma unroll
@@ -33,7 +33,7 @@ __global__ void k_scan_reduce(const int* __restrict__ in, int64_t n, int* __rest
 }
 
 // Single block: exclusive scan of `m` partials in place; total -> *total.
-__global__ void k_scan_partials(int* __restrict__ part, int m, int* __restrict__ total) {
+static __global__ void k_scan_partials(int* __restrict__ part, int m, int* __restrict__ total) {
   __shared__ int sw[32];
   int carry = 0;
   for (int base = 0; base < m; base += 1024) {
@@ -47,7 +47,7 @@ __global__ void k_scan_partials(int* __restrict__ part, int m, int* __restrict__
   if (threadIdx.x == 0 && total) *total = carry;
 }
 
-__global__ void k_scan_apply(const int* __restrict__ in, int64_t n, const int* __restrict__ part,
+static __global__ void k_scan_apply(const int* __restrict__ in, int64_t n, const int* __restrict__ part,
                              int* __restrict__ out) {
   __shared__ int sw[kScanThreads / 32];
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;

@@ -89,6 +89,7 @@ def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
     tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
     tab.use_graphs(graphs)
     tab.dedup_mode(mode)
+    tab.scatter_mode("atomic" if mode == "tiles" else "transpose")
     seed, scale = 1234, 0.05
     tab.init_synthetic(seed, scale)
     tab.place_cache(caches)
@@ -145,6 +146,7 @@ def test_csr_bags_empty_bags_and_empty_table(ec, torch):
     bag = np.concatenate([[0], np.cumsum(np.concatenate(lens))]).astype(np.int64)
     tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=max(n), max_batch_size=B)
     tab.init_synthetic(5, 1.0)
+    w0 = [tab.read_rows(t, np.arange(rows[t])) for t in range(3)]
     caches = [np.arange(10), [], np.arange(0, 1000, 3)]
     tab.place_cache(caches)
     ids = torch.from_numpy(ids_h.view(np.int32)).cuda()
@@ -152,9 +154,18 @@ def test_csr_bags_empty_bags_and_empty_table(ec, torch):
     out = tab.forward(ids, offs, B, bag_offsets=bag_t)
     check_batch(ec, tab, ids_h, offs, caches, rows, D, 5, 1.0, bag_offs=bag, B=B, out=out)
     assert (out.cpu().numpy()[:, D:2 * D] == 0).all()  # empty table pools to zeros
-    g = torch.ones(B, 3 * D, device="cuda")
+    g = torch.randn(B, 3 * D, device="cuda")
     tab.backward(g, 0.5)
     torch.cuda.synchronize()
+    gh = g.cpu().numpy()
+    for t in range(3):  # CSR bags through the transposed reduction (binary-searched bag of each lookup)
+        seg = ids_h[offs[t]:offs[t + 1]]
+        if not seg.size:
+            continue
+        u, inv = O.dedup(seg)
+        bo = bag[t * B:(t + 1) * B + 1] - offs[t]
+        _, want = O.backward_sgd(np.ascontiguousarray(gh[:, t * D:(t + 1) * D]), inv[:seg.size], bo, w0[t][u], 0.5)
+        np.testing.assert_allclose(tab.read_rows(t, u), want, rtol=RTOL, atol=1e-5 * np.abs(want).max())
     tab.close()
 
 
