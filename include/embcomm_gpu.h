@@ -253,10 +253,11 @@ int ec_tables_use_graphs(ec_tables t, int enable);
  * -> k_inverse_partition); 2 forces the cluster kernel whenever every
  * table's batch has <= 131072 lookups.  Identical results. */
 int ec_tables_dedup_mode(ec_tables t, int mode);
-/* Gradient reduction per unique row (K6a): 0 (default) transpose — lookups
- * grouped by unique (count, scan, fill) and summed in registers, runs inside a
- * 32-entry chunk stored, boundary runs added atomically; 1 one float4 atomic
- * per lookup after warp-level pre-aggregation. */
+/* Gradient reduction per unique row (K6a): 1 one float4 atomic per lookup
+ * after warp-level pre-aggregation; 2 transpose — lookups grouped by unique
+ * (count, scan, fill) and summed in registers, runs inside a 32-entry chunk
+ * stored, boundary runs added atomically; 0 (default) picks the transpose when
+ * some table has >= 32768 lookups in the batch. */
 int ec_tables_scatter_mode(ec_tables t, int mode);
 int ec_tables_profile_read(ec_tables t, double* ms_host, uint64_t* calls_host, uint64_t* launches,
                            int reset);

@@ -479,6 +479,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   ntiles = static_cast<int>(tl.size());
   int64_t nmax = 0;
   for (uint32_t t = 0; t < T; ++t) nmax = std::max<int64_t>(nmax, geom_off[t + 1] - geom_off[t]);
+  max_n_batch = nmax;
   // The cluster kernel wins when the tables alone fill the GPU and each
   // thread's dependency chain is short (measured: Kaggle 26 tables x 16K
   // lookups 43 vs 52 us; 8 tables x 82K lookups 104 vs 64 us).
@@ -564,7 +565,11 @@ template <int VEC>
 void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
   // ugrad rows and occurrence counts were zeroed by k_gather
-  if (scatter_mode == 1) {
+  // auto: the transpose pays off when tables see many lookups per batch (hot
+  // rows repeat thousands of times); measured: 26 x 65536 lookups 418 -> 175 us,
+  // 8 x 81920 91 -> 84 us, but 26 x 16384 30 -> 53 us
+  const bool atomic = scatter_mode == 1 || (scatter_mode == 0 && max_n_batch < 32768);
+  if (atomic) {
     k_scatter<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
                                                        bag_off, inv.p, grad, ugrad.p);
     launched();
@@ -996,7 +1001,7 @@ int ec_tables_dedup_mode(ec_tables t, int mode) {
 
 int ec_tables_scatter_mode(ec_tables t, int mode) {
   return guard([&] {
-    if (mode < 0 || mode > 1) invalid("scatter mode: 0 transpose + segmented reduction, 1 float4 atomics");
+    if (mode < 0 || mode > 2) invalid("scatter mode: 0 auto, 1 float4 atomics, 2 transpose");
     Engine& e = E(t);
     e.scatter_mode = mode;
     e.clear_graphs();

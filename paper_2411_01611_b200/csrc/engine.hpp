@@ -158,7 +158,8 @@ struct Engine {
   int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr, cnt, off, part;
   View<uint32_t> list_u, list_g;
-  int scatter_mode = 0;  // 0 transpose + segmented reduction, 1 float4 atomics
+  int scatter_mode = 0;  // 0 auto, 1 float4 atomics, 2 transpose + segmented reduction
+  int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
   void select(int i);
   DevBuf<Tile> tiles;
   DevBuf<int4> stiles;                // scatter tiles (table, bag lo, bag hi, -)

@@ -76,9 +76,9 @@ class EmbeddingTables:
         """"auto" (cluster per table when the tables fill the GPU), "tiles", or "cluster"."""
         check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1, "cluster": 2}[mode]))
 
-    def scatter_mode(self, mode: str = "transpose"):
-        """Backward gradient reduction: "transpose" (default) or "atomic"."""
-        check(N.lib().ec_tables_scatter_mode(self._h, {"transpose": 0, "atomic": 1}[mode]))
+    def scatter_mode(self, mode: str = "auto"):
+        """Backward gradient reduction: "auto", "atomic" or "transpose"."""
+        check(N.lib().ec_tables_scatter_mode(self._h, {"auto": 0, "atomic": 1, "transpose": 2}[mode]))
 
     def profile(self, enable: bool = True):
         """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""
