@@ -197,6 +197,17 @@ int ec_classify_samples(const uint32_t* ids_host, uint64_t num_samples, int64_t 
 int ec_schedule_order(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
                       uint64_t vocab, const uint32_t* cache_ids_host, uint64_t k, int device,
                       uint32_t* order_host, uint64_t* num_hot);
+/* build_skew_table (core/src/trace.cpp:128-150): access counts of the
+ * num_ids trace ids (histogram on the GPU), observed ids sorted by (count
+ * desc, id asc) with the running fraction of all accesses; output arrays need
+ * capacity min(num_ids, vocab); *num_entries = observed ids. */
+int ec_build_skew_table(const uint32_t* ids_host, uint64_t num_ids, uint64_t vocab, int device,
+                        uint32_t* ids_out_host, uint64_t* counts_out_host, double* cum_fraction_out_host,
+                        uint64_t* num_entries);
+/* estimate_distribution (trace.cpp:161-183): P(e) = (count + s) / (total + s*E). */
+int ec_estimate_distribution(const uint32_t* entry_ids_host, const uint64_t* entry_counts_host,
+                             uint64_t num_entries, uint64_t total_accesses, uint64_t vocab, double smoothing,
+                             ec_dist* out);
 
 /* --------------------------------------------------------- lookup engine
  * No reference counterpart (SURVEY.md §2 "★ new"): row-wise sharded fp32

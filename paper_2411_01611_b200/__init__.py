@@ -37,7 +37,7 @@ __all__ = [
     "delta_comm", "CachePlan", "optimal_cache_size_scan", "optimal_cache_size_search", "memory_io_proxy",
     "place_topk_global", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
     "SimResult", "measure_unique", "simulate_epoch", "Trace", "classify_samples", "build_schedule",
-    "SampleClasses", "BatchSchedule", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
+    "SampleClasses", "BatchSchedule", "SkewTable", "build_skew_table", "estimate_distribution", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
 ]
 
 kCostUnitsNote = "one unit = one embedding vector = one transmitted index"
@@ -518,6 +518,44 @@ def build_schedule(trace: Trace, cache_ids, batch_size: int, shuffle_seed: Optio
     def pack(v):
         return [v[i:i + batch_size].tolist() for i in range(0, len(v), batch_size)]
     return BatchSchedule(pack(order[:h]), pack(order[h:]), batch_size)
+
+
+@dataclass
+class SkewTable:
+    """SkewTable (core/include/embcomm/trace.hpp:39-51): observed ids ranked by
+    (count desc, id asc) with the running share of all accesses."""
+    ids: np.ndarray
+    counts: np.ndarray
+    cum_fraction: np.ndarray
+    total_accesses: int
+
+    @property
+    def entries(self):
+        return list(zip(self.ids.tolist(), self.counts.tolist(), self.cum_fraction.tolist()))
+
+
+def build_skew_table(trace: Trace, device: int = 0) -> SkewTable:
+    """build_skew_table (core/src/trace.cpp:128-150); histogram on the GPU."""
+    ids = _u32(trace.ids)
+    cap = max(1, min(ids.size, trace.vocab_size))
+    oid = np.empty(cap, np.uint32)
+    cnt = np.empty(cap, np.uint64)
+    cum = np.empty(cap, np.float64)
+    n = C.c_uint64()
+    check(N.lib().ec_build_skew_table(ids.ctypes.data, ids.size, trace.vocab_size, device, oid.ctypes.data,
+                                      cnt.ctypes.data, cum.ctypes.data, C.byref(n)))
+    k = n.value
+    return SkewTable(oid[:k].copy(), cnt[:k].copy(), cum[:k].copy(), int(ids.size))
+
+
+def estimate_distribution(table: SkewTable, vocab_size: int, smoothing: float = 0.0) -> EmbeddingDistribution:
+    """estimate_distribution (core/src/trace.cpp:161-183)."""
+    ids = _u32(table.ids)
+    cnt = np.ascontiguousarray(table.counts, dtype=np.uint64)
+    h = C.c_void_p()
+    check(N.lib().ec_estimate_distribution(ids.ctypes.data, cnt.ctypes.data, ids.size, table.total_accesses,
+                                           vocab_size, smoothing, C.byref(h)))
+    return EmbeddingDistribution(h.value)
 
 
 from .tables import EmbeddingGroup, EmbeddingTables, exchange_plan, shard_rows  # noqa: E402

@@ -535,4 +535,5 @@ int ec_place_topk_global(const ec_dist* dists, uint32_t T, uint64_t budget, uint
 
 namespace ec {
 const Dist& dist_of(ec_dist h) { return D(h); }
+ec_dist make_dist(Dist&& d) { return new ec_dist_s{std::move(d)}; }
 }  // namespace ec

@@ -30,6 +30,7 @@ struct Plan {
 
 const char* last_error();
 const Dist& dist_of(ec_dist h);
+ec_dist make_dist(Dist&& d);
 
 double presence(double p, int64_t b);
 double unique_from_rank(const Dist& d, int64_t b, uint64_t first);

@@ -613,3 +613,82 @@ int ec_simulate_trace(const uint32_t* ids, uint64_t q, int64_t d, uint64_t vocab
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ frequency placement (a17)
+// build_skew_table (core/src/trace.cpp:128-150): exact access counts — the
+// O(Q*d) histogram runs on the GPU — then the observed ids ordered by (count
+// desc, id asc) with the running fraction, on the host (O(S log S) over the S
+// observed ids).  estimate_distribution (trace.cpp:161-183) restated on the
+// host so probabilities and ranks are bit-identical.
+namespace {
+__global__ void k_histogram(const uint32_t* __restrict__ ids, uint64_t n, uint64_t vocab,
+                            unsigned long long* __restrict__ counts, int* __restrict__ bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = ids[i];
+    if (id >= vocab) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    // hot ids repeat inside a warp: one atomic per distinct id
+    const unsigned peers = __match_any_sync(__activemask(), id);
+    if ((__ffs(peers) - 1) == lane_id()) atomicAdd(counts + id, static_cast<unsigned long long>(__popc(peers)));
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ec_build_skew_table(const uint32_t* ids_host, uint64_t n, uint64_t vocab, int device, uint32_t* out_ids,
+                        uint64_t* out_counts, double* out_cum, uint64_t* n_entries) {
+  return guard([&] {
+    if (n == 0) invalid("empty trace");
+    if (vocab < 1) invalid("vocabulary size must be >= 1");
+    use_device(device);
+    Stream st;
+    DevBuf<uint32_t> d_ids(n);
+    DevBuf<unsigned long long> d_cnt(vocab);
+    DevBuf<int> d_bad(1);
+    EC_CUDA(cudaMemcpyAsync(d_ids.p, ids_host, n * sizeof(uint32_t), cudaMemcpyHostToDevice, st.s));
+    EC_CUDA(cudaMemsetAsync(d_cnt.p, 0, vocab * sizeof(unsigned long long), st.s));
+    EC_CUDA(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st.s));
+    k_histogram<<<grid_for(n, device), 256, 0, st.s>>>(d_ids.p, n, vocab, d_cnt.p, d_bad.p);
+    EC_LAUNCH();
+    std::vector<unsigned long long> cnt(vocab);
+    int bad = 0;
+    EC_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt.p, vocab * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st.s));
+    EC_CUDA(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, st.s));
+    EC_CUDA(cudaStreamSynchronize(st.s));
+    if (bad) invalid("trace id out of range [0, " + std::to_string(vocab) + ")");
+    std::vector<uint32_t> obs;
+    for (uint64_t id = 0; id < vocab; ++id)
+      if (cnt[id]) obs.push_back(static_cast<uint32_t>(id));
+    std::sort(obs.begin(), obs.end(), [&](uint32_t a, uint32_t b) { return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b; });
+    uint64_t run = 0;
+    for (size_t k = 0; k < obs.size(); ++k) {
+      run += cnt[obs[k]];
+      if (out_ids) out_ids[k] = obs[k];
+      if (out_counts) out_counts[k] = cnt[obs[k]];
+      if (out_cum) out_cum[k] = static_cast<double>(run) / static_cast<double>(n);
+    }
+    *n_entries = obs.size();
+  });
+}
+
+int ec_estimate_distribution(const uint32_t* entry_ids, const uint64_t* entry_counts, uint64_t n_entries,
+                             uint64_t total_accesses, uint64_t vocab, double smoothing, ec_dist* out) {
+  return guard([&] {
+    if (smoothing < 0.0) invalid("smoothing must be >= 0");
+    uint32_t max_id = 0;
+    for (uint64_t k = 0; k < n_entries; ++k) max_id = std::max(max_id, entry_ids[k]);
+    if (n_entries && vocab < static_cast<uint64_t>(max_id) + 1)
+      invalid("vocabulary size " + std::to_string(vocab) + " smaller than max observed id " + std::to_string(max_id));
+    if (vocab == 0) invalid("vocabulary size must be >= 1");
+    const double denom = static_cast<double>(total_accesses) + smoothing * static_cast<double>(vocab);
+    if (!(denom > 0.0)) invalid("cannot estimate a distribution from zero observations without smoothing");
+    std::vector<double> p(vocab, smoothing / denom);
+    for (uint64_t k = 0; k < n_entries; ++k) p[entry_ids[k]] = (static_cast<double>(entry_counts[k]) + smoothing) / denom;
+    *out = make_dist(Dist::from_probabilities(std::move(p)));
+  });
+}
+
+}  // extern "C"

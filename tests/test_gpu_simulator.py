@@ -147,3 +147,22 @@ def test_trace_validation(ec):
     assert ec.classify_samples(t, []).normal == [0, 1]
     c = ec.classify_samples(t, [0, 1])
     assert (c.hot, c.normal) == ([0], [1])
+
+
+def test_skew_table_bit_exact(ec, ref):
+    """build_skew_table (trace.cpp:128-150): GPU histogram + (count desc, id
+    asc) order, cumulative fractions identical to the reference; placement
+    from the estimated distribution equals the reference's top_ids."""
+    rng = np.random.default_rng(21)
+    for E, n, a in [(10, 100, 1.5), (5000, 200000, 1.2), (100000, 50000, 1.05)]:
+        ids = (rng.zipf(a, n) - 1).astype(np.uint32) % E
+        t = ec.Trace(1, E, ids)
+        st = ec.build_skew_table(t)
+        oid, cnt, cum = ref.ref_build_skew_table(ids, 1, E)
+        assert (st.ids == oid).all() and (st.counts == cnt).all() and (st.cum_fraction == cum).all()
+        d = ec.estimate_distribution(st, E, 0.0)
+        rd = ref.ref_estimate_distribution(ids, 1, E, 0.0)
+        k = min(E, 64)
+        assert (d.top_ids(k) == rd.top_ids(k)).all()
+    with pytest.raises(ec.ValidationError):
+        ec.build_skew_table(ec.Trace(1, 4, np.array([1, 9], np.uint32)))

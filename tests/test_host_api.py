@@ -204,3 +204,21 @@ def test_planner_vs_reference_randomized(ref, ec):
             rr = ref.ref_delta_comm(r, M, a, de, eff, q, k)
             assert (mm.candidate_id, mm.presence_gain, mm.threshold, mm.delta_comm, mm.recommend) == (
                 rr["candidate_id"], rr["presence_gain"], rr["threshold"], rr["delta_comm"], rr["recommend"])
+
+
+def test_estimate_distribution_vs_reference(ref, ec):
+    """estimate_distribution (trace.cpp:161-183) on the reference's own skew
+    table: identical ranked probabilities and rank -> id map."""
+    rng = np.random.default_rng(8)
+    for smoothing in (0.0, 0.5, 2.0):
+        E = int(rng.integers(2, 3000))
+        ids = rng.zipf(1.3, 5000).astype(np.uint32) % E
+        oid, cnt, cum = ref.ref_build_skew_table(ids, 1, E)
+        table = ec.SkewTable(oid, cnt, cum, ids.size)
+        mine = ec.estimate_distribution(table, E, smoothing)
+        theirs = ref.ref_estimate_distribution(ids, 1, E, smoothing)
+        rp, r2i = theirs.export()
+        assert (mine.ranked_probs() == rp).all() and (mine.rank_to_id() == r2i).all()
+    with pytest.raises(ec.ValidationError):
+        ec.estimate_distribution(ec.SkewTable(np.zeros(0, np.uint32), np.zeros(0, np.uint64),
+                                              np.zeros(0), 0), 10, 0.0)
