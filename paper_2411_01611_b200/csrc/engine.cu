@@ -291,8 +291,7 @@ void Engine::create(const ec_tables_config& c) {
     b.ctr.alloc(counters_size(T));
     b.cnt.alloc(N);
     b.off.alloc(N + 1);
-    b.list_u.alloc(N);
-    b.list_g.alloc(N);
+    b.list.alloc(N);
     b.part.alloc((N + kScanTile) / kScanTile + 1);
     EC_CUDA(cudaMemset(b.ctr.p, 0, b.ctr.bytes()));
   }
@@ -342,8 +341,7 @@ void Engine::select(int i) {
   cnt = view(b.cnt);
   off = view(b.off);
   part = view(b.part);
-  list_u = view(b.list_u);
-  list_g = view(b.list_g);
+  list = view(b.list);
 }
 
 uint64_t Engine::device_bytes() const {
@@ -556,8 +554,12 @@ template <int VEC>
 void Engine::fwd_pool(cudaStream_t st) {
   if (storage == EC_STORAGE_HOST && !consuming_prefetch) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PhaseScope ph(prof, kPhasePool, st);
-  k_pool<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off,
-                                                  inv.p, urows.p, out_ptr);
+  if (!bag_off && geom_p == 1) {
+    k_pool1<VEC, 8><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr);
+  } else {
+    k_pool<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+                                                    bag_off, inv.p, urows.p, out_ptr);
+  }
   launched();
 }
 
@@ -587,10 +589,9 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   k_uscan_apply<<<nparts, kScanThreads, 0, st>>>(cnt.p, ctr.p, static_cast<int>(T), part.p, off.p);
   launched();
   k_bwd_fill<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, tdev.p, bag_off, static_cast<int>(T), static_cast<int>(geom_b),
-                                         static_cast<int>(geom_p), inv.p, off.p, cnt.p, list_u.p, list_g.p);
+                                         static_cast<int>(geom_p), inv.p, off.p, cnt.p, list.p);
   launched();
-  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list_u.p, list_g.p, grad,
-                                                      ugrad.p);
+  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p);
   launched();
 }
 

@@ -59,14 +59,14 @@ struct BatchBufs {
   DevBuf<unsigned long long> status, tstat;  // tile / table look-back words
   DevBuf<int> ctr;
   DevBuf<int> cnt, off, part;          // backward transpose: occurrences per unique, offsets, scan partials
-  DevBuf<uint32_t> list_u, list_g;     // lookups grouped by unique: (unique, grad row)
+  DevBuf<uint2> list;                  // lookups grouped by unique: (unique, grad row)
   const uint32_t* indices = nullptr;  // batch held by a pending prefetch
   uint64_t geom_version = 0;
   bool pending = false;               // prefetched, not yet consumed by forward
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
            utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + tstat.bytes() + ctr.bytes() +
-           cnt.bytes() + off.bytes() + part.bytes() + list_u.bytes() + list_g.bytes();
+           cnt.bytes() + off.bytes() + part.bytes() + list.bytes();
   }
 };
 
@@ -157,7 +157,7 @@ struct Engine {
   bool cluster_ok = false;          // ... and the cluster path is the faster one
   int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr, cnt, off, part;
-  View<uint32_t> list_u, list_g;
+  View<uint2> list;
   int scatter_mode = 0;  // 0 auto, 1 float4 atomics, 2 transpose + segmented reduction
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
   void select(int i);

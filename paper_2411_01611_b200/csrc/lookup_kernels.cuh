@@ -423,6 +423,41 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
   }
 }
 
+// Pooling 1 (the Criteo configs): every bag is one lookup, so the pool is an
+// indexed row copy; R bags in flight per thread, evict-first stores for the
+// [B, T*D] output (written once, not re-read by this step).
+template <int VEC, int R>
+__global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__ td, int T, int B,
+                                                    const uint32_t* __restrict__ inv, const float* __restrict__ urows,
+                                                    float* __restrict__ out) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int nbags = T * B;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
+    uint32_t u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      u[r] = kInvalidSlot;
+      if (q < nbags) {
+        const int s = q / T, t = q - s * T;
+        u[r] = __ldcs(inv + td[t].base + s);
+      }
+    }
+    float4 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = load_row(urows, u[r], D, m.c);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      if (q < nbags) __stcs(reinterpret_cast<float4*>(out + static_cast<int64_t>(q) * D + m.c * 4), v[r]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K6
 // Bags visited table-major (q = t*B + s): the 32/VEC bags a warp holds are
 // consecutive samples of one table, so hot rows repeat inside the warp; lanes
@@ -886,7 +921,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ 
                                                        const TableDev* __restrict__ td, const int64_t* __restrict__ bag_off,
                                                        int T, int B, int P, const uint32_t* __restrict__ inv,
                                                        const int* __restrict__ off, int* __restrict__ cursor,
-                                                       uint32_t* __restrict__ list_u, uint32_t* __restrict__ list_g) {
+                                                       uint2* __restrict__ list) {
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const Tile tile = tiles[ti];
     const TableDev tb = td[tile.table];
@@ -902,9 +937,9 @@ __global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ 
       b0 = __shfl_sync(kFull, b0, leader);
       if (u != kInvalidSlot) {
         const int pos = off[u] + b0 + __popc(peers & ((1u << lane_id()) - 1));
-        list_u[pos] = u;
-        list_g[pos] = static_cast<uint32_t>(bag_of(tb, bag_off, B, P, static_cast<int>(tile.table), p)) * T +
-                      tile.table;  // row of grad viewed as [B*T, D]
+        // (unique, row of grad viewed as [B*T, D]) in one 8-byte store
+        list[pos] = make_uint2(u, static_cast<uint32_t>(bag_of(tb, bag_off, B, P, static_cast<int>(tile.table), p)) * T +
+                                      tile.table);
       }
     }
   }
@@ -912,8 +947,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ 
 
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
-                                                         const uint32_t* __restrict__ list_u,
-                                                         const uint32_t* __restrict__ list_g,
+                                                         const uint2* __restrict__ list,
                                                          const float* __restrict__ grad, float* __restrict__ ugrad) {
   constexpr int D = VEC * 4;
   const RowMap<VEC> m;
@@ -923,7 +957,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
   const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / VEC;
   for (int c0 = gid * kRunChunk; c0 < n; c0 += groups * kRunChunk) {
     const int c1 = min(n, c0 + kRunChunk);
-    uint32_t cu = list_u[c0];
+    uint32_t cu = list[c0].x;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     bool first_run = true;  // the run containing c0 may start before the chunk
     int i = c0;
@@ -933,9 +967,9 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
       float4 v4[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const bool ok = i + k < c1;
-        u4[k] = ok ? list_u[i + k] : kInvalidSlot;
-        g4[k] = ok ? list_g[i + k] : 0;
+        const uint2 e = i + k < c1 ? list[i + k] : make_uint2(kInvalidSlot, 0);
+        u4[k] = e.x;
+        g4[k] = e.y;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
