@@ -276,19 +276,29 @@ def run_ours(args, wl):
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
     e2e_end = torch.cuda.Event(enable_timing=True)
+    copy_stream = torch.cuda.Stream()
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def h2d(k):  # step k's ids, pinned host -> device, on the copy stream
+        with torch.cuda.stream(copy_stream):
+            dev_ids[k % 2].copy_(host_ids[k % N_BATCHES], non_blocking=True)
+            copied[k % 2].record(copy_stream)
+
     def e2e_steps(nsteps):
-        dev_ids[0].copy_(host_ids[0], non_blocking=True)
-        if args.prefetch:
-            tab.prefetch(dev_ids[0], offs, B, P)
+        # input pipelining: step k+1's H2D overlaps step k's compute; every
+        # step still moves its own ids host->device and reads its result back
+        h2d(0)
         res = None
         for k in range(nsteps):
-            cur_ids, nxt_ids = dev_ids[k % 2], dev_ids[(k + 1) % 2]
-            if not args.prefetch:
-                cur_ids.copy_(host_ids[k % N_BATCHES], non_blocking=True)
-            o = tab.forward(cur_ids, offs, B, P, out=out)
-            if args.prefetch:  # H2D of the next step's ids, then its prefetch
-                nxt_ids.copy_(host_ids[(k + 1) % N_BATCHES], non_blocking=True)
-                tab.prefetch(nxt_ids, offs, B, P)
+            stream.wait_event(copied[k % 2])
+            if k + 1 < nsteps:
+                h2d(k + 1)  # dev_ids[(k+1)%2] is free: step k-1 finished (its stats synchronised)
+            if args.prefetch and k == 0:
+                tab.prefetch(dev_ids[0], offs, B, P)
+            o = tab.forward(dev_ids[k % 2], offs, B, P, out=out)
+            if args.prefetch and k + 1 < nsteps:
+                stream.wait_event(copied[(k + 1) % 2])
+                tab.prefetch(dev_ids[(k + 1) % 2], offs, B, P)
             tab.backward(o, LR)
             res = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
         return res

@@ -223,6 +223,7 @@ Engine::~Engine() {
   if (pstream) cudaStreamDestroy(pstream);
   if (side2) cudaStreamDestroy(side2);
   if (ev_side2) cudaEventDestroy(ev_side2);
+  if (ctr_host) cudaFreeHost(ctr_host);
   if (ev_fwd) cudaEventDestroy(ev_fwd);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
@@ -297,6 +298,7 @@ void Engine::create(const ec_tables_config& c) {
   }
   for (BatchBufs& b : bb) b.tstat.alloc(T);
   select(0);
+  EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctr_host), counters_size(T) * sizeof(int), cudaHostAllocDefault));
   tiles.alloc(max_tiles);
   tdev.alloc(T);
   td_host.resize(T);
@@ -876,11 +878,11 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
 void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
   use_device(device);
   h.resize(counters_size(T));
+  // the counters are final once this batch's dedup/partition ran on `st`
+  // (a consumed prefetch was joined into `st`); one small pinned copy
+  EC_CUDA(cudaMemcpyAsync(ctr_host, ctr.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
   EC_CUDA(cudaStreamSynchronize(st));
-  EC_CUDA(cudaStreamSynchronize(side));
-  EC_CUDA(cudaStreamSynchronize(pstream));
-  EC_CUDA(cudaStreamSynchronize(side2));
-  EC_CUDA(cudaMemcpy(h.data(), ctr.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  std::memcpy(h.data(), ctr_host, h.size() * sizeof(int));
   Counters c = counters(h.data(), T);
   if (*c.err) {
     *c.err = 0;

@@ -157,6 +157,7 @@ struct Engine {
   bool cluster_ok = false;          // ... and the cluster path is the faster one
   int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr, cnt, off, part;
+  int* ctr_host = nullptr;  // pinned staging for ec_lookup_stats
   View<uint2> list;
   int scatter_mode = 0;  // 0 auto, 1 float4 atomics, 2 transpose + segmented reduction
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
