@@ -341,7 +341,7 @@ def run_ours(args, wl):
     dom_gbs = hbm_phases[dom]["gbs"]
     # dram bytes per launch of that kernel from the committed ncu --set full capture
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"r1_{args.workload}_traffic.json")
+    tfile = os.path.join(ROOT, "profiles", f"{args.workload}_traffic.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(dom)
     step_alg = sum(mean_bytes.values())
@@ -371,12 +371,12 @@ def run_ours(args, wl):
                    "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5),
-                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int(T * 8 * 2 + 72)},
+                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4)},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": round(dom_gbs / peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": hbm_phases[dom]["alg_bytes"],
-                     "traffic_source": (f"profiles/r1_{args.workload}_traffic.json (ncu --set full, dram read+write "
+                     "traffic_source": (f"profiles/{args.workload}_traffic.json (ncu --set full, dram read+write "
                                         "bytes per launch)") if traffic else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
         "step_alg_bytes": int(step_alg),
