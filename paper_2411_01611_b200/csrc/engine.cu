@@ -828,7 +828,7 @@ void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
     // one thread-block cluster per table: K1 + K2 in a single kernel
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
-    PhaseScope ph(prof, kPhaseInsert, st);
+    PhaseScope ph(prof, kPhaseDedupCluster, st);
     k_dedup_cluster<<<kClusterCtas * T, kClusterThreads, 0, st>>>(tdev.p, static_cast<int>(T), indices, slot_of.p,
                                                                  tstat.p, ctr.p, uniq.p, uslot.p, utab.p, inv.p,
                                                                  usrc.p, missq.p);
