@@ -58,7 +58,7 @@ class EmbeddingDistribution:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and N._lib is not None:
+        if h and N is not None and N._lib is not None:
             for s in self._sampler.values():
                 N._lib.ec_sampler_destroy(s)
             N._lib.ec_dist_destroy(h)
