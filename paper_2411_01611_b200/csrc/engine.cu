@@ -165,6 +165,13 @@ int Engine::host_grid() const {
   // concurrent HBM gather 4x)
   return env > 0 ? env : 32;
 }
+int Engine::host_write_grid() const {
+  static const int env = [] {
+    const char* v = std::getenv("EC_HOST_WRITE_CTAS");
+    return v ? std::atoi(v) : 0;
+  }();
+  return env > 0 ? env : host_grid();
+}
 int Engine::row_grid() const { return sm_count(device) * (storage == EC_STORAGE_HOST ? 3 : 4); }
 
 static uint32_t log2_ceil(uint64_t x) {
@@ -610,7 +617,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
     {
       PhaseScope ph(prof, kPhaseApplyHost, side2);
-      k_apply_host<VEC, 4><<<host_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+      k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
                                                                  ugrad.p, lr, rank, world);
       launched();
     }
