@@ -544,9 +544,12 @@ void Engine::fwd_gather_local(cudaStream_t st) {
     // host misses on the side stream, overlapping the HBM hit gather
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
+    PhaseScope ph(prof, kPhaseGatherHost, side);
     // few CTAs: the host link, not the SMs, bounds this kernel, and a full
     // persistent grid would hold every SM slot while it waits on PCIe reads
-    launch_gather_host<VEC>(side);
+    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                               world);
+    launched();
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
   PhaseScope ph(prof, kPhaseGather, st);
@@ -614,12 +617,8 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
     {
       PhaseScope ph(prof, kPhaseApplyHost, side2);
-      if (VEC % 2 == 0)
-        k_apply_host8<(VEC % 2 == 0 ? VEC / 2 : 1), 4><<<host_write_grid(), kThreads, 0, side2>>>(
-            tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, ugrad.p, lr, rank, world);
-      else
-        k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                         urows.p, ugrad.p, lr, rank, world);
+      k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                                 ugrad.p, lr, rank, world);
       launched();
     }
     EC_CUDA(cudaEventRecord(ev_side2, side2));
@@ -761,13 +760,8 @@ void Engine::drop_prefetch(cudaStream_t st) {
 template <int VEC>
 void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
-  if (VEC % 2 == 0) {  // 256-bit accesses over the host link
-    k_gather_host8<(VEC % 2 == 0 ? VEC / 2 : 1), 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p,
-                                                                                      utab.p, urows.p, rank, world);
-  } else {
-    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                            world);
-  }
+  k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                          world);
   launched();
 }
 

@@ -999,97 +999,3 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
 }
 
 }  // namespace ec
-
-// ===================================================================
-// Host-tier kernels with 256-bit accesses (LDG/STG.E.ENL2.256): a 64-byte
-// row is 2 requests instead of 4 on the host link, whose transaction rate —
-// not bytes — bounds these kernels.  L8 = D/8 lanes per row.
-// ===================================================================
-namespace ec {
-
-struct f8 {
-  float v[8];
-};
-__device__ __forceinline__ f8 ld8(const float* p) {
-  f8 r;
-  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
-                 "=f"(r.v[7])
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st8(float* p, const f8& r) {
-  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]),
-               "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
-               : "memory");
-}
-
-template <int L8, int R>
-__global__ void __launch_bounds__(kThreads) k_gather_host8(const TableDev* __restrict__ td, int T,
-                                                           const int* __restrict__ ctr,
-                                                           const uint32_t* __restrict__ missq,
-                                                           const uint32_t* __restrict__ uniq,
-                                                           const uint16_t* __restrict__ utab,
-                                                           float* __restrict__ urows, int rank, int world) {
-  constexpr int D = L8 * 8;
-  constexpr int RPW = 32 / L8;
-  const int sub = lane_id() / L8, c = lane_id() % L8;
-  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
-    f8 v[R];
-    int dst[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = q0 + r * RPW + sub;
-      dst[r] = -1;
-      if (q < nm) {
-        const uint32_t g = missq[q];
-        const uint32_t id = uniq[g];
-        if (static_cast<int>(id % world) == rank) {
-          v[r] = ld8(td[utab[g]].store + static_cast<int64_t>(id / world) * D + c * 8);
-          dst[r] = static_cast<int>(g);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (dst[r] >= 0) st8(urows + static_cast<int64_t>(dst[r]) * D + c * 8, v[r]);
-  }
-}
-
-template <int L8, int R>
-__global__ void __launch_bounds__(kThreads) k_apply_host8(const TableDev* __restrict__ td, int T,
-                                                          const int* __restrict__ ctr,
-                                                          const uint32_t* __restrict__ missq,
-                                                          const uint32_t* __restrict__ uniq,
-                                                          const uint16_t* __restrict__ utab,
-                                                          const float* __restrict__ urows,
-                                                          const float* __restrict__ ugrad, float lr, int rank,
-                                                          int world) {
-  constexpr int D = L8 * 8;
-  constexpr int RPW = 32 / L8;
-  const int sub = lane_id() / L8, c = lane_id() % L8;
-  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = q0 + r * RPW + sub;
-      if (q >= nm) continue;
-      const uint32_t g = missq[q];
-      const uint32_t id = uniq[g];
-      if (static_cast<int>(id % world) != rank) continue;
-      const f8 w = ld8(urows + static_cast<int64_t>(g) * D + c * 8);
-      const f8 gr = ld8(ugrad + static_cast<int64_t>(g) * D + c * 8);
-      f8 nw;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) nw.v[e] = w.v[e] - lr * gr.v[e];
-      st8(td[utab[g]].store + static_cast<int64_t>(id / world) * D + c * 8, nw);
-    }
-  }
-}
-
-}  // namespace ec
