@@ -139,6 +139,17 @@ int ec_optimal_cache_size_search(ec_dist d, const ec_device_model* m, const ec_w
                                  ec_cache_plan* out, uint32_t* cached_ids_host);    /* :206-289 */
 int ec_memory_io_proxy(ec_dist d, const ec_workload* w, const uint32_t* cache_ids_host,
                        uint64_t k, double* out);                                    /* :291-294 */
+/* GPU planner sweeps.  Many expected_unique_from_rank
+ * evaluations at once: out[i] = sum over ranks >= first_ranks[i] (NULL: 0) of
+ * 1-(1-p)^batch_sizes[i], fp64 terms reduced on the device (~1e-12 relative
+ * to the host's sequential sum, not bitwise).  ec_cost_curve evaluates the
+ * planner's cost of caching the top-k prefix at the Eq. 7 batch size (clamped
+ * to Q) for every k in ks (cache_planner.cpp:24-53); infeasible k give batch
+ * -1 and NaN costs.  The bit-exact planner is ec_optimal_cache_size_search. */
+int ec_expected_unique_many(ec_dist d, const int64_t* batch_sizes_host, const uint64_t* first_ranks_host,
+                            uint64_t n, int device, double* out_host);
+int ec_cost_curve(ec_dist d, const ec_device_model* m, const ec_workload* w, const int64_t* ks_host, uint64_t n,
+                  int device, ec_cost* out_host, int64_t* batch_out_host);
 /* Multi-table placement under one row budget: global top-`budget_rows` by
  * access probability across tables (ties: lower table, then the
  * distribution's own rank order).  Per table the chosen set is always a

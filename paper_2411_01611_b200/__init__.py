@@ -341,6 +341,31 @@ def memory_io_proxy(dist, spec: WorkloadSpec, cache_ids) -> float:
     return out.value
 
 
+def expected_unique_many(dist: EmbeddingDistribution, batch_sizes, first_ranks=None, device: int = 0) -> np.ndarray:
+    """Many expected_unique_from_rank evaluations at once on the GPU (fp64
+    terms, device reduction: ~1e-12 relative to the bit-exact host sum)."""
+    b = np.ascontiguousarray(batch_sizes, dtype=np.int64)
+    f = None if first_ranks is None else np.ascontiguousarray(first_ranks, dtype=np.uint64)
+    out = np.empty(b.size, np.float64)
+    check(N.lib().ec_expected_unique_many(dist._h, b.ctypes.data, None if f is None else f.ctypes.data, b.size,
+                                          device, out.ctypes.data))
+    return out
+
+
+def cost_curve(dist: EmbeddingDistribution, device_model: DeviceModel, num_samples: int, lookups_per_sample: int,
+               cache_sizes, device: int = 0):
+    """Planner cost of caching each top-k prefix at its Eq. 7 batch size
+    (cache_planner.cpp:24-53), all k on the GPU.  Returns (list of
+    CostBreakdown, batch sizes; -1 where no batch fits)."""
+    ks = np.ascontiguousarray(cache_sizes, dtype=np.int64)
+    out = (N.Cost * ks.size)()
+    bs = np.empty(ks.size, np.int64)
+    w = N.Workload(num_samples, 1, lookups_per_sample)
+    check(N.lib().ec_cost_curve(dist._h, C.byref(device_model._c()), C.byref(w), ks.ctypes.data, ks.size, device,
+                                out, bs.ctypes.data))
+    return [CostBreakdown._from(c) for c in out], bs
+
+
 def place_topk_global(dists: Sequence[EmbeddingDistribution], budget_rows: int) -> list[int]:
     """Per-table cache sizes for the global top-`budget_rows` rows by probability."""
     arr = (C.c_void_p * len(dists))(*[d._h.value for d in dists])

@@ -129,6 +129,8 @@ _SIGS = {
     "ec_optimal_cache_size_search": [vp, P(DeviceModelC), P(Workload), P(CachePlanC), vp],
     "ec_memory_io_proxy": [vp, P(Workload), vp, u64, P(f64)],
     "ec_place_topk_global": [vp, u32, u64, vp],
+    "ec_expected_unique_many": [vp, vp, vp, u64, C.c_int, vp],
+    "ec_cost_curve": [vp, P(DeviceModelC), P(Workload), vp, u64, C.c_int, vp, vp],
     "ec_sampler_create": [vp, C.c_int, P(vp)],
     "ec_sampler_destroy": [vp],
     "ec_sample_stream": [vp, u64, u64, u64, vp, vp],
