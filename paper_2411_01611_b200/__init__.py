@@ -35,7 +35,7 @@ __all__ = [
     "expected_unique_per_batch", "expected_unique_from_rank", "coalesced_batch_cost", "baseline_epoch_cost",
     "coalesced_epoch_cost", "cached_epoch_cost", "DeviceModel", "max_batch_size", "MarginalReport",
     "delta_comm", "CachePlan", "optimal_cache_size_scan", "optimal_cache_size_search", "memory_io_proxy",
-    "place_topk_global", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
+    "place_topk_global", "expected_unique_many", "cost_curve", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
     "SimResult", "measure_unique", "simulate_epoch", "Trace", "classify_samples", "build_schedule",
     "SampleClasses", "BatchSchedule", "SkewTable", "build_skew_table", "estimate_distribution", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
 ]
