@@ -321,6 +321,19 @@ typedef struct {
  * K1..K5 on `stream` (host misses on an internal side stream joined by an
  * event).  No host synchronisation unless world > 1. */
 int ec_lookup_fwd(ec_tables t, const ec_batch* batch, float* out_dev, void* stream);
+/* Hot/normal scheduling of a dataset (classify_samples +
+ * build_schedule, core/src/trace.cpp:185-240, with one id per table per
+ * sample): ids_dev is sample-major [q, num_tables]; a sample is hot iff every
+ * id is cached under the current placement.  order_dev (q entries) receives
+ * the hot samples then the normal ones, each in original order; *num_hot is
+ * the hot count (synchronises `stream`).  ec_tables_gather_batch writes
+ * samples order[first .. first+count) as a table-major pooling-1 batch
+ * (indices_dev[t*count + i]) ready for ec_lookup_fwd; batches cut inside the
+ * hot prefix never touch the cold tier. */
+int ec_tables_schedule(ec_tables t, const uint32_t* ids_dev, uint64_t num_samples, uint32_t* order_dev,
+                       uint64_t* num_hot, void* stream);
+int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t* order_dev, uint64_t first,
+                           uint32_t count, uint32_t* indices_dev, void* stream);
 /* Start the next batch while the current one finishes (single rank): its
  * dedup, hit/miss partition and pinned-host miss gather run on internal
  * streams into a second buffer set, overlapping the current backward; the

@@ -158,6 +158,8 @@ _SIGS = {
     "ec_lookup_bwd": [vp, vp, f32, vp],
     "ec_lookup_prefetch": [vp, P(Batch), vp],
     "ec_lookup_prefetch_wait": [vp, vp],
+    "ec_tables_schedule": [vp, vp, u64, vp, P(u64), vp],
+    "ec_tables_gather_batch": [vp, vp, vp, u64, u32, vp, vp],
     "ec_lookup_stats": [vp, vp, P(BatchStats), vp, vp],
     "ec_export_unique": [vp, u32, vp, u64, P(u64)],
     "ec_export_inverse": [vp, u32, vp],

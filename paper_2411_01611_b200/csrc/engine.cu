@@ -42,6 +42,7 @@
 #include "common.hpp"
 #include "device_util.cuh"
 #include "engine.hpp"
+#include "scan.cuh"
 
 namespace ec {
 
@@ -1061,6 +1062,46 @@ int ec_lookup_prefetch(ec_tables t, const ec_batch* b, void* stream) {
   return guard([&] {
     if (!b) invalid("null batch");
     E(t).prefetch(*b, as_stream(stream));
+  });
+}
+
+int ec_tables_schedule(ec_tables t, const uint32_t* ids_dev, uint64_t q, uint32_t* order_dev, uint64_t* num_hot,
+                       void* stream) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (!ids_dev || !order_dev || !num_hot) invalid("null argument");
+    if (q == 0) invalid("empty dataset");
+    if (q >= (1ull << 31)) invalid("at most 2^31-1 samples");
+    use_device(e.device);
+    cudaStream_t st = as_stream(stream);
+    DevBuf<int> hot(q), excl(q), part(scan_parts(q)), scal(2);
+    EC_CUDA(cudaMemsetAsync(scal.p, 0, 2 * sizeof(int), st));
+    const int grid = sm_count(e.device) * 4;
+    k_classify_tables<<<grid, 256, 0, st>>>(e.tdev.p, static_cast<int>(e.T), ids_dev, q, hot.p, scal.p + 1);
+    EC_LAUNCH();
+    exclusive_scan(hot.p, static_cast<int64_t>(q), excl.p, part.p, scal.p, st);
+    k_stable_order<<<grid, 256, 0, st>>>(hot.p, excl.p, scal.p, q, order_dev);
+    EC_LAUNCH();
+    int h[2];
+    EC_CUDA(cudaMemcpyAsync(h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    EC_CUDA(cudaStreamSynchronize(st));
+    if (h[1]) invalid("dataset id out of range of its table");
+    *num_hot = static_cast<uint64_t>(h[0]);
+  });
+}
+
+int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t* order_dev, uint64_t first,
+                           uint32_t count, uint32_t* indices_dev, void* stream) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (!ids_dev || !order_dev || !indices_dev) invalid("null argument");
+    use_device(e.device);
+    if (!count) return;
+    const uint64_t n = static_cast<uint64_t>(count) * e.T;
+    const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, sm_count(e.device) * 8ull));
+    k_gather_batch<<<grid, 256, 0, as_stream(stream)>>>(ids_dev, order_dev, first, count, static_cast<int>(e.T),
+                                                         indices_dev);
+    EC_LAUNCH();
   });
 }
 

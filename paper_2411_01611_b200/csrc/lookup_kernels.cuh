@@ -999,3 +999,50 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
 }
 
 }  // namespace ec
+
+// ===================================================================
+// Hot/normal scheduling of a multi-table dataset (
+// classify_samples / build_schedule, core/src/trace.cpp:185-240, extended to
+// one id per table per sample): a sample is hot iff every id is cached.
+// ===================================================================
+namespace ec {
+
+__global__ void k_classify_tables(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ ids, uint64_t q,
+                                  int* __restrict__ hot, int* __restrict__ err) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < q; s += (uint64_t)gridDim.x * blockDim.x) {
+    int h = 1;
+    for (int t = 0; t < T; ++t) {
+      const uint32_t id = ids[s * T + t];
+      const TableDev tb = td[t];
+      if (id >= tb.rows) {
+        atomicExch(err, 1);
+        h = 0;
+        continue;
+      }
+      h &= __ldg(tb.remap + id) >= 0;
+    }
+    hot[s] = h;
+  }
+}
+
+__global__ void k_stable_order(const int* __restrict__ hot, const int* __restrict__ excl, const int* __restrict__ n_hot,
+                               uint64_t q, uint32_t* __restrict__ order) {
+  const int H = *n_hot;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < q; s += (uint64_t)gridDim.x * blockDim.x) {
+    const int e = excl[s];
+    order[hot[s] ? e : H + static_cast<int>(s) - e] = static_cast<uint32_t>(s);
+  }
+}
+
+// indices[t*count + i] = ids[order[first + i]*T + t]: a batch in the
+// table-major layout ec_lookup_fwd takes (pooling 1).
+__global__ void k_gather_batch(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ order, uint64_t first,
+                               uint32_t count, int T, uint32_t* __restrict__ out) {
+  const uint64_t n = static_cast<uint64_t>(count) * T;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = i / count, k = i - t * count;
+    out[i] = ids[static_cast<uint64_t>(order[first + k]) * T + t];
+  }
+}
+
+}  // namespace ec

@@ -155,6 +155,27 @@ class EmbeddingTables:
         b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo, batch_size, pooling)
         check(N.lib().ec_lookup_prefetch(self._h, C.byref(b), _stream_ptr(self.torch, self.device)))
 
+    def schedule(self, sample_ids):
+        """Hot/normal order of a dataset (sample-major [q, T] int32/uint32 CUDA
+        tensor): returns (order tensor, number of hot samples).  A sample is hot
+        iff all its ids are cached (classify_samples, trace.cpp:185-204)."""
+        torch = self.torch
+        q = sample_ids.numel() // self.T
+        order = torch.empty(q, dtype=torch.int32, device=sample_ids.device)
+        nh = C.c_uint64()
+        check(N.lib().ec_tables_schedule(self._h, sample_ids.data_ptr(), q, order.data_ptr(), C.byref(nh),
+                                         _stream_ptr(torch, self.device)))
+        return order, int(nh.value)
+
+    def gather_batch(self, sample_ids, order, first: int, count: int, out=None):
+        """Samples order[first:first+count] as a table-major pooling-1 batch."""
+        torch = self.torch
+        if out is None:
+            out = torch.empty(count * self.T, dtype=torch.int32, device=sample_ids.device)
+        check(N.lib().ec_tables_gather_batch(self._h, sample_ids.data_ptr(), order.data_ptr(), first, count,
+                                             out.data_ptr(), _stream_ptr(torch, self.device)))
+        return out
+
     def prefetch_wait(self):
         """Make the current stream wait for a pending prefetch."""
         check(N.lib().ec_lookup_prefetch_wait(self._h, _stream_ptr(self.torch, self.device)))
