@@ -318,6 +318,44 @@ def run_ours(args, wl):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---- hot/normal scheduling (paper §Experiment Settings):
+    # one epoch of EPOCH_BATCHES batches timed in dataset order and in the
+    # GPU-built hot-first order; hot batches never reach the cold tier
+    hot_normal = None
+    if world == 1 and args.schedule_batches > 0 and P == 1:
+        q = args.schedule_batches * B
+        per_table = torch.empty((T, q), dtype=torch.int32, device="cuda")
+        for t, d in enumerate(dists):
+            ec.DiscreteSampler(d, local).sample_into(per_table[t].data_ptr(), batch_seed(rank, 1000, t), 0, q)
+        samples = per_table.t().contiguous()  # sample-major [q, T]
+        natural = torch.arange(q, dtype=torch.int32, device="cuda")
+        sched, n_hot = tab.schedule(samples)
+        bbuf = torch.empty(T * B, dtype=torch.int32, device="cuda")
+
+        def epoch(order):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.schedule_batches)]
+            for i, (a, z) in enumerate(ev):
+                flush.fill_(float(i))
+                a.record(stream)
+                tab.gather_batch(samples, order, i * B, B, out=bbuf)
+                o = tab.forward(bbuf, offs, B, P, out=out)
+                tab.backward(o, LR)
+                z.record(stream)
+            torch.cuda.synchronize()
+            return sum(a.elapsed_time(z) for a, z in ev)
+
+        epoch(natural)
+        epoch(sched)  # warm both (graph capture of the batch buffer)
+        t_nat = epoch(natural)
+        t_sch = epoch(sched)
+        look = q * T
+        hot_normal = {"batches": args.schedule_batches, "samples": q, "hot_samples": n_hot,
+                      "hot_batches": n_hot // B,
+                      "lookups_per_s_dataset_order": round(look / (t_nat * 1e-3), 1),
+                      "lookups_per_s_hot_first": round(look / (t_sch * 1e-3), 1),
+                      "speedup": round(t_nat / t_sch, 3)}
+
     # ---- roofline of the dominant kernel + whole-step algorithmic traffic
     import statistics as S
     pb = [phase_bytes(s, wl, T) for s in stats]
@@ -386,6 +424,7 @@ def run_ours(args, wl):
         "comm": {"model_rows_per_batch": s0["miss_rows"], "model_bytes_per_batch": s0["model_bytes"],
                  "unique_rows_per_batch": s0["unique_rows"], "hit_rows_per_batch": s0["hit_rows"],
                  "wire_bytes_per_batch": s0["wire_bytes"]},
+        "hot_normal_schedule": hot_normal,
         "setup_s": round(setup_s, 1),
     }
     res["clocks"] = clk.summary()
@@ -500,6 +539,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="kaggle")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule-batches", type=int, default=32,
+                    help="epoch length for the hot/normal scheduling measurement (0: skip)")
     ap.add_argument("--prefetch", action="store_true",
                     help="pipelined steps: ec_lookup_prefetch of the next batch overlaps this backward")
     args = ap.parse_args()
