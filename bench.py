@@ -343,15 +343,19 @@ def run_ours(args, wl):
                 tab.backward(o, LR)
                 z.record(stream)
             torch.cuda.synchronize()
-            return sum(a.elapsed_time(z) for a, z in ev)
+            return [a.elapsed_time(z) for a, z in ev]
 
         epoch(natural)
         epoch(sched)  # warm both (graph capture of the batch buffer)
-        t_nat = epoch(natural)
-        t_sch = epoch(sched)
+        t_nat = sum(epoch(natural))
+        per = epoch(sched)
+        t_sch = sum(per)
         look = q * T
+        nhb = n_hot // B
         hot_normal = {"batches": args.schedule_batches, "samples": q, "hot_samples": n_hot,
-                      "hot_batches": n_hot // B,
+                      "hot_batches": nhb,
+                      "ms_per_hot_batch": round(sum(per[:nhb]) / max(1, nhb), 5),
+                      "ms_per_normal_batch": round(sum(per[nhb:]) / max(1, len(per) - nhb), 5),
                       "lookups_per_s_dataset_order": round(look / (t_nat * 1e-3), 1),
                       "lookups_per_s_hot_first": round(look / (t_sch * 1e-3), 1),
                       "speedup": round(t_nat / t_sch, 3)}
