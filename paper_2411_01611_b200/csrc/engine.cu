@@ -545,12 +545,9 @@ void Engine::fwd_gather_local(cudaStream_t st) {
     // host misses on the side stream, overlapping the HBM hit gather
     EC_CUDA(cudaEventRecord(ev_part, st));
     EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
-    PhaseScope ph(prof, kPhaseGatherHost, side);
     // few CTAs: the host link, not the SMs, bounds this kernel, and a full
     // persistent grid would hold every SM slot while it waits on PCIe reads
-    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                               world);
-    launched();
+    launch_gather_host<VEC>(side);
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
   PhaseScope ph(prof, kPhaseGather, st);
@@ -761,8 +758,13 @@ void Engine::drop_prefetch(cudaStream_t st) {
 template <int VEC>
 void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
-  k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                          world);
+  static const bool tma = std::getenv("EC_HOST_TMA") != nullptr;
+  if (tma)
+    k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                             world);
+  else
+    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                            world);
   launched();
 }
 

@@ -1046,3 +1046,77 @@ __global__ void k_gather_batch(const uint32_t* __restrict__ ids, const uint32_t*
 }
 
 }  // namespace ec
+
+// ===================================================================
+// Experimental: pinned-host misses fetched by the TMA bulk-copy engine
+// (cp.async.bulk global -> shared, completion counted on an mbarrier) rather
+// than by SM loads; rows then go smem -> urows.  One elected thread per CTA
+// issues a batch of row copies.
+// ===================================================================
+namespace ec {
+
+constexpr int kTmaRows = 64;  // rows in flight per CTA
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __restrict__ td, int T,
+                                                              const int* __restrict__ ctr,
+                                                              const uint32_t* __restrict__ missq,
+                                                              const uint32_t* __restrict__ uniq,
+                                                              const uint16_t* __restrict__ utab,
+                                                              float* __restrict__ urows, int rank, int world) {
+  constexpr int D = VEC * 4;
+  constexpr uint32_t kRowBytes = D * 4;
+  __shared__ __align__(128) float buf[kTmaRows * D];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ uint32_t dst_g[kTmaRows];
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const uint32_t bar_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar_addr));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int q0 = blockIdx.x * kTmaRows; q0 < nm; q0 += gridDim.x * kTmaRows) {
+    const int cnt = min(kTmaRows, nm - q0);
+    if (threadIdx.x == 0) {
+      uint32_t bytes = 0;
+      for (int r = 0; r < cnt; ++r) {
+        const uint32_t g = missq[q0 + r];
+        const uint32_t id = uniq[g];
+        dst_g[r] = g;
+        if (static_cast<int>(id % world) != rank) {
+          dst_g[r] = 0xFFFFFFFFu;
+          continue;
+        }
+        bytes += kRowBytes;
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_addr), "r"(bytes) : "memory");
+      for (int r = 0; r < cnt; ++r) {
+        const uint32_t g = dst_g[r];
+        if (g == 0xFFFFFFFFu) continue;
+        const float* src = td[utab[g]].store + static_cast<int64_t>(uniq[g] / world) * D;
+        const uint32_t dsts = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dsts),
+                     "l"(src), "r"(kRowBytes), "r"(bar_addr)
+                     : "memory");
+      }
+    }
+    // wait for the bytes of this batch
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(bar_addr),
+        "r"(phase)
+        : "memory");
+    phase ^= 1;
+    for (int i = threadIdx.x; i < cnt * VEC; i += blockDim.x) {
+      const int r = i / VEC, c = i - r * VEC;
+      const uint32_t g = dst_g[r];
+      if (g != 0xFFFFFFFFu)
+        st4(urows + static_cast<int64_t>(g) * D + c * 4, *reinterpret_cast<const float4*>(buf + r * D + c * 4));
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace ec
