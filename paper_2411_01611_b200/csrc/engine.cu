@@ -615,8 +615,13 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
     {
       PhaseScope ph(prof, kPhaseApplyHost, side2);
-      k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
-                                                                 ugrad.p, lr, rank, world);
+      static const bool tma = std::getenv("EC_HOST_TMA") != nullptr;
+      if (tma)
+        k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+                                                                          urows.p, ugrad.p, lr, rank, world);
+      else
+        k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+                                                                         urows.p, ugrad.p, lr, rank, world);
       launched();
     }
     EC_CUDA(cudaEventRecord(ev_side2, side2));

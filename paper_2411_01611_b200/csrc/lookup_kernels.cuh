@@ -1055,7 +1055,7 @@ __global__ void k_gather_batch(const uint32_t* __restrict__ ids, const uint32_t*
 // ===================================================================
 namespace ec {
 
-constexpr int kTmaRows = 64;  // rows in flight per CTA
+constexpr int kTmaRows = 128;  // rows in flight per CTA
 
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __restrict__ td, int T,
@@ -1117,6 +1117,62 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
     }
     __syncthreads();
   }
+}
+
+}  // namespace ec
+
+namespace ec {
+
+// Host write-back through the TMA engine: new rows are built in shared memory
+// and bulk-stored to the pinned host shard (cp.async.bulk global <- shared).
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __restrict__ td, int T,
+                                                             const int* __restrict__ ctr,
+                                                             const uint32_t* __restrict__ missq,
+                                                             const uint32_t* __restrict__ uniq,
+                                                             const uint16_t* __restrict__ utab,
+                                                             const float* __restrict__ urows,
+                                                             const float* __restrict__ ugrad, float lr, int rank,
+                                                             int world) {
+  constexpr int D = VEC * 4;
+  constexpr uint32_t kRowBytes = D * 4;
+  __shared__ __align__(128) float buf[kTmaRows * D];
+  __shared__ uint32_t dst_g[kTmaRows];
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  for (int q0 = blockIdx.x * kTmaRows; q0 < nm; q0 += gridDim.x * kTmaRows) {
+    const int cnt = min(kTmaRows, nm - q0);
+    if (threadIdx.x < cnt) {
+      const uint32_t g = missq[q0 + threadIdx.x];
+      dst_g[threadIdx.x] = static_cast<int>(uniq[g] % world) == rank ? g : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * VEC; i += blockDim.x) {
+      const int r = i / VEC, c = i - r * VEC;
+      const uint32_t g = dst_g[r];
+      if (g == 0xFFFFFFFFu) continue;
+      const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + c * 4);
+      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4);
+      *reinterpret_cast<float4*>(buf + r * D + c * 4) =
+          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async (TMA) proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < cnt; ++r) {
+        const uint32_t g = dst_g[r];
+        if (g == 0xFFFFFFFFu) continue;
+        float* dst = td[utab[g]].store + static_cast<int64_t>(uniq[g] / world) * D;
+        const uint32_t srcs = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srcs),
+                     "r"(kRowBytes)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem reusable
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes done before exit
 }
 
 }  // namespace ec
