@@ -1055,7 +1055,7 @@ __global__ void k_gather_batch(const uint32_t* __restrict__ ids, const uint32_t*
 // ===================================================================
 namespace ec {
 
-constexpr int kTmaRows = 128;  // rows in flight per CTA
+constexpr int kTmaBytes = 16384;  // staged row bytes in flight per CTA
 
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __restrict__ td, int T,
@@ -1066,6 +1066,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
                                                               float* __restrict__ urows, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
+  constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
   __shared__ __align__(128) float buf[kTmaRows * D];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ uint32_t dst_g[kTmaRows];
@@ -1079,30 +1080,26 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
   uint32_t phase = 0;
   for (int q0 = blockIdx.x * kTmaRows; q0 < nm; q0 += gridDim.x * kTmaRows) {
     const int cnt = min(kTmaRows, nm - q0);
-    if (threadIdx.x == 0) {
-      uint32_t bytes = 0;
-      for (int r = 0; r < cnt; ++r) {
-        const uint32_t g = missq[q0 + r];
-        const uint32_t id = uniq[g];
-        dst_g[r] = g;
-        if (static_cast<int>(id % world) != rank) {
-          dst_g[r] = 0xFFFFFFFFu;
-          continue;
-        }
-        bytes += kRowBytes;
-      }
-      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_addr), "r"(bytes) : "memory");
-      for (int r = 0; r < cnt; ++r) {
-        const uint32_t g = dst_g[r];
-        if (g == 0xFFFFFFFFu) continue;
-        const float* src = td[utab[g]].store + static_cast<int64_t>(uniq[g] / world) * D;
-        const uint32_t dsts = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         dsts),
-                     "l"(src), "r"(kRowBytes), "r"(bar_addr)
-                     : "memory");
-      }
+    // every thread issues the bulk copies of its rows; thread 0 arms the barrier
+    // with the batch's byte count (tx may complete before the expect: the phase
+    // still needs thread 0's arrival)
+    int mine = 0;
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      const uint32_t g = missq[q0 + r];
+      const uint32_t id = uniq[g];
+      const bool own = static_cast<int>(id % world) == rank;
+      dst_g[r] = own ? g : 0xFFFFFFFFu;
+      if (!own) continue;
+      ++mine;
+      const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+      const uint32_t dsts = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dsts),
+                   "l"(src), "r"(kRowBytes), "r"(bar_addr)
+                   : "memory");
     }
+    const int rows = __syncthreads_count(mine);  // mine <= 1 when cnt <= blockDim
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_addr), "r"(rows * kRowBytes) : "memory");
     // wait for the bytes of this batch
     asm volatile(
         "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(bar_addr),
@@ -1136,6 +1133,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
                                                              int world) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
+  constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
   __shared__ __align__(128) float buf[kTmaRows * D];
   __shared__ uint32_t dst_g[kTmaRows];
   const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
@@ -1157,22 +1155,19 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async (TMA) proxy
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int r = 0; r < cnt; ++r) {
-        const uint32_t g = dst_g[r];
-        if (g == 0xFFFFFFFFu) continue;
-        float* dst = td[utab[g]].store + static_cast<int64_t>(uniq[g] / world) * D;
-        const uint32_t srcs = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srcs),
-                     "r"(kRowBytes)
-                     : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem reusable
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      const uint32_t g = dst_g[r];
+      if (g == 0xFFFFFFFFu) continue;
+      float* dst = td[utab[g]].store + static_cast<int64_t>(uniq[g] / world) * D;
+      const uint32_t srcs = static_cast<uint32_t>(__cvta_generic_to_shared(buf + r * D));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(srcs), "r"(kRowBytes)
+                   : "memory");
     }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem reusable
     __syncthreads();
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes done before exit
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes done before exit
 }
 
 }  // namespace ec
