@@ -160,11 +160,24 @@ int Engine::host_grid() const {
     const char* v = std::getenv("EC_HOST_CTAS");
     return v ? std::atoi(v) : 0;
   }();
-  // 32 CTAs x 256 threads keep ~8k row reads in flight, enough to saturate the
-  // host link for 64-256 B rows, while leaving the L2/HBM request queues to the
-  // main-stream kernels (measured: 8 CTAs starve the link, >= 148 slow the
-  // concurrent HBM gather 4x)
-  return env > 0 ? env : 32;
+  if (env > 0) return env;
+  // TMA path: the copy engine holds the row reads, so CTAs are cheap -- 2 per
+  // SM keep 16 KiB each in flight (measured best of 74/148/296).
+  // LSU path: 32 CTAs x 256 threads keep ~8k row reads in flight, enough to
+  // saturate the host link for 64-256 B rows, while leaving the L2/HBM request
+  // queues to the main-stream kernels (measured: 8 CTAs starve the link, >= 148
+  // slow the concurrent HBM gather 4x)
+  return host_tma() ? sm_count(device) * 2 : 32;
+}
+// Host-link row traffic goes through the TMA bulk-copy engine unless
+// EC_HOST_TMA=0: its reads do not occupy the LSU/L1 miss queues, so the
+// concurrent HBM gather runs at its isolated speed (35 -> 14 us, Kaggle).
+bool Engine::host_tma() {
+  static const bool on = [] {
+    const char* v = std::getenv("EC_HOST_TMA");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 int Engine::host_write_grid() const {
   static const int env = [] {
@@ -615,7 +628,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
     {
       PhaseScope ph(prof, kPhaseApplyHost, side2);
-      static const bool tma = std::getenv("EC_HOST_TMA") != nullptr;
+      const bool tma = host_tma();
       if (tma)
         k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
                                                                           urows.p, ugrad.p, lr, rank, world);
@@ -763,7 +776,7 @@ void Engine::drop_prefetch(cudaStream_t st) {
 template <int VEC>
 void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
-  static const bool tma = std::getenv("EC_HOST_TMA") != nullptr;
+  const bool tma = host_tma();
   if (tma)
     k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
                                                              world);

@@ -203,6 +203,7 @@ struct Engine {
   void create(const ec_tables_config& c);
   uint64_t device_bytes() const;
   int host_grid() const;
+  static bool host_tma();
   int host_write_grid() const;
   int row_grid() const;
   void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
