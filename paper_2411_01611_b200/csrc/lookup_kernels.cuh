@@ -1078,8 +1078,10 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
   }
   __syncthreads();
   uint32_t phase = 0;
-  for (int q0 = blockIdx.x * kTmaRows; q0 < nm; q0 += gridDim.x * kTmaRows) {
-    const int cnt = min(kTmaRows, nm - q0);
+  // spread the misses over every CTA (each SM's TMA unit issues its own rows)
+  const int chunk = max(1, min(kTmaRows, (nm + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x)));
+  for (int q0 = blockIdx.x * chunk; q0 < nm; q0 += gridDim.x * chunk) {
+    const int cnt = min(chunk, nm - q0);
     // every thread issues the bulk copies of its rows; thread 0 arms the barrier
     // with the batch's byte count (tx may complete before the expect: the phase
     // still needs thread 0's arrival)
@@ -1137,8 +1139,10 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
   __shared__ __align__(128) float buf[kTmaRows * D];
   __shared__ uint32_t dst_g[kTmaRows];
   const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
-  for (int q0 = blockIdx.x * kTmaRows; q0 < nm; q0 += gridDim.x * kTmaRows) {
-    const int cnt = min(kTmaRows, nm - q0);
+  // spread the misses over every CTA (each SM's TMA unit issues its own rows)
+  const int chunk = max(1, min(kTmaRows, (nm + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x)));
+  for (int q0 = blockIdx.x * chunk; q0 < nm; q0 += gridDim.x * chunk) {
+    const int cnt = min(chunk, nm - q0);
     if (threadIdx.x < cnt) {
       const uint32_t g = missq[q0 + threadIdx.x];
       dst_g[threadIdx.x] = static_cast<int>(uniq[g] % world) == rank ? g : 0xFFFFFFFFu;
