@@ -245,7 +245,7 @@ Engine::~Engine() {
   if (side2) cudaStreamDestroy(side2);
   if (ev_side2) cudaEventDestroy(ev_side2);
   if (ctr_host) cudaFreeHost(ctr_host);
-  if (ev_fwd) cudaEventDestroy(ev_fwd);
+  if (ev_release) cudaEventDestroy(ev_release);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
@@ -295,7 +295,9 @@ void Engine::create(const ec_tables_config& c) {
   }
   remap.alloc(remap_off[T]);
   EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
-  hash.alloc(hash_off[T]);
+  // one dedup hash per batch-buffer set: a prefetched batch's dedup never
+  // waits for the current batch's gather to clean the shared slots
+  hash.alloc(2 * hash_off[T]);
   EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
   const uint64_t N = max_n * T;
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
@@ -321,7 +323,7 @@ void Engine::create(const ec_tables_config& c) {
   select(0);
   EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctr_host), counters_size(T) * sizeof(int), cudaHostAllocDefault));
   tiles.alloc(max_tiles);
-  tdev.alloc(T);
+  tdev_buf.alloc(2 * T);
   td_host.resize(T);
   for (uint32_t t = 0; t < T; ++t) {
     TableDev& d = td_host[t];
@@ -334,20 +336,29 @@ void Engine::create(const ec_tables_config& c) {
     d.base = 0;
     d.n = 0;
   }
-  EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
+  upload_tdev();
+  select(cur);
   EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   EC_CUDA(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
   EC_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
-  EC_CUDA(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_release, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
 }
 
+void Engine::upload_tdev() {
+  std::vector<TableDev> both(td_host);
+  both.insert(both.end(), td_host.begin(), td_host.end());
+  for (uint32_t t = 0; t < T; ++t) both[T + t].hash += hash_off[T];
+  EC_CUDA(cudaMemcpy(tdev_buf.p, both.data(), both.size() * sizeof(TableDev), cudaMemcpyHostToDevice));
+}
+
 void Engine::select(int i) {
   cur = i;
+  tdev = View<TableDev>{tdev_buf.p + static_cast<size_t>(i) * T, T};
   BatchBufs& b = bb[i];
   slot_of = view(b.slot_of);
   inv = view(b.inv);
@@ -531,7 +542,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   select(cur);
   if (stiles.n < sc.size()) stiles.alloc(sc.size());
   if (nstiles) EC_CUDA(cudaMemcpy(stiles.p, sc.data(), sc.size() * sizeof(int4), cudaMemcpyHostToDevice));
-  EC_CUDA(cudaMemcpy(tdev.p, td_host.data(), T * sizeof(TableDev), cudaMemcpyHostToDevice));
+  upload_tdev();
   geom_b = b.batch_size;
   geom_p = b.pooling;
   geom_fixed = b.bag_offsets_dev == nullptr;
@@ -694,6 +705,9 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     if (nx.indices == b.indices_dev && nx.geom_version == geom_version) {
       // dedup, hit/miss and host-miss gather already ran (ec_lookup_prefetch)
       nx.pending = false;
+      // everything enqueued so far (last batch's backward and its host-tier
+      // joins) used the outgoing set: the next prefetch may reuse it after this
+      EC_CUDA(cudaEventRecord(ev_release, st));
       select(cur ^ 1);
       EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
       consuming_prefetch = true;
@@ -739,9 +753,9 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   if (!same) invalid("prefetch needs the geometry (offsets, batch size, pooling, bag offsets) of the last forward");
   use_device(device);
   if (bb[cur ^ 1].pending) drop_prefetch(st);
-  // the shared hash is clean once the current forward's k_gather ran
-  EC_CUDA(cudaEventRecord(ev_fwd, st));
-  EC_CUDA(cudaStreamWaitEvent(pstream, ev_fwd, 0));
+  // the other set (own hash, cleaned by its last gather) is free once the work
+  // recorded at its release has run; a never-used set has no release to wait for
+  EC_CUDA(cudaStreamWaitEvent(pstream, ev_release, 0));
   const int saved = cur;
   select(cur ^ 1);
   try {
@@ -768,8 +782,10 @@ void Engine::drop_prefetch(cudaStream_t st) {
   BatchBufs& nx = bb[cur ^ 1];
   if (!nx.pending) return;
   EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
-  k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev.p, T, nx.ctr.p, nx.utab.p, nx.uslot.p);
+  k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T, T, nx.ctr.p,
+                                                      nx.utab.p, nx.uslot.p);
   launched();
+  EC_CUDA(cudaEventRecord(ev_release, st));  // the set is free again
   nx.pending = false;
 }
 

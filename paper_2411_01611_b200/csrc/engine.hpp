@@ -164,7 +164,8 @@ struct Engine {
   void select(int i);
   DevBuf<Tile> tiles;
   DevBuf<int4> stiles;                // scatter tiles (table, bag lo, bag hi, -)
-  DevBuf<TableDev> tdev;
+  DevBuf<TableDev> tdev_buf;  // two copies of the table descriptors, one per batch-buffer set (own hash each)
+  View<TableDev> tdev;        // the selected set's copy
   std::vector<TableDev> td_host;
   int ntiles = 0, nstiles = 0, tail_lo = 0;
 
@@ -176,7 +177,7 @@ struct Engine {
   float* out_ptr = nullptr;
 
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
-  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_fwd = nullptr, ev_pf = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr;
   uint64_t geom_version = 0;
   bool consuming_prefetch = false;
   void prefetch(const ec_batch& b, cudaStream_t st);
@@ -204,6 +205,7 @@ struct Engine {
   uint64_t device_bytes() const;
   int host_grid() const;
   static bool host_tma();
+  void upload_tdev();
   int host_write_grid() const;
   int row_grid() const;
   void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
