@@ -657,7 +657,9 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       EC_CUDA(cudaStreamIsCapturing(st, &cs));  // replayed graphs are not FIFO with the prefetch's launches
       EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
-      k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+      // (the prefetched ids are found in the pending set's hash)
+      k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T,
+                                                                        T, ctr.p, missq.p, uniq.p, utab.p,
                                                                         urows.p, ugrad.p, lr, rank, world, nx.usrc.p,
                                                                         nx.urows.p);
       launched();
