@@ -301,8 +301,12 @@ def run_ours(args, wl):
                 stream.wait_event(copied[(k + 1) % 2])
                 tab.prefetch(dev_ids[(k + 1) % 2], offs, B, P)
             tab.backward(o, LR)
-            res = tab.stats(per_table=True)  # D2H of the step's result (per-table miss counts)
-        return res
+            # D2H of the step's result (per-table unique/miss counts) into a
+            # pinned ring slot; decoded one step later, like an async loss log
+            tab.stats_enqueue(k % 2)
+            if k > 0:
+                res = tab.stats_collect((k - 1) % 2, per_table=True)
+        return tab.stats_collect((nsteps - 1) % 2, per_table=True)
 
     e2e_steps(max(args.warmup, 8))  # untimed: captures the graphs of this buffer rotation
     barrier()
@@ -545,8 +549,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule-batches", type=int, default=32,
                     help="epoch length for the hot/normal scheduling measurement (0: skip)")
-    ap.add_argument("--prefetch", action="store_true",
-                    help="pipelined steps: ec_lookup_prefetch of the next batch overlaps this backward")
+    ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
+                    help="unpipelined steps (default: ec_lookup_prefetch of the next batch overlaps this step)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

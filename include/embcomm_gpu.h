@@ -363,6 +363,15 @@ typedef struct {
 /* Synchronises `stream`; per-table arrays (length num_tables) may be NULL. */
 int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* unique_per_table_host,
                     int64_t* miss_per_table_host);
+/* Asynchronous form for training loops: ec_lookup_stats_enqueue copies the
+ * last forward's counters into pinned ring slot `slot` (0..EC_STATS_SLOTS-1)
+ * on `stream` without synchronising; ec_lookup_stats_collect waits for that
+ * copy only and decodes it like ec_lookup_stats (reference counterpart: the
+ * per-batch unique/miss counts of embcomm simulate_epoch). */
+#define EC_STATS_SLOTS 4
+int ec_lookup_stats_enqueue(ec_tables t, void* stream, int slot);
+int ec_lookup_stats_collect(ec_tables t, int slot, ec_batch_stats* out, int64_t* unique_per_table_host,
+                            int64_t* miss_per_table_host);
 /* Parity exports of the last forward (synchronise): unique ids of table t in
  * first-occurrence order, inverse (positions into that list), per-unique hit
  * flag, and the gathered unique rows. */

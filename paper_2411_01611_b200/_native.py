@@ -161,6 +161,8 @@ _SIGS = {
     "ec_tables_schedule": [vp, vp, u64, vp, P(u64), vp],
     "ec_tables_gather_batch": [vp, vp, vp, u64, u32, vp, vp],
     "ec_lookup_stats": [vp, vp, P(BatchStats), vp, vp],
+    "ec_lookup_stats_enqueue": [vp, vp, i32],
+    "ec_lookup_stats_collect": [vp, i32, P(BatchStats), vp, vp],
     "ec_export_unique": [vp, u32, vp, u64, P(u64)],
     "ec_export_inverse": [vp, u32, vp],
     "ec_export_hit": [vp, u32, vp],

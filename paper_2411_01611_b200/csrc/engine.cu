@@ -245,6 +245,9 @@ Engine::~Engine() {
   if (side2) cudaStreamDestroy(side2);
   if (ev_side2) cudaEventDestroy(ev_side2);
   if (ctr_host) cudaFreeHost(ctr_host);
+  if (ring_host) cudaFreeHost(ring_host);
+  for (cudaEvent_t ev : ring_ev)
+    if (ev) cudaEventDestroy(ev);
   if (ev_release) cudaEventDestroy(ev_release);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
@@ -322,6 +325,9 @@ void Engine::create(const ec_tables_config& c) {
   for (BatchBufs& b : bb) b.tstat.alloc(T);
   select(0);
   EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctr_host), counters_size(T) * sizeof(int), cudaHostAllocDefault));
+  EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring_host), EC_STATS_SLOTS * counters_size(T) * sizeof(int),
+                        cudaHostAllocDefault));
+  for (cudaEvent_t& ev : ring_ev) EC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   tiles.alloc(max_tiles);
   tdev_buf.alloc(2 * T);
   td_host.resize(T);
@@ -1155,29 +1161,72 @@ int ec_lookup_bwd(ec_tables t, const float* grad, float lr, void* stream) {
   return guard([&] { E(t).backward(grad, lr, as_stream(stream)); });
 }
 
+static void decode_stats(Engine& e, int* h, uint64_t lookups, uint64_t wire_rows, uint64_t wire_bytes,
+                         ec_batch_stats* out, int64_t* u_per, int64_t* m_per) {
+  Counters c = counters(h, e.T);
+  ec_batch_stats s{};
+  s.lookups = lookups;
+  s.index_units = s.lookups;
+  for (uint32_t i = 0; i < e.T; ++i) {
+    const int Ui = c.ubase[i + 1] - c.ubase[i];
+    s.unique_rows += Ui;
+    s.miss_rows += c.M[i];
+    s.hot_tables += c.M[i] == 0;
+    if (u_per) u_per[i] = Ui;
+    if (m_per) m_per[i] = c.M[i];
+  }
+  s.hit_rows = s.unique_rows - s.miss_rows;
+  s.model_bytes = s.miss_rows * e.D * sizeof(float) + s.index_units * sizeof(uint32_t);
+  s.wire_rows = wire_rows;
+  s.wire_bytes = wire_bytes;
+  *out = s;
+}
+
+int ec_lookup_stats_enqueue(ec_tables t, void* stream, int slot) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (!e.have_fwd) invalid("no forward batch yet");
+    if (slot < 0 || slot >= EC_STATS_SLOTS) invalid("stats slot out of [0, EC_STATS_SLOTS)");
+    use_device(e.device);
+    const size_t n = counters_size(e.T);
+    cudaStream_t st = as_stream(stream);
+    // a slot is reused only after its previous copy landed
+    if (e.ring_full[slot]) EC_CUDA(cudaEventSynchronize(e.ring_ev[slot]));
+    EC_CUDA(cudaMemcpyAsync(e.ring_host + slot * n, e.ctr.p, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    EC_CUDA(cudaEventRecord(e.ring_ev[slot], st));
+    e.ring_lookups[slot] = static_cast<uint64_t>(e.geom_off[e.T]);
+    e.ring_wire_rows[slot] = e.last_wire_rows;
+    e.ring_wire_bytes[slot] = e.last_wire_bytes;
+    e.ring_full[slot] = true;
+  });
+}
+
+int ec_lookup_stats_collect(ec_tables t, int slot, ec_batch_stats* out, int64_t* u_per, int64_t* m_per) {
+  return guard([&] {
+    Engine& e = E(t);
+    if (slot < 0 || slot >= EC_STATS_SLOTS) invalid("stats slot out of [0, EC_STATS_SLOTS)");
+    if (!e.ring_full[slot]) invalid("stats slot was not enqueued");
+    use_device(e.device);
+    EC_CUDA(cudaEventSynchronize(e.ring_ev[slot]));
+    e.ring_full[slot] = false;
+    int* h = e.ring_host + slot * counters_size(e.T);
+    Counters c = counters(h, e.T);
+    if (*c.err) {
+      EC_CUDA(cudaMemset(counters(e.ctr.p, e.T).err, 0, sizeof(int)));
+      invalid("lookup id out of range of its table in the enqueued batch");
+    }
+    decode_stats(e, h, e.ring_lookups[slot], e.ring_wire_rows[slot], e.ring_wire_bytes[slot], out, u_per, m_per);
+  });
+}
+
 int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* u_per, int64_t* m_per) {
   return guard([&] {
     Engine& e = E(t);
     if (!e.have_fwd) invalid("no forward batch yet");
     std::vector<int> h;
     e.read_counters(as_stream(stream), h);
-    Counters c = counters(h.data(), e.T);
-    ec_batch_stats s{};
-    s.lookups = static_cast<uint64_t>(e.geom_off[e.T]);
-    s.index_units = s.lookups;
-    for (uint32_t i = 0; i < e.T; ++i) {
-      const int Ui = c.ubase[i + 1] - c.ubase[i];
-      s.unique_rows += Ui;
-      s.miss_rows += c.M[i];
-      s.hot_tables += c.M[i] == 0;
-      if (u_per) u_per[i] = Ui;
-      if (m_per) m_per[i] = c.M[i];
-    }
-    s.hit_rows = s.unique_rows - s.miss_rows;
-    s.model_bytes = s.miss_rows * e.D * sizeof(float) + s.index_units * sizeof(uint32_t);
-    s.wire_rows = e.last_wire_rows;
-    s.wire_bytes = e.last_wire_bytes;
-    *out = s;
+    decode_stats(e, h.data(), static_cast<uint64_t>(e.geom_off[e.T]), e.last_wire_rows, e.last_wire_bytes, out, u_per,
+                 m_per);
   });
 }
 

@@ -158,6 +158,11 @@ struct Engine {
   int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr, cnt, off, part;
   int* ctr_host = nullptr;  // pinned staging for ec_lookup_stats
+  // ec_lookup_stats_enqueue ring: pinned counter copies + their completion events
+  int* ring_host = nullptr;
+  cudaEvent_t ring_ev[EC_STATS_SLOTS] = {};
+  uint64_t ring_lookups[EC_STATS_SLOTS] = {}, ring_wire_rows[EC_STATS_SLOTS] = {}, ring_wire_bytes[EC_STATS_SLOTS] = {};
+  bool ring_full[EC_STATS_SLOTS] = {};
   View<uint2> list;
   int scatter_mode = 0;  // 0 auto, 1 float4 atomics, 2 transpose + segmented reduction
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry

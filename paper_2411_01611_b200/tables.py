@@ -198,6 +198,23 @@ class EmbeddingTables:
             d["miss_per_table"] = m
         return d
 
+    def stats_enqueue(self, slot: int) -> None:
+        """Queue a copy of the last forward's counters into pinned ring slot
+        `slot` on the current stream (no synchronisation)."""
+        check(N.lib().ec_lookup_stats_enqueue(self._h, _stream_ptr(self.torch, self.device), slot))
+
+    def stats_collect(self, slot: int, per_table: bool = False):
+        """Wait for slot `slot`'s copy and decode it like stats()."""
+        s = N.BatchStats()
+        u = np.zeros(self.T, np.int64)
+        m = np.zeros(self.T, np.int64)
+        check(N.lib().ec_lookup_stats_collect(self._h, slot, C.byref(s), u.ctypes.data, m.ctypes.data))
+        d = s.as_dict()
+        if per_table:
+            d["unique_per_table"] = u
+            d["miss_per_table"] = m
+        return d
+
     # ------------------------------------------------------ parity exports
     def export_unique(self, table: int) -> np.ndarray:
         n = C.c_uint64()

@@ -222,6 +222,32 @@ def test_config2_kaggle_shape_host_tier(ec, torch, ref):
     tab.close()
 
 
+def test_async_stats_ring_matches_sync_stats(ec, torch):
+    """ec_lookup_stats_enqueue/collect (pinned ring, no sync at enqueue)
+    decode each batch's counters exactly like the synchronous ec_lookup_stats,
+    also when collected after later batches ran; bad slots are errors."""
+    rows, D, B, P = [5000, 300, 7], 8, 256, 2
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.1)) for r in rows]
+    tab = ec.EmbeddingTables(rows, D, storage="host", max_lookups_per_table=B * P, max_batch_size=B)
+    tab.place_cache([d.top_ids(k) for d, k in zip(dists, [50, 20, 0])])
+    offs = np.arange(len(rows) + 1, dtype=np.int64) * B * P
+    want = []
+    for j in range(4):
+        ids = make_ids(ec, torch, dists, [B * P] * len(rows), 900 + j)[0]
+        tab.forward(ids, offs, B, P)
+        tab.stats_enqueue(j)
+        want.append(tab.stats(per_table=True))
+    for j in range(4):
+        got = tab.stats_collect(j, per_table=True)
+        for k, v in want[j].items():
+            assert np.array_equal(np.asarray(got[k]), np.asarray(v)), (j, k)
+    with pytest.raises(Exception):
+        tab.stats_collect(0)  # already collected
+    with pytest.raises(Exception):
+        tab.stats_enqueue(4)
+    tab.close()
+
+
 @pytest.mark.parametrize("storage,graphs", [("host", False), ("host", True), ("hbm", True)])
 def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
     """fwd(j) -> prefetch(j+1) -> bwd(j) gives the same outputs and final rows
