@@ -306,6 +306,7 @@ def run_ours(args, wl):
             tab.stats_enqueue(k % 2)
             if k > 0:
                 res = tab.stats_collect((k - 1) % 2, per_table=True)
+        tab.prefetch_wait()  # joins the last step's deferred host-tier write-back into `stream`
         return tab.stats_collect((nsteps - 1) % 2, per_table=True)
 
     e2e_steps(max(args.warmup, 8))  # untimed: captures the graphs of this buffer rotation

@@ -342,11 +342,16 @@ int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t*
  * results equal the unpipelined sequence.  Same geometry as the last forward
  * required. */
 int ec_lookup_prefetch(ec_tables t, const ec_batch* batch, void* stream);
-/* Make `stream` wait for a pending prefetch (no-op without one). */
+/* Make `stream` wait for a pending prefetch and for the deferred host-tier
+ * write-back of the last backward (no-op without either). */
 int ec_lookup_prefetch_wait(ec_tables t, void* stream);
 /* Backward of the last forward: grad_dev laid out like out_dev; applies
  * w <- w - lr * (sum of grads of every lookup of the row) to the cache copy
- * of cached rows and to the owning shard of the others (K6). */
+ * of cached rows and to the owning shard of the others (K6).  Single rank,
+ * pinned-host tier: the host write-back keeps running on an internal stream
+ * (overlapping the next forward); every later engine call that needs it
+ * orders itself after it, and ec_lookup_prefetch_wait joins it into a
+ * caller's stream (a device synchronise also covers it). */
 int ec_lookup_bwd(ec_tables t, const float* grad_dev, float lr, void* stream);
 
 typedef struct {

@@ -249,6 +249,8 @@ Engine::~Engine() {
   for (cudaEvent_t ev : ring_ev)
     if (ev) cudaEventDestroy(ev);
   if (ev_release) cudaEventDestroy(ev_release);
+  if (ev_grad) cudaEventDestroy(ev_grad);
+  if (ev_patch) cudaEventDestroy(ev_patch);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
@@ -349,6 +351,8 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_release, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
@@ -392,6 +396,7 @@ uint64_t Engine::device_bytes() const {
 
 void Engine::init_synthetic(uint64_t seed, float scale, cudaStream_t st) {
   use_device(device);
+  join_host_writes(st);
   for (uint32_t t = 0; t < T; ++t) {
     if (!local_rows[t]) continue;
     const uint64_t n = local_rows[t] * D;
@@ -418,6 +423,7 @@ void Engine::fill_cache(cudaStream_t st, bool from_store) {
 
 void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
   use_device(device);
+  EC_CUDA(cudaDeviceSynchronize());  // deferred host-tier write-backs land first
   // host-side validation + first-occurrence dedup of each table's list
   std::vector<uint32_t> all_ids;
   std::vector<uint16_t> all_tab;
@@ -635,42 +641,62 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
 // K6b for rows this rank applies itself: misses it owns (HBM, or pinned host
 // on the side stream) and — single rank only — cache hits.  With world > 1
 // the replicated hot rows are updated by the rank-ordered exchange instead.
+// Cold rows written back over the host link on side2 (full duplex with the
+// host reads of a prefetched batch), and the prefetched batch's copies of rows
+// updated here refreshed on the side stream (after its host gather, FIFO on
+// `side`).  Both start at ev_grad (gradients complete).  Never captured.
+template <int VEC>
+void Engine::enqueue_host_writeback(float lr) {
+  EC_CUDA(cudaStreamWaitEvent(side2, ev_grad, 0));
+  {
+    PhaseScope ph(prof, kPhaseApplyHost, side2);
+    if (host_tma())
+      k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+                                                                        urows.p, ugrad.p, lr, rank, world);
+    else
+      k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+                                                                       urows.p, ugrad.p, lr, rank, world);
+    launched();
+  }
+  EC_CUDA(cudaEventRecord(ev_side2, side2));
+  const BatchBufs& nx = bb[cur ^ 1];
+  if (nx.pending) {
+    EC_CUDA(cudaStreamWaitEvent(side, ev_grad, 0));
+    EC_CUDA(cudaStreamWaitEvent(side, ev_pf, 0));
+    // (the prefetched ids are found in the pending set's hash)
+    k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T,
+                                                                      T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                                      ugrad.p, lr, rank, world, nx.usrc.p, nx.urows.p);
+    launched();
+    EC_CUDA(cudaEventRecord(ev_patch, side));
+  }
+}
+
+// Work a caller's stream must see before reusing the current set or the host
+// tier: the deferred write-back and prefetch patch (single rank, host tier).
+void Engine::join_host_writes(cudaStream_t st) {
+  if (storage != EC_STORAGE_HOST) return;
+  EC_CUDA(cudaStreamWaitEvent(st, ev_side2, 0));
+  EC_CUDA(cudaStreamWaitEvent(st, ev_patch, 0));
+}
+
+// K6b for rows this rank applies itself: misses it owns (HBM, or pinned host
+// via enqueue_host_writeback) and — single rank only — cache hits.  With
+// world > 1 the replicated hot rows are updated by the rank-ordered exchange
+// instead, and the host write-back is joined before it.
 template <int VEC>
 void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
   if (host) {
-    EC_CUDA(cudaEventRecord(ev_part, st));  // gradients complete
-    // cold rows written back over the host link on their own stream
-    // (full duplex with the host reads of a prefetched batch)
-    EC_CUDA(cudaStreamWaitEvent(side2, ev_part, 0));
-    {
-      PhaseScope ph(prof, kPhaseApplyHost, side2);
-      const bool tma = host_tma();
-      if (tma)
-        k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                          urows.p, ugrad.p, lr, rank, world);
-      else
-        k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                         urows.p, ugrad.p, lr, rank, world);
-      launched();
-    }
-    EC_CUDA(cudaEventRecord(ev_side2, side2));
-    const BatchBufs& nx = bb[cur ^ 1];
-    if (nx.pending) {
-      // refresh the prefetched batch's copies of rows updated here; after its
-      // host gather (FIFO on the side stream) and after our gradients
-      EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      EC_CUDA(cudaStreamIsCapturing(st, &cs));  // replayed graphs are not FIFO with the prefetch's launches
-      EC_CUDA(cudaStreamWaitEvent(side, ev_pf, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
-      // (the prefetched ids are found in the pending set's hash)
-      k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T,
-                                                                        T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                        urows.p, ugrad.p, lr, rank, world, nx.usrc.p,
-                                                                        nx.urows.p);
-      launched();
-      EC_CUDA(cudaEventRecord(ev_side, side));
-    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    EC_CUDA(cudaStreamIsCapturing(st, &cs));
+    // inside a captured backward the record becomes an external event node,
+    // so the uncaptured write-back launched after the replay starts right here
+    if (cs == cudaStreamCaptureStatusActive)
+      EC_CUDA(cudaEventRecordWithFlags(ev_grad, st, cudaEventRecordExternal));
+    else
+      EC_CUDA(cudaEventRecord(ev_grad, st));
+    if (world > 1) enqueue_host_writeback<VEC>(lr);
   }
   {
     PhaseScope ph(prof, kPhaseApply, st);
@@ -678,10 +704,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
     launched();
   }
-  if (host) {
-    EC_CUDA(cudaStreamWaitEvent(st, ev_side2, 0));
-    if (bb[cur ^ 1].pending) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
-  }
+  if (host && world > 1) join_host_writes(st);
 }
 
 
@@ -718,6 +741,7 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
       EC_CUDA(cudaEventRecord(ev_release, st));
       select(cur ^ 1);
       EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
+      if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_patch, 0));
       consuming_prefetch = true;
       try {
         const GraphKey key{2, b.indices_dev, b.bag_offsets_dev, out, 0};
@@ -735,6 +759,7 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     }
     drop_prefetch(st);
   }
+  join_host_writes(st);  // this set's last write-back still reads its buffers
   if (world == 1) {
     const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
     run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
@@ -764,6 +789,7 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // the other set (own hash, cleaned by its last gather) is free once the work
   // recorded at its release has run; a never-used set has no release to wait for
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_release, 0));
+  join_host_writes(pstream);
   const int saved = cur;
   select(cur ^ 1);
   try {
@@ -790,6 +816,7 @@ void Engine::drop_prefetch(cudaStream_t st) {
   BatchBufs& nx = bb[cur ^ 1];
   if (!nx.pending) return;
   EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
+  join_host_writes(st);
   k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T, T, nx.ctr.p,
                                                       nx.utab.p, nx.uslot.p);
   launched();
@@ -921,6 +948,9 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
     std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
     const GraphKey key{bb[cur ^ 1].pending ? 3 : 1, grad, bag_off, out_ptr, lr_bits};
     run_maybe_graphed(key, st, [&] { scatter_and_apply_local(grad, lr, st); });
+    // host-tier write-back left running: it overlaps the next forward and is
+    // joined by whatever next reuses this set or the host tier
+    if (storage == EC_STORAGE_HOST) EC_DISPATCH_VEC(enqueue_host_writeback, lr);
   } else {
     scatter_and_apply_local(grad, lr, st);
     exchange_bwd(lr, st);  // remote misses -> owners, replicated hot rows in rank order
@@ -1154,6 +1184,7 @@ int ec_lookup_prefetch_wait(ec_tables t, void* stream) {
     Engine& e = E(t);
     use_device(e.device);
     if (e.bb[e.cur ^ 1].pending) EC_CUDA(cudaStreamWaitEvent(as_stream(stream), e.ev_pf, 0));
+    e.join_host_writes(as_stream(stream));
   });
 }
 

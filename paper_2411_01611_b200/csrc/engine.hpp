@@ -182,7 +182,8 @@ struct Engine {
   float* out_ptr = nullptr;
 
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
-  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr;
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr,
+              ev_grad = nullptr, ev_patch = nullptr;
   uint64_t geom_version = 0;
   bool consuming_prefetch = false;
   void prefetch(const ec_batch& b, cudaStream_t st);
@@ -225,6 +226,8 @@ struct Engine {
   template <int VEC> void fwd_pool(cudaStream_t st);
   template <int VEC> void bwd_scatter(const float* grad, cudaStream_t st);
   template <int VEC> void bwd_apply_local(float lr, cudaStream_t st);
+  template <int VEC> void enqueue_host_writeback(float lr);
+  void join_host_writes(cudaStream_t st);
   void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
   void forward_prologue(const ec_batch& b, float* out, cudaStream_t st);
   void gather_local(cudaStream_t st);

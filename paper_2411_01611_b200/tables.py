@@ -177,7 +177,8 @@ class EmbeddingTables:
         return out
 
     def prefetch_wait(self):
-        """Make the current stream wait for a pending prefetch."""
+        """Make the current stream wait for a pending prefetch and the last
+        backward's deferred host-tier write-back."""
         check(N.lib().ec_lookup_prefetch_wait(self._h, _stream_ptr(self.torch, self.device)))
 
     def backward(self, grad, lr: float):
