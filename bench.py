@@ -54,6 +54,7 @@ SEED = 20241101
 N_BATCHES = 4          # distinct batches cycled through the timed steps
 FLUSH_BYTES = 256 << 20  # > 126 MB L2, written between timed steps
 LR = 0.01
+MODES = {}  # kernel-variant overrides for experiments (--dedup-mode / --scatter-mode)
 
 
 def batch_seed(rank, j, t):
@@ -140,6 +141,10 @@ def build_tables(ec, torch, wl, rank, world, device):
     tab = ec.EmbeddingTables(rows, D, storage=wl["storage"], rank=rank, world=world,
                              max_lookups_per_table=B * P, max_batch_size=B, device=device)
     tab.init_synthetic(SEED, 0.05)
+    if MODES.get("dedup"):
+        tab.dedup_mode(MODES["dedup"])
+    if MODES.get("scatter"):
+        tab.scatter_mode(MODES["scatter"])
     if world > 1:
         import torch.distributed as dist
         uid = [ec.EmbeddingTables.comm_unique_id() if rank == 0 else None]
@@ -369,9 +374,11 @@ def run_ours(args, wl):
     import statistics as S
     pb = [phase_bytes(s, wl, T) for s in stats]
     mean_bytes = {k: S.mean(p[k] for p in pb) for k in pb[0]}
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    pfile = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(pfile)) if os.path.exists(pfile) else {}
+    peak = float(peaks.get("hbm_gbs") or 6650.0)
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy, burst) - of measured" if peaks.get("hbm_gbs") else
+                "B200_PROFILING.md fallback 6.65 TB/s (MEASURED_PEAKS.json absent) - of fallback")
     phases = {}
     for name, tot in prof["ms"].items():
         calls = prof["calls"][name]
@@ -426,7 +433,7 @@ def run_ours(args, wl):
                      "alg_bytes_per_launch": hbm_phases[dom]["alg_bytes"],
                      "traffic_source": (f"profiles/{args.workload}_traffic.json (ncu --set full, dram read+write "
                                         "bytes per launch)") if traffic else None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+                     "peak_source": peak_src},
         "step_alg_bytes": int(step_alg),
         "step_alg_gbs": round(step_alg / (ms * 1e-3) / 1e9, 1),
         "phases": phases,
@@ -552,7 +559,10 @@ def main():
                     help="epoch length for the hot/normal scheduling measurement (0: skip)")
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
                     help="unpipelined steps (default: ec_lookup_prefetch of the next batch overlaps this step)")
+    ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster"], default=None)
+    ap.add_argument("--scatter-mode", choices=["auto", "atomic", "transpose"], default=None)
     args = ap.parse_args()
+    MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode)
     if args.warmup < 3:
         args.warmup = 3
     wl = WORKLOADS[args.workload]

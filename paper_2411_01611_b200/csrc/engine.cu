@@ -281,13 +281,21 @@ void Engine::create(const ec_tables_config& c) {
   remap_off.assign(T + 1, 0);
   hash_off.assign(T + 1, 0);
   hash_lg.resize(T);
+  hash_direct.resize(T);
+  uint64_t direct_bytes = 0;
   for (uint32_t t = 0; t < T; ++t) {
     if (rows[t] < 1 || rows[t] > 0xFFFFFFFFull) invalid("table " + std::to_string(t) + " rows out of [1, 2^32-1]");
     local_rows[t] = rows[t] > static_cast<uint64_t>(rank) ? (rows[t] - rank + world - 1) / world : 0;
     store_off[t + 1] = store_off[t] + local_rows[t];
     remap_off[t + 1] = remap_off[t] + rows[t];
     hash_lg[t] = std::max<uint32_t>(5, log2_ceil(2 * std::min<uint64_t>(max_n, rows[t])));
-    hash_off[t + 1] = hash_off[t] + (1ull << hash_lg[t]);
+    // small tables: one slot per id (no hashing, no probing, one atomic per insert)
+    hash_direct[t] = rows[t] <= std::max<uint64_t>(1ull << hash_lg[t], kDirectRows) &&
+                             direct_bytes + rows[t] * 16 <= kDirectBudget
+                         ? 1
+                         : 0;
+    if (hash_direct[t]) direct_bytes += rows[t] * 16;  // both buffer sets
+    hash_off[t + 1] = hash_off[t] + (hash_direct[t] ? rows[t] : (1ull << hash_lg[t]));
   }
   const uint64_t store_elems = store_off[T] * D;
   if (storage == EC_STORAGE_HBM) {
@@ -338,6 +346,8 @@ void Engine::create(const ec_tables_config& c) {
     d.hash = hash.p + hash_off[t];
     d.shift = 32 - hash_lg[t];
     d.mask = static_cast<uint32_t>((1ull << hash_lg[t]) - 1);
+    d.direct = hash_direct[t];
+    d.pad_ = 0;
     d.remap = remap.p + remap_off[t];
     d.store = store_base + store_off[t] * D;
     d.rows = rows[t];
@@ -524,12 +534,14 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   int64_t nmax = 0;
   for (uint32_t t = 0; t < T; ++t) nmax = std::max<int64_t>(nmax, geom_off[t + 1] - geom_off[t]);
   max_n_batch = nmax;
-  // The cluster kernel wins when the tables alone fill the GPU and each
-  // thread's dependency chain is short (measured: Kaggle 26 tables x 16K
-  // lookups 43 vs 52 us; 8 tables x 82K lookups 104 vs 64 us).
-  cluster_fits = nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * kMaxItems;
-  cluster_ok = static_cast<int64_t>(T) * kClusterCtas >= sm_count(device) &&
+  // The cluster kernel wins when the tables alone fill the GPU (one cluster
+  // of 8 CTAs per table); larger per-table batches need more items per thread.
+  cluster_fits = nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * kClusterMaxItems;
+  for (uint32_t t = 0; t < T; ++t) cluster_fits = cluster_fits && td_host[t].direct;
+  cluster_ok = cluster_fits && static_cast<int64_t>(T) * kClusterCtas >= sm_count(device) &&
                nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * 8;
+  cluster_items = 1;
+  while (static_cast<int64_t>(kClusterCtas) * kClusterThreads * cluster_items < nmax) cluster_items *= 2;
   tail_lo = static_cast<int>(T);
   for (int t = static_cast<int>(T) - 1; t >= 0 && ft[t] == ntiles; --t) tail_lo = t;  // trailing empty tables
   for (uint32_t t = 0; t < static_cast<uint32_t>(tail_lo); ++t) {
@@ -902,15 +914,33 @@ void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
   pool(st);
 }
 
+template <int ITEMS>
+void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
+  constexpr size_t smem = cluster_smem_bytes(ITEMS);
+  static bool attr_set[64] = {};  // per device
+  if (!attr_set[device & 63]) {
+    EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    attr_set[device & 63] = true;
+  }
+  k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
+                                                                         ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
+                                                                         missq.p);
+}
+
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   if ((cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2)) {
     // one thread-block cluster per table: K1 + K2 in a single kernel
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
     PhaseScope ph(prof, kPhaseDedupCluster, st);
-    k_dedup_cluster<<<kClusterCtas * T, kClusterThreads, 0, st>>>(tdev.p, static_cast<int>(T), indices, slot_of.p,
-                                                                 tstat.p, ctr.p, uniq.p, uslot.p, utab.p, inv.p,
-                                                                 usrc.p, missq.p);
+    switch (cluster_items) {
+      case 1: launch_dedup_cluster<1>(indices, st); break;
+      case 2: launch_dedup_cluster<2>(indices, st); break;
+      case 4: launch_dedup_cluster<4>(indices, st); break;
+      case 8: launch_dedup_cluster<8>(indices, st); break;
+      default: launch_dedup_cluster<16>(indices, st); break;
+    }
     launched();
     return;
   }

@@ -19,6 +19,8 @@ struct TableDev {
   uint64_t rows;             // E_t
   int64_t base;              // first lookup of this table in the batch
   int64_t n;                 // lookups of this table in the batch
+  uint32_t direct;           // 1: `hash` is direct-mapped (slot = id, rows slots), no probing
+  uint32_t pad_;
 };
 
 struct Tile {
@@ -125,6 +127,11 @@ struct Engine {
   uint32_t max_b = 0;
   std::vector<uint64_t> rows, local_rows, store_off, remap_off, hash_off;
   std::vector<uint32_t> hash_lg;
+  std::vector<uint32_t> hash_direct;  // per table: direct-mapped dedup set
+  // direct-map a table's dedup set (8 B per row and buffer set) up to this many
+  // rows, within a total budget; the cluster dedup kernel needs it
+  static constexpr uint64_t kDirectRows = 1ull << 27;
+  static constexpr uint64_t kDirectBudget = 16ull << 30;
 
   DevBuf<float> store_dev;
   float* store_host = nullptr;  // pinned, mapped
@@ -155,6 +162,7 @@ struct Engine {
   View<unsigned long long> tstat;   // one per table (cluster dedup)
   bool cluster_fits = false;        // every table's batch fits one cluster
   bool cluster_ok = false;          // ... and the cluster path is the faster one
+  int cluster_items = 1;            // positions per thread of the cluster kernel
   int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
   View<int> ctr, cnt, off, part;
   int* ctr_host = nullptr;  // pinned staging for ec_lookup_stats
@@ -229,6 +237,8 @@ struct Engine {
   template <int VEC> void enqueue_host_writeback(float lr);
   void join_host_writes(cudaStream_t st);
   void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
+  template <int ITEMS>
+  void launch_dedup_cluster(const uint32_t* indices, cudaStream_t st);
   void forward_prologue(const ec_batch& b, float* out, cudaStream_t st);
   void gather_local(cudaStream_t st);
   void pool(cudaStream_t st);

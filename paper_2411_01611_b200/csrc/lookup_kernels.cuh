@@ -54,6 +54,24 @@ __device__ __forceinline__ uint32_t hash_insert_from(unsigned long long* tab, ui
   }
 }
 
+// Slot of `id` in a table's dedup set: the id itself when direct-mapped.
+__device__ __forceinline__ uint32_t table_slot(const TableDev& t, uint32_t id) {
+  return t.direct ? id : hash_slot(id, t.shift);
+}
+
+// Insert (id, first position lpos) into a table's dedup set; returns its slot.
+// Direct-mapped: one 64-bit atomicMin on the id's own slot (empty = ~0).
+__device__ __forceinline__ uint32_t set_insert(const TableDev& t, uint32_t id, uint32_t lpos) {
+  const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
+  if (t.direct) {
+    atomicMin(t.hash + id, mine);
+    return id;
+  }
+  const uint32_t h = hash_slot(id, t.shift);
+  const unsigned long long cur = atomicCAS(t.hash + h, kEmptySlot, mine);
+  return cur == kEmptySlot ? h : hash_insert_from(t.hash, t.mask, h, cur, id, lpos);
+}
+
 __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
                                                      const uint32_t* __restrict__ indices,
                                                      uint32_t* __restrict__ slot_of,
@@ -90,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     }
     // lanes holding the same id collapse to their lowest lane (= smallest position)
     peers[j] = __match_any_sync(kFull, id[j]);
-    h[j] = hash_slot(id[j], t.shift);
+    h[j] = table_slot(t, id[j]);
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j)  // home-slot probes of all items in flight together
@@ -101,8 +119,15 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     const int64_t p = tile.start + off;
     const int leader = __ffs(peers[j]) - 1;
     uint32_t slot = 0;
-    if (live[j] && leader == lane_id())
-      slot = hash_insert_from(t.hash, t.mask, h[j], cur[j], id[j], static_cast<uint32_t>(p - t.base));
+    if (live[j] && leader == lane_id()) {
+      if (t.direct) {
+        if (static_cast<uint32_t>(cur[j]) > static_cast<uint32_t>(p - t.base))
+          atomicMin(t.hash + h[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p - t.base));
+        slot = h[j];
+      } else {
+        slot = hash_insert_from(t.hash, t.mask, h[j], cur[j], id[j], static_cast<uint32_t>(p - t.base));
+      }
+    }
     slot = __shfl_sync(kFull, slot, leader);
     if (live[j]) slot_of[p] = slot;
     else if (off < tile.count) slot_of[p] = kInvalidSlot;  // out-of-range id: skipped downstream
@@ -615,7 +640,7 @@ __global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __r
       const uint32_t id = uniq[g];
       if (static_cast<int>(id % world) != rank) continue;
       const TableDev tb = td[utab[g]];
-      uint32_t h = hash_slot(id, tb.shift);
+      uint32_t h = table_slot(tb, id);
       for (;;) {
         const unsigned long long v = __ldcg(tb.hash + h);
         if (v == kEmptySlot) break;
@@ -648,36 +673,79 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
 // ===================================================================
 // K1 + K2 in one kernel: one thread-block cluster per table.
 //
-// The batch of a table is split into kClusterCtas contiguous chunks, one per
-// CTA; inside a CTA each thread owns kMaxItems-or-fewer consecutive positions
-// (thread-major), so the rank of a first occurrence is an exclusive scan of
-// per-thread counts plus a popcount inside the thread.  Phases are separated
-// by cluster barriers (release/acquire at cluster scope) instead of kernel
-// boundaries; the CTA totals are exchanged through distributed shared memory.
-// Tables take tickets in order and chain their unique bases with a short
-// look-back (one word per table), so the global unique index is in
-// (table, first occurrence) order exactly as the tile path produces it.
+// Needs every table's dedup set direct-mapped (slot = id; engine.cu sizes
+// those sets at creation).  The batch of a table is split into kClusterCtas
+// contiguous chunks, one per CTA; inside a CTA each thread owns up to ITEMS
+// consecutive positions (thread-major), so the rank of a first occurrence is
+// an exclusive scan of per-thread counts plus a popcount inside the thread.
+// Ids and per-item state stay in registers for the whole kernel.
+//
+//   L  hot ids (id < kClusterLocal: the top ranks of a parametric table, or
+//      all of a small table) are deduplicated per CTA in shared memory
+//      (direct-mapped atomicMin after a warp match-any collapse): the L2 set
+//      then sees one insert per (CTA, hot id) instead of thousands of
+//      same-address atomics.  Colder ids go straight to L2.
+//   G  representatives: one 64-bit atomicMin (id << 32 | position) on the
+//      id's slot keeps its first position                  -- cluster barrier
+//   F  each representative reads its id's first position p_f; firsts are the
+//      representatives with p_f == own position; CTA scan; per-thread words
+//      (exclusive count << 16 | first mask) to shared memory -- cluster barrier
+//   B  unique base: CTA totals over DSMEM; table totals by a warp-parallel
+//      look-back over the lower tables (clusters are dispatched in order)
+//   E  unique index of every representative: its own rank if first, else
+//      computed from p_f and the owning thread's word (DSMEM) -- no third
+//      barrier and no re-read of the L2 set; emit the firsts with the K2
+//      hit/miss partition (usrc, miss queue, per-table miss counts); tag the
+//      L2 slots (read later by k_patch_prefetch)
+//   I  inverse: representatives hold their index, hot duplicates read it from
+//      shared memory
 // ===================================================================
+#ifdef EC_TRACE  // phase timestamps for tools/dedup_bench.cu only
+__device__ unsigned long long* g_trace;
+#define EC_TRACE_AT(ph)                                                       \
+  do {                                                                       \
+    if (g_trace && threadIdx.x == 0) {                                       \
+      unsigned long long ns;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));                 \
+      g_trace[blockIdx.x * 8 + (ph)] = ns;                                   \
+    }                                                                        \
+  } while (0)
+#else
+#define EC_TRACE_AT(ph) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace ec {
 
 namespace cg = cooperative_groups;
 constexpr int kClusterCtas = 8;
 constexpr int kClusterThreads = 512;
-constexpr int kMaxItems = 32;  // per thread -> n_t <= 8 * 512 * 32 = 131072
+constexpr int kClusterMaxItems = 16;     // per thread -> n_t <= 8 * 512 * 16 = 65536
+constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared memory
+// per-table look-back word: count [0,32), CTA arrivals [32,40), inclusive flag
+constexpr unsigned long long kTabInc = 1ull << 40;
+__host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLocal * sizeof(uint32_t); }
 
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads)
+template <int ITEMS>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, ITEMS <= 4 ? 2 : 1)
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
-                    uint32_t* __restrict__ slot_of, unsigned long long* __restrict__ tstatus, int* __restrict__ ctr,
-                    uint32_t* __restrict__ uniq, uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab,
-                    uint32_t* __restrict__ inv, int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+                    unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
+                    uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
+                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+  static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
+  extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
+  __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
+  __shared__ int s_total, s_base, s_pref[kClusterCtas];
+  __shared__ int sw[kClusterThreads / 32];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
-  __shared__ int s_table, s_total, s_prefix, s_base;
-  __shared__ int sw[kClusterThreads / 32];
+  // clusters are dispatched in blockIdx order, so every lower table is running
+  // or done when this one looks back (the forward-progress rule of a
+  // decoupled-look-back scan over blockIdx)
+  const int t = static_cast<int>(blockIdx.x) / kClusterCtas;
+  EC_TRACE_AT(0);
   Counters c = counters(ctr, T);
-  if (crank == 0 && threadIdx.x == 0) s_table = atomicAdd(c.tile_counter, 1);  // ticket = table id
-  cluster.sync();
-  const int t = *cluster.map_shared_rank(&s_table, 0);
   const TableDev tb = td[t];
   const int64_t n = tb.n;
   const int64_t chunk = (n + kClusterCtas - 1) / kClusterCtas;
@@ -685,145 +753,183 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
   const int items = static_cast<int>((c1 - c0 + kClusterThreads - 1) / kClusterThreads);
   const int64_t p0 = c0 + static_cast<int64_t>(threadIdx.x) * items;  // this thread's first position
   const int my = static_cast<int>(max(int64_t{0}, min(static_cast<int64_t>(items), c1 - p0)));
+  const uint32_t nloc = tb.rows < kClusterLocal ? static_cast<uint32_t>(tb.rows) : kClusterLocal;
+  uint32_t id[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) id[j] = j < my ? __ldcs(indices + tb.base + p0 + j) : kEmptyKey;
+  {  // clear the hot-id slots (while the ids are in flight)
+    uint4* s4 = reinterpret_cast<uint4*>(sval);
+    const uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
+    for (uint32_t i = threadIdx.x; i < (nloc + 3) / 4; i += kClusterThreads) s4[i] = e;
+  }
+  __syncthreads();
+  EC_TRACE_AT(1);
 
-  // ---- P1: insert (packed atomicMin keeps each id's first position)
-  for (int j0 = 0; j0 < items; j0 += 4) {
-    uint32_t id[4], h[4];
-    unsigned long long cur[4];
-    bool live[4];
-    unsigned peers[4];
+  // ---- L: local representatives of hot ids
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = j0 + k;
-      live[k] = j < my;
-      id[k] = live[k] ? __ldcs(indices + tb.base + p0 + j) : kEmptyKey;
-      if (live[k] && id[k] >= tb.rows) {
-        atomicExch(c.err, 1);
-        live[k] = false;
-        id[k] = kEmptyKey;
-      }
+  for (int j = 0; j < ITEMS; ++j) {
+    if (j < my && id[j] >= tb.rows) {
+      atomicExch(c.err, 1);
+      id[j] = kEmptyKey;  // out of range: skipped, inverse = kInvalidSlot
     }
+    const uint32_t key = id[j] < nloc ? id[j] : kEmptyKey;
+    const unsigned peers = __match_any_sync(kFull, key);
+    // lowest lane of a group = its smallest position
+    if (key != kEmptyKey && __ffs(peers) - 1 == lane_id()) atomicMin(sval + key, static_cast<uint32_t>(p0 + j));
+  }
+  __syncthreads();
+  EC_TRACE_AT(2);
+
+  // ---- G: representatives insert into the direct-mapped L2 set
+  uint32_t rep = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      peers[k] = __match_any_sync(kFull, id[k]);
-      h[k] = hash_slot(id[k], tb.shift);
-      cur[k] = (live[k] && __ffs(peers[k]) - 1 == lane_id()) ? __ldcg(tb.hash + h[k]) : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = j0 + k;
-      const int leader = __ffs(peers[k]) - 1;
-      uint32_t slot = 0;
-      if (live[k] && leader == lane_id())
-        slot = hash_insert_from(tb.hash, tb.mask, h[k], cur[k], id[k], static_cast<uint32_t>(p0 + j));
-      slot = __shfl_sync(kFull, slot, leader);
-      if (j < my) slot_of[tb.base + p0 + j] = live[k] ? slot : kInvalidSlot;
+  for (int j = 0; j < ITEMS; ++j) {
+    const bool r = id[j] < nloc ? sval[id[j]] == static_cast<uint32_t>(p0 + j) : id[j] != kEmptyKey;
+    if (r) {
+      rep |= 1u << j;
+      atomicMin(tb.hash + id[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p0 + j));
     }
   }
+  EC_TRACE_AT(3);
   cluster.sync();  // every insert of this table is done
 
-  // ---- P2: first-occurrence flags, CTA scan, cluster prefix via DSMEM
-  uint32_t mask = 0;
-  for (int j0 = 0; j0 < items; j0 += 4) {
-    uint32_t hs[4];
+  // ---- F: first positions; firsts; CTA scan
+  uint32_t pf[ITEMS], first = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) hs[k] = (j0 + k) < my ? slot_of[tb.base + p0 + j0 + k] : kInvalidSlot;
+  for (int j = 0; j < ITEMS; ++j) pf[j] = ((rep >> j) & 1) ? static_cast<uint32_t>(__ldcg(tb.hash + id[j])) : 0u;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (hs[k] != kInvalidSlot &&
-          static_cast<uint32_t>(__ldcg(tb.hash + hs[k])) == static_cast<uint32_t>(p0 + j0 + k))
-        mask |= 1u << (j0 + k);
-  }
+  for (int j = 0; j < ITEMS; ++j)
+    if (((rep >> j) & 1) && pf[j] == static_cast<uint32_t>(p0 + j)) first |= 1u << j;
   int total;
-  const int ex = block_exclusive_scan<kClusterThreads>(__popc(mask), sw, &total);
-  if (threadIdx.x == 0) s_total = total;
-  cluster.sync();
+  const int ex = block_exclusive_scan<kClusterThreads>(__popc(first), sw, &total);
+  sxm[threadIdx.x] = (static_cast<uint32_t>(ex) << 16) | first;
   if (threadIdx.x == 0) {
-    int before = 0, all = 0;
-    for (unsigned r = 0; r < kClusterCtas; ++r) {
-      const int v = *cluster.map_shared_rank(&s_total, r);
-      if (r < crank) before += v;
-      all += v;
+    s_total = total;
+    // table aggregate: every CTA adds (1 << 32 | its count); complete at 8 arrivals
+    atomicAdd(tstatus + t, (1ull << 32) | static_cast<uint32_t>(total));
+  }
+  EC_TRACE_AT(4);
+  cluster.sync();
+
+  // remap of the firsts, in flight during the look-back
+  int32_t rm[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) rm[j] = ((first >> j) & 1) ? __ldg(tb.remap + id[j]) : 0;
+
+  // ---- B: unique base of the table and of every CTA of it
+  if (threadIdx.x < 32) {
+    // CTA totals over DSMEM, one lane each
+    const int v = lane_id() < kClusterCtas ? *cluster.map_shared_rank(&s_total, lane_id()) : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < kClusterCtas; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane_id() >= o) incl += y;
     }
-    s_prefix = before;
-    if (crank == 0) {
-      // table-level look-back: tickets are taken in order, so every lower
-      // table is running or done; its word becomes inclusive soon
-      int excl = 0;
-      if (t > 0) {
-        publish(tstatus + t, kStatAgg | static_cast<uint32_t>(all));
-        for (int k = t - 1; k >= 0; --k) {
-          unsigned long long v;
-          do {
-            v = *reinterpret_cast<volatile unsigned long long*>(tstatus + k);
-          } while ((v >> 32) == 0);
-          excl += static_cast<int>(static_cast<uint32_t>(v));
-          if ((v >> 32) == 2) break;
-        }
+    if (lane_id() < kClusterCtas) s_pref[lane_id()] = incl - v;
+    const int all = __shfl_sync(kFull, incl, kClusterCtas - 1);
+    // look-back over the lower tables, 32 at a time: a word is usable once all
+    // 8 CTAs of its table added their counts; an inclusive word ends the walk
+    int excl = 0;
+    for (int k0 = t - 1; k0 >= 0; k0 -= 32) {
+      const int k = k0 - lane_id();
+      unsigned long long w = kTabInc;  // before table 0: an inclusive zero
+      if (k >= 0) {
+        do {
+          w = *reinterpret_cast<volatile unsigned long long*>(tstatus + k);
+        } while (!(w & kTabInc) && ((w >> 32) & 0xFF) < kClusterCtas);
       }
-      publish(tstatus + t, kStatInc | static_cast<uint32_t>(excl + all));
-      c.ubase[t] = excl;
-      if (t == T - 1) c.ubase[T] = excl + all;
+      const unsigned inc = __ballot_sync(kFull, (w & kTabInc) != 0);
+      const int stop = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+      excl += __reduce_add_sync(kFull, lane_id() <= stop ? static_cast<int>(static_cast<uint32_t>(w)) : 0);
+      if (inc) break;
+    }
+    if (lane_id() == 0) {
+      if (crank == 0) {
+        publish(tstatus + t, kTabInc | (static_cast<unsigned long long>(kClusterCtas) << 32) |
+                                 static_cast<uint32_t>(excl + all));
+        c.ubase[t] = excl;
+        if (t == T - 1) c.ubase[T] = excl + all;
+      }
       s_base = excl;
     }
   }
-  cluster.sync();
-  const int base = *cluster.map_shared_rank(&s_base, 0) + s_prefix + ex;
+  __syncthreads();
+  EC_TRACE_AT(5);
 
-  // ---- P3: emit unique ids in first-occurrence order, tag their slots
+  // ---- E: unique index of every representative (pf[j] becomes it)
+  const int tbase = s_base;
+  const int base = tbase + s_pref[crank] + ex;
   {
-    uint32_t m = mask;
+    uint32_t xw[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {  // remote thread words, all in flight
+      xw[j] = 0;
+      if (((rep & ~first) >> j) & 1) {
+        const int64_t q = pf[j];
+        const int cf = static_cast<int>(q / chunk);
+        const int64_t q0 = static_cast<int64_t>(cf) * chunk, q1 = min(n, q0 + chunk);
+        const int itf = static_cast<int>((q1 - q0 + kClusterThreads - 1) / kClusterThreads);
+        const int thf = static_cast<int>((q - q0) / itf);
+        xw[j] = *cluster.map_shared_rank(sxm + thf, cf);
+        pf[j] = (static_cast<uint32_t>(cf) << 8) | static_cast<uint32_t>(q - q0 - static_cast<int64_t>(thf) * itf);
+      }
+    }
     int r = 0;
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      const int64_t p = tb.base + p0 + j;
-      const uint32_t g = static_cast<uint32_t>(base + r++);
-      const uint32_t id = indices[p];
-      const uint32_t h = slot_of[p];
-      uniq[g] = id;
-      uslot[g] = h;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      if ((first >> j) & 1) {
+        pf[j] = static_cast<uint32_t>(base + r++);
+      } else if ((rep >> j) & 1) {
+        const uint32_t cf = pf[j] >> 8, jf = pf[j] & 0xFF;
+        pf[j] = static_cast<uint32_t>(tbase + s_pref[cf]) + (xw[j] >> 16) + __popc(xw[j] & 0xFFFFu & ((1u << jf) - 1));
+      }
+      if (((rep >> j) & 1) && id[j] < nloc) sval[id[j]] = pf[j];  // for this CTA's hot duplicates
+    }
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // remote reads done
+  {
+    uint32_t missm = 0;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      if (!((first >> j) & 1)) continue;
+      const uint32_t g = pf[j];
+      uniq[g] = id[j];
+      uslot[g] = id[j];
       utab[g] = static_cast<uint16_t>(t);
-      tb.hash[h] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
+      usrc[g] = rm[j];  // cache row, or -1: a miss iff the id is not cached (core/src/simulator.cpp:99)
+      if (rm[j] < 0) missm |= 1u << j;
+      tb.hash[id[j]] = (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g;
     }
-  }
-  cluster.sync();  // all tags of this table visible
-
-  // ---- P4: inverse
-  for (int j0 = 0; j0 < my; j0 += 4) {
-    uint32_t hs[4];
+    // miss queue: one atomic per warp
+    const int nm = __popc(missm);
+    int incl = nm;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) hs[k] = (j0 + k) < my ? slot_of[tb.base + p0 + j0 + k] : kInvalidSlot;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (j0 + k < my)
-        inv[tb.base + p0 + j0 + k] = hs[k] == kInvalidSlot ? kInvalidSlot
-                                                           : static_cast<uint32_t>(__ldcg(tb.hash + hs[k])) & ~kRankTag;
-  }
-
-  // ---- P5: hit/miss partition of this table's uniques (K2)
-  const int ub = *cluster.map_shared_rank(&s_base, 0);
-  int U = 0;
-  for (unsigned r = 0; r < kClusterCtas; ++r) U += *cluster.map_shared_rank(&s_total, r);
-  for (int b0 = crank * kClusterThreads; b0 < U; b0 += kClusterCtas * kClusterThreads) {
-    const int g = ub + b0 + static_cast<int>(threadIdx.x);
-    const bool live = b0 + static_cast<int>(threadIdx.x) < U;
-    bool miss = false;
-    if (live) {
-      const int32_t s = __ldg(tb.remap + uniq[g]);
-      usrc[g] = s;
-      miss = s < 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane_id() >= o) incl += y;
     }
-    const unsigned mb = __ballot_sync(kFull, miss);
+    const int wtot = __shfl_sync(kFull, incl, 31);
     int qbase = 0;
-    if (mb && lane_id() == __ffs(mb) - 1) {
-      qbase = atomicAdd(c.miss_total, __popc(mb));
-      atomicAdd(c.M + t, __popc(mb));
+    if (lane_id() == 31 && wtot) {
+      qbase = atomicAdd(c.miss_total, wtot);
+      atomicAdd(c.M + t, wtot);
     }
-    qbase = __shfl_sync(kFull, qbase, __ffs(mb ? mb : 1u) - 1);
-    if (miss) missq[qbase + __popc(mb & ((1u << lane_id()) - 1))] = static_cast<uint32_t>(g);
+    qbase = __shfl_sync(kFull, qbase, 31) + incl - nm;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+      if ((missm >> j) & 1) missq[qbase++] = pf[j];
   }
-  cluster.sync();  // keep DSMEM of every CTA alive until all remote reads are done
+  __syncthreads();
+  EC_TRACE_AT(6);
+
+  // ---- I: inverse
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j)
+    if (j < my)
+      inv[tb.base + p0 + j] = id[j] == kEmptyKey ? kInvalidSlot : (((rep >> j) & 1) ? pf[j] : sval[id[j]]);
+  EC_TRACE_AT(7);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // keep this CTA's smem alive for remote readers
 }
 
 }  // namespace ec

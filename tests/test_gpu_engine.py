@@ -334,3 +334,32 @@ def test_skew_sweep_distributions(ec, torch, ref):
     out = tab.forward(ids, offs, B, P)
     check_batch(ec, tab, ids_h, offs, caches, rows, D, 11, 0.3, P=P, B=B, out=out, ref=ref)
     tab.close()
+
+
+@pytest.mark.parametrize("n_max", [700, 8192, 16384, 32768, 65536])
+def test_cluster_dedup_every_width(ec, torch, ref, n_max):
+    """The cluster kernel at every positions-per-thread width (1..16): tiny
+    tables (direct-mapped local set, thousands of repeats of 3 ids), mid-size
+    tables (local hash), a 10M-row table, ragged per-table counts and an empty
+    table; sets, inverse and hit/miss vs the oracle, counts vs the reference."""
+    rows = [3, 24, 5000, 13000, 142572, 10131227, 1000]
+    rng = np.random.default_rng(n_max)
+    n = [n_max, int(rng.integers(1, n_max)), n_max, 0, int(rng.integers(1, n_max)), n_max, 17]
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    caches = [d.top_ids(k) for d, k in zip(dists, [1, 0, 100, 5, 1000, 20000, 999])]
+    D, B = 8, 1
+    offs = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+    # CSR: one bag per table holding all of its lookups
+    bag = np.concatenate([[0], offs[1:]]).astype(np.int64)
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=n_max, max_batch_size=B)
+    tab.dedup_mode("cluster")
+    tab.init_synthetic(4, 0.5)
+    tab.place_cache(caches)
+    ids, _ = make_ids(ec, torch, dists, n, 900 + n_max)
+    bag_t = torch.from_numpy(bag).cuda()
+    for rep in range(2):  # the second batch sees a clean hash
+        out = tab.forward(ids, offs, B, bag_offsets=bag_t)
+        check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, rows, D, 4, 0.5, bag_offs=bag, B=B,
+                    ref=ref)  # (one bag of up to 64K rows: pooled sums are covered by the other tests)
+        tab.backward(torch.zeros(B, len(rows) * D, device="cuda"), 0.0)
+    tab.close()
