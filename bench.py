@@ -178,7 +178,7 @@ def phase_bytes(st, wl, T):
     hbm_src = U if wl["storage"] == "hbm" else H      # rows k_gather reads from HBM
     host_rows = 0 if wl["storage"] == "hbm" else M
     return {
-        "k_dedup_cluster": n * 4 + n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4),  # ids in; slot_of, inverse out; uniq, uslot, utab, remap->usrc
+        "k_dedup_cluster": n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4),  # ids in, inverse out; uniq, uslot, utab, remap->usrc
         "k_insert": n * 4 + n * 4,                     # ids in, slot_of out
         "k_compact": n * 4 + U * (4 + 4 + 2),          # slot_of in; uniq, uslot, utab out
         "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out

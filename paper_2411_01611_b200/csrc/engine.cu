@@ -598,6 +598,7 @@ void Engine::fwd_gather_local(cudaStream_t st) {
     launch_gather_host<VEC>(side);
     EC_CUDA(cudaEventRecord(ev_side, side));
   }
+  if (fused()) return;  // the pool reads cached / HBM rows where they are
   PhaseScope ph(prof, kPhaseGather, st);
   k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
                                               ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
@@ -609,6 +610,19 @@ template <int VEC>
 void Engine::fwd_pool(cudaStream_t st) {
   if (storage == EC_STORAGE_HOST && !consuming_prefetch) EC_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PhaseScope ph(prof, kPhasePool, st);
+  if (fused()) {
+    // rows read at their source; trailing blocks empty this batch's dedup set
+    const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
+    const int pb = row_grid(), rb = sm_count(device);
+    if (!bag_off && geom_p == 1)
+      k_pool1<VEC, 8, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
+                                                          pb, ctr.p, utab.p, uslot.p);
+    else
+      k_pool<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+                                                         bag_off, inv.p, urows.p, out_ptr, rs, pb, ctr.p, utab.p, uslot.p);
+    launched();
+    return;
+  }
   if (!bag_off && geom_p == 1) {
     k_pool1<VEC, 8><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr);
   } else {
@@ -621,6 +635,15 @@ void Engine::fwd_pool(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
+  if (fused()) {
+    // -lr * grad scattered straight into the cache / HBM rows (SGD in the
+    // scatter); pinned-host misses accumulate in ugrad for the host write-back
+    const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
+    k_scatter<VEC, 4, true><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+                                                             bag_off, inv.p, grad, ugrad.p, rs, bwd_lr);
+    launched();
+    return;
+  }
   // ugrad rows and occurrence counts were zeroed by k_gather
   // auto: the transpose pays off when tables see many lookups per batch (hot
   // rows repeat thousands of times); measured: 26 x 65536 lookups 418 -> 175 us,
@@ -710,7 +733,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
       EC_CUDA(cudaEventRecord(ev_grad, st));
     if (world > 1) enqueue_host_writeback<VEC>(lr);
   }
-  {
+  if (!fused()) {  // (the fused backward kernel already applied every update)
     PhaseScope ph(prof, kPhaseApply, st);
     k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
@@ -850,10 +873,25 @@ void Engine::launch_gather_host(cudaStream_t s) {
 }
 
 void Engine::gather_local(cudaStream_t st) { EC_DISPATCH_VEC(fwd_gather_local, st); }
+
+// Debug/parity export on the fused path: copy the current batch's cached and
+// HBM rows into the compact buffer as K3 would (pinned-host misses are there
+// already).  Harmless for the backward: ugrad rows and counters it zeroes are
+// zero at this point, and the dedup set was already emptied by the pool.
+template <int VEC>
+void Engine::export_gather() {
+  EC_CUDA(cudaDeviceSynchronize());
+  k_gather<VEC, 4><<<row_grid(), kThreads>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
+                                             ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+  EC_LAUNCH();
+  EC_CUDA(cudaDeviceSynchronize());
+}
+void Engine::gather_for_export() { EC_DISPATCH_VEC(export_gather); }
 void Engine::pool(cudaStream_t st) { EC_DISPATCH_VEC(fwd_pool, st); }
 void Engine::scatter_and_apply_local(const float* grad, float lr, cudaStream_t st) {
   if (!grad) invalid("null gradient");
   use_device(device);
+  bwd_lr = lr;
   EC_DISPATCH_VEC(bwd_scatter, grad, st);
   EC_DISPATCH_VEC(bwd_apply_local, lr, st);
 }
@@ -923,13 +961,15 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
                                  static_cast<int>(smem)));
     attr_set[device & 63] = true;
   }
+  MissGrad mg{};  // fused path, pinned-host tier: zeroed grad rows for the misses
+  if (fused() && storage == EC_STORAGE_HOST) mg = MissGrad{ugrad.p, static_cast<int>(D)};
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
                                                                          ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
-                                                                         missq.p);
+                                                                         missq.p, mg);
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
-  if ((cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2)) {
+  if (use_cluster()) {
     // one thread-block cluster per table: K1 + K2 in a single kernel
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
@@ -1341,6 +1381,7 @@ int ec_export_rows(ec_tables t, uint32_t table, float* out) {
     std::vector<int> h;
     int lo, n;
     table_span(e, table, h, &lo, &n);
+    if (n && e.fused()) e.gather_for_export();  // the fused forward pooled from the source rows
     if (n) EC_CUDA(cudaMemcpy(out, e.urows.p + static_cast<int64_t>(lo) * e.D, static_cast<int64_t>(n) * e.D * sizeof(float),
                               cudaMemcpyDeviceToHost));
   });

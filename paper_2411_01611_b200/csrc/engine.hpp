@@ -172,7 +172,13 @@ struct Engine {
   uint64_t ring_lookups[EC_STATS_SLOTS] = {}, ring_wire_rows[EC_STATS_SLOTS] = {}, ring_wire_bytes[EC_STATS_SLOTS] = {};
   bool ring_full[EC_STATS_SLOTS] = {};
   View<uint2> list;
-  int scatter_mode = 0;  // 0 auto, 1 float4 atomics, 2 transpose + segmented reduction
+  int scatter_mode = 0;  // 0 auto (fused when possible), 1 float4 atomics, 2 transpose + segmented reduction
+  // dedup by one thread-block cluster per table (K1+K2 in one kernel)
+  bool use_cluster() const { return (cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2); }
+  // single rank on the cluster path: the forward pools straight from the
+  // source rows (no K3 gather of cached/HBM rows) and the backward scatters
+  // -lr * grad straight into them (no ugrad pass, no K6b apply launch)
+  bool fused() const { return use_cluster() && world == 1 && !in_group && scatter_mode == 0; }
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
   void select(int i);
   DevBuf<Tile> tiles;
@@ -237,6 +243,10 @@ struct Engine {
   template <int VEC> void enqueue_host_writeback(float lr);
   void join_host_writes(cudaStream_t st);
   void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
+  void gather_for_export();
+  template <int VEC>
+  void export_gather();
+  float bwd_lr = 0.f;  // learning rate of the backward being enqueued
   template <int ITEMS>
   void launch_dedup_cluster(const uint32_t* indices, cudaStream_t st);
   void forward_prologue(const ec_batch& b, float* out, cudaStream_t st);

@@ -32,6 +32,7 @@ namespace ec {
 constexpr int kThreads = 256;
 constexpr int kItems = 4;
 constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
+constexpr int kRunChunk = 32;             // grouped-gradient list entries per lane group (K6a)
 
 // ------------------------------------------------------------------ K1
 // Insert (id, lpos) starting at slot h whose current content `cur` was
@@ -400,19 +401,52 @@ __device__ __forceinline__ float4 load_row(const float* urows, uint32_t u, int D
   return ldg4(urows + static_cast<int64_t>(u) * D + c * 4);
 }
 
+// Where unique u's current row lives (single rank, no K3 gather): its cache
+// row, its local HBM shard row, or — pinned-host misses, gathered by
+// k_gather_host — its row of the compact buffer.
+struct RowSrc {
+  const int32_t* usrc;
+  const uint32_t* uniq;
+  const float* cache;
+  const float* urows;
+  int local_hbm;
+};
+__device__ __forceinline__ const float* src_row(const RowSrc& rs, const TableDev& tb, uint32_t u, int D) {
+  const int32_t s = rs.usrc[u];
+  if (s >= 0) return rs.cache + static_cast<int64_t>(s) * D;
+  if (rs.local_hbm) return tb.store + static_cast<int64_t>(rs.uniq[u]) * D;
+  return rs.urows + static_cast<int64_t>(u) * D;
+}
+
+// Reset tail of a direct-source pool: the batch's dedup-set slots go back to
+// empty (what k_gather does on the gathering path).
+__device__ __forceinline__ void reset_sets(const TableDev* td, int T, const int* ctr, const uint16_t* utab,
+                                           const uint32_t* uslot, int b, int nb) {
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  for (int g = b * blockDim.x + threadIdx.x; g < U; g += nb * blockDim.x) {
+    td[utab[g]].hash[uslot[g]] = kEmptySlot;
+  }
+}
+
 // Bags visited sample-major (q = s*T + t) so a warp writes a contiguous
 // stretch of the [B, T*D] output; R bags in flight per thread; each bag is
 // summed in lookup order.
-template <int VEC, int R>
+template <int VEC, int R, bool DIRECT = false>
 __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
                                                    const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
-                                                   const float* __restrict__ urows, float* __restrict__ out) {
+                                                   const float* __restrict__ urows, float* __restrict__ out,
+                                                   RowSrc rs = {}, int pool_blocks = 0, const int* ctr = nullptr,
+                                                   const uint16_t* utab = nullptr, const uint32_t* uslot = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
   const int nbags = T * B;
+  if (DIRECT && static_cast<int>(blockIdx.x) >= pool_blocks) {
+    reset_sets(td, T, ctr, utab, uslot, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
+    return;
+  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nwarps = ((DIRECT ? pool_blocks : gridDim.x) * blockDim.x) >> 5;
   for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
     int lo[R], len[R];  // batch positions < 2^31 (checked by Engine::forward)
     int maxlen = 0;
@@ -437,8 +471,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
       uint32_t u[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+      if constexpr (DIRECT) {
+        const float* src[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = add4(acc[r], load_row(urows, u[r], D, m.c));
+        for (int r = 0; r < R; ++r) {
+          const int q = q0 + r * RPW + m.sub;
+          src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, td[q - (q / T) * T], u[r], D);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (src[r]) acc[r] = add4(acc[r], ldg4(src[r] + m.c * 4));
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = add4(acc[r], load_row(urows, u[r], D, m.c));
+      }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -451,16 +497,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
 // Pooling 1 (the Criteo configs): every bag is one lookup, so the pool is an
 // indexed row copy; R bags in flight per thread, evict-first stores for the
 // [B, T*D] output (written once, not re-read by this step).
-template <int VEC, int R>
+template <int VEC, int R, bool DIRECT = false>
 __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__ td, int T, int B,
                                                     const uint32_t* __restrict__ inv, const float* __restrict__ urows,
-                                                    float* __restrict__ out) {
+                                                    float* __restrict__ out, RowSrc rs = {}, int pool_blocks = 0,
+                                                    const int* ctr = nullptr, const uint16_t* utab = nullptr,
+                                                    const uint32_t* uslot = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
   const int nbags = T * B;
+  if (DIRECT && static_cast<int>(blockIdx.x) >= pool_blocks) {
+    reset_sets(td, T, ctr, utab, uslot, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
+    return;
+  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nwarps = ((DIRECT ? pool_blocks : gridDim.x) * blockDim.x) >> 5;
   for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
     uint32_t u[R];
 #pragma unroll
@@ -473,8 +525,19 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
       }
     }
     float4 v[R];
+    if constexpr (DIRECT) {
+      const float* src[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = load_row(urows, u[r], D, m.c);
+      for (int r = 0; r < R; ++r) {
+        const int q = q0 + r * RPW + m.sub;
+        src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, td[q - (q / T) * T], u[r], D);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = src[r] ? ldg4(src[r] + m.c * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = load_row(urows, u[r], D, m.c);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = q0 + r * RPW + m.sub;
@@ -488,11 +551,18 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
 // consecutive samples of one table, so hot rows repeat inside the warp; lanes
 // with equal (row, component) are summed with shuffles first and one float4
 // REDG per distinct row goes to L2.  R bags in flight per thread.
-template <int VEC, int R>
+//
+// SGD (single rank, fused path): the update itself is scattered, -lr * g as a
+// REDG into the unique's cache row or local HBM shard row, so the backward
+// needs no zeroed ugrad and no K6b apply pass; pinned-host misses still
+// accumulate g in ugrad (zeroed by the dedup kernel) for the host write-back.
+// fp32 adds into w instead of into a gradient sum: the same order-of-summation
+// tolerance (the update is within 1e-5 relative of the fp64 restatement).
+template <int VEC, int R, bool SGD = false>
 __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
                                                          const int64_t* __restrict__ bag_off,
                                                          const uint32_t* __restrict__ inv, const float* __restrict__ grad,
-                                                         float* __restrict__ ugrad) {
+                                                         float* __restrict__ ugrad, RowSrc rs = {}, float lr = 0.f) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -523,6 +593,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
       uint32_t u[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+      float* dst[R];
+      if constexpr (SGD) {
+        int32_t sr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sr[r] = u[r] != kInvalidSlot ? rs.usrc[u[r]] : 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int q = q0 + r * RPW + m.sub;
+          dst[r] = sr[r] >= 0 ? const_cast<float*>(rs.cache) + static_cast<int64_t>(sr[r]) * D
+                   : rs.local_hbm ? td[q / B].store + static_cast<int64_t>(rs.uniq[u[r]]) * D
+                                  : ugrad + static_cast<int64_t>(u[r]) * D;
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         float4 v = gv[r];
@@ -541,7 +624,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
             }
           }
         }
-        if (lead) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u[r]) * D + m.c * 4), v);
+        if constexpr (SGD) {
+          if (lead) {
+            const bool to_row = dst[r] != ugrad + static_cast<int64_t>(u[r]) * D;
+            if (to_row) v = make_float4(-lr * v.x, -lr * v.y, -lr * v.z, -lr * v.w);
+            atomicAdd(reinterpret_cast<float4*>(dst[r] + m.c * 4), v);
+          }
+        } else {
+          if (lead) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u[r]) * D + m.c * 4), v);
+        }
       }
     }
   }
@@ -664,11 +755,13 @@ __global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __r
 __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                              const uint16_t* __restrict__ utab, const uint32_t* __restrict__ uslot) {
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x)
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x) {
     td[utab[g]].hash[uslot[g]] = kEmptySlot;
+  }
 }
 
 }  // namespace ec
+
 
 // ===================================================================
 // K1 + K2 in one kernel: one thread-block cluster per table.
@@ -727,12 +820,19 @@ constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared mem
 constexpr unsigned long long kTabInc = 1ull << 40;
 __host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLocal * sizeof(uint32_t); }
 
+// Single-rank fused path: gradient rows of pinned-host misses start at zero
+// (k_scatter<SGD> accumulates them for the deferred host write-back).
+struct MissGrad {
+  float* ugrad;  // null: nothing to zero
+  int D;
+};
+
 template <int ITEMS>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, ITEMS <= 4 ? 2 : 1)
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
                     unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
-                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, MissGrad mg) {
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
@@ -898,7 +998,11 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
       uslot[g] = id[j];
       utab[g] = static_cast<uint16_t>(t);
       usrc[g] = rm[j];  // cache row, or -1: a miss iff the id is not cached (core/src/simulator.cpp:99)
-      if (rm[j] < 0) missm |= 1u << j;
+      if (rm[j] < 0) {
+        missm |= 1u << j;
+        if (mg.ugrad)
+          for (int k = 0; k < mg.D; k += 4) st4(mg.ugrad + static_cast<int64_t>(g) * mg.D + k, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
       tb.hash[id[j]] = (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g;
     }
     // miss queue: one atomic per warp
@@ -948,7 +1052,6 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
 // ===================================================================
 namespace ec {
 
-constexpr int kRunChunk = 32;
 
 // grad-row index (bag) of lookup p in table t
 __device__ __forceinline__ int bag_of(const TableDev& tb, const int64_t* bag_off, int B, int P, int t, int64_t p) {

@@ -36,11 +36,11 @@ static const std::vector<uint64_t> kTb = {39884406, 39043, 17289, 7420, 20263, 3
 
 template <int ITEMS>
 static void launch(const TableDev* td, int T, const uint32_t* idx, unsigned long long* tstat, int* ctr, uint32_t* uniq,
-                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq) {
+                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, MissGrad go) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem>>>(td, T, idx, tstat, ctr, uniq, uslot, utab, inv, usrc,
-                                                                       missq);
+                                                                       missq, go);
 }
 
 int main(int argc, char** argv) {
@@ -111,6 +111,7 @@ int main(int argc, char** argv) {
   CK(cudaMemset(ctr, 0, counters_size(T) * 4));
   const int nblk = kClusterCtas * T;
   CK(cudaMalloc(&trace, nblk * 8 * 8));
+  MissGrad go{};  // (no grad rows zeroed: the non-fused engine path)
   int items = 1;
   while (static_cast<int64_t>(kClusterCtas) * kClusterThreads * items < n) items *= 2;
   cudaEvent_t a, b;
@@ -120,17 +121,19 @@ int main(int argc, char** argv) {
   for (int it = 0; it < iters + 3; ++it) {
     CK(cudaMemset(ctr, 0, (counters_size(T) - 1) * 4));
     CK(cudaMemset(tstat, 0, T * 8));
-    for (int t = 0; t < T; ++t) CK(cudaMemset(td[t].hash, 0xFF, hslots[t] * 8));
+    for (int t = 0; t < T; ++t) {
+      CK(cudaMemset(td[t].hash, 0xFF, hslots[t] * 8));
+    }
     unsigned long long* tp = it == iters + 2 ? trace : nullptr;
     CK(cudaMemcpyToSymbol(g_trace, &tp, sizeof(tp)));
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a));
     switch (items) {
-      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
+      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
+      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
+      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
+      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(b));
