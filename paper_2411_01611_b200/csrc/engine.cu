@@ -864,11 +864,11 @@ void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
   const bool tma = host_tma();
   if (tma)
-    k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                             world);
+    k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                             ugrad.p, rank, world);
   else
-    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                            world);
+    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                            ugrad.p, rank, world);
   launched();
 }
 
@@ -961,11 +961,9 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
                                  static_cast<int>(smem)));
     attr_set[device & 63] = true;
   }
-  MissGrad mg{};  // fused path, pinned-host tier: zeroed grad rows for the misses
-  if (fused() && storage == EC_STORAGE_HOST) mg = MissGrad{ugrad.p, static_cast<int>(D)};
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
                                                                          ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
-                                                                         missq.p, mg);
+                                                                         missq.p);
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {

@@ -178,7 +178,8 @@ struct Engine {
   // single rank on the cluster path: the forward pools straight from the
   // source rows (no K3 gather of cached/HBM rows) and the backward scatters
   // -lr * grad straight into them (no ugrad pass, no K6b apply launch)
-  bool fused() const { return use_cluster() && world == 1 && !in_group && scatter_mode == 0; }
+  // (only where the atomic scatter is the right backward: <= 32K lookups per table)
+  bool fused() const { return use_cluster() && world == 1 && !in_group && scatter_mode == 0 && max_n_batch < 32768; }
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
   void select(int i);
   DevBuf<Tile> tiles;

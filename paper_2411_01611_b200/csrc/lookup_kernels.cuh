@@ -348,12 +348,14 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
 }
 
 // Misses served from pinned host memory (UVA-mapped shard), side stream.
+// Also zeroes the misses' gradient rows (the fused single-rank backward
+// accumulates them there for the host write-back).
 template <int VEC, int R>
 __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                                                           const uint32_t* __restrict__ missq,
                                                           const uint32_t* __restrict__ uniq,
                                                           const uint16_t* __restrict__ utab, float* __restrict__ urows,
-                                                          int rank, int world) {
+                                                          float* __restrict__ ugrad, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __rest
       if (q < nm) {
         const uint32_t g = missq[q];
         const uint32_t id = uniq[g];
+        st4(ugrad + static_cast<int64_t>(g) * D + m.c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
         if (static_cast<int>(id % world) == rank) {
           const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
           v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
@@ -820,19 +823,13 @@ constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared mem
 constexpr unsigned long long kTabInc = 1ull << 40;
 __host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLocal * sizeof(uint32_t); }
 
-// Single-rank fused path: gradient rows of pinned-host misses start at zero
-// (k_scatter<SGD> accumulates them for the deferred host write-back).
-struct MissGrad {
-  float* ugrad;  // null: nothing to zero
-  int D;
-};
 
 template <int ITEMS>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, ITEMS <= 4 ? 2 : 1)
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
                     unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
-                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, MissGrad mg) {
+                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
@@ -998,11 +995,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
       uslot[g] = id[j];
       utab[g] = static_cast<uint16_t>(t);
       usrc[g] = rm[j];  // cache row, or -1: a miss iff the id is not cached (core/src/simulator.cpp:99)
-      if (rm[j] < 0) {
-        missm |= 1u << j;
-        if (mg.ugrad)
-          for (int k = 0; k < mg.D; k += 4) st4(mg.ugrad + static_cast<int64_t>(g) * mg.D + k, make_float4(0.f, 0.f, 0.f, 0.f));
-      }
+      if (rm[j] < 0) missm |= 1u << j;
       tb.hash[id[j]] = (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g;
     }
     // miss queue: one atomic per warp
@@ -1272,7 +1265,8 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
                                                               const uint32_t* __restrict__ missq,
                                                               const uint32_t* __restrict__ uniq,
                                                               const uint16_t* __restrict__ utab,
-                                                              float* __restrict__ urows, int rank, int world) {
+                                                              float* __restrict__ urows, float* __restrict__ ugrad,
+                                                              int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
   constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
@@ -1320,8 +1314,10 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
     for (int i = threadIdx.x; i < cnt * VEC; i += blockDim.x) {
       const int r = i / VEC, c = i - r * VEC;
       const uint32_t g = dst_g[r];
-      if (g != 0xFFFFFFFFu)
+      if (g != 0xFFFFFFFFu) {
         st4(urows + static_cast<int64_t>(g) * D + c * 4, *reinterpret_cast<const float4*>(buf + r * D + c * 4));
+        st4(ugrad + static_cast<int64_t>(g) * D + c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
     }
     __syncthreads();
   }

@@ -36,11 +36,11 @@ static const std::vector<uint64_t> kTb = {39884406, 39043, 17289, 7420, 20263, 3
 
 template <int ITEMS>
 static void launch(const TableDev* td, int T, const uint32_t* idx, unsigned long long* tstat, int* ctr, uint32_t* uniq,
-                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, MissGrad go) {
+                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem>>>(td, T, idx, tstat, ctr, uniq, uslot, utab, inv, usrc,
-                                                                       missq, go);
+                                                                       missq);
 }
 
 int main(int argc, char** argv) {
@@ -111,7 +111,6 @@ int main(int argc, char** argv) {
   CK(cudaMemset(ctr, 0, counters_size(T) * 4));
   const int nblk = kClusterCtas * T;
   CK(cudaMalloc(&trace, nblk * 8 * 8));
-  MissGrad go{};  // (no grad rows zeroed: the non-fused engine path)
   int items = 1;
   while (static_cast<int64_t>(kClusterCtas) * kClusterThreads * items < n) items *= 2;
   cudaEvent_t a, b;
@@ -129,11 +128,11 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a));
     switch (items) {
-      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
-      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
-      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
-      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
-      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, go); break;
+      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(b));
@@ -147,6 +146,26 @@ int main(int argc, char** argv) {
   std::printf("%s: T=%d n=%lld items=%d smem=%zu  kernel %.2f us  U=%d (host %llu) misses=%d err=%d\n", tb ? "tb" : "kaggle", T,
               (long long)n, items, cluster_smem_bytes(items), 1e3 * tot / iters, hc[2 * T], (unsigned long long)expect_u,
               hc[2 * T + 1], hc[2 * T + 3]);
+  {  // validate the last launch: uniq[inv[p]] == ids[p], usrc[g] == remap[uniq[g]]
+    const int U = hc[2 * T];
+    std::vector<uint32_t> hinv(N), huniq(U);
+    std::vector<int32_t> husrc(U);
+    std::vector<uint16_t> hutab(U);
+    CK(cudaMemcpy(hinv.data(), inv, N * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(huniq.data(), uniq, U * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(husrc.data(), usrc, U * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hutab.data(), utab, U * 2, cudaMemcpyDeviceToHost));
+    long bad_inv = 0, bad_src = 0, miss = 0;
+    for (size_t p = 0; p < N; ++p)
+      if (hinv[p] >= static_cast<uint32_t>(U) || huniq[hinv[p]] != ids[p]) ++bad_inv;
+    for (int g = 0; g < U; ++g) {
+      const uint64_t k = std::min<uint64_t>(rows[hutab[g]], cache_rows / T);
+      const int32_t want = huniq[g] < k ? static_cast<int32_t>(huniq[g]) : -1;
+      if (husrc[g] != want) ++bad_src;
+      miss += want < 0;
+    }
+    std::printf("validate: bad inverse %ld, bad usrc %ld, expected misses %ld\n", bad_inv, bad_src, miss);
+  }
   std::vector<unsigned long long> tr(nblk * 8);
   CK(cudaMemcpy(tr.data(), trace, tr.size() * 8, cudaMemcpyDeviceToHost));
   unsigned long long t0 = ~0ull;
