@@ -15,6 +15,7 @@ against row-sharded tables (weak scaling).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -53,6 +54,7 @@ WORKLOADS = {
 SEED = 20241101
 N_BATCHES = 4          # distinct batches cycled through the timed steps
 FLUSH_BYTES = 256 << 20  # > 126 MB L2, written between timed steps
+HEAD_START_CYCLES = 2_000_000  # ~1 ms device sleep before a timed loop (see run_ours)
 LR = 0.01
 MODES = {}  # kernel-variant overrides for experiments (--dedup-mode / --scatter-mode)
 
@@ -199,8 +201,10 @@ def run_ours(args, wl):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    # a non-default stream, so the engine can capture and replay CUDA graphs
-    torch.cuda.set_stream(torch.cuda.Stream())
+    # a non-default stream, so the engine can capture and replay CUDA graphs;
+    # high priority, so the step's critical kernels (pool, scatter) win SM slots
+    # over the prefetch / host-tier kernels on the engine's low-priority streams
+    torch.cuda.set_stream(torch.cuda.Stream(priority=args.stream_priority))
     T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
     t0 = time.time()
     tab, dists, caches, ks = build_tables(ec, torch, wl, rank, world, local)
@@ -209,6 +213,9 @@ def run_ours(args, wl):
     out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
+    # input stream: produces the step's ids (the e2e loop's host->device copies);
+    # a prefetch is ordered after it, not after the compute stream's forward
+    copy_stream = torch.cuda.Stream()
 
     def step(j):
         # pipelined training step: forward of batch j (its dedup, hit/miss and
@@ -217,7 +224,7 @@ def run_ours(args, wl):
         # holds all of its work
         o = tab.forward(ids[j], offs, B, P, out=out)
         if args.prefetch:
-            tab.prefetch(ids[(j + 1) % N_BATCHES], offs, B, P)
+            tab.prefetch(ids[(j + 1) % N_BATCHES], offs, B, P, stream=copy_stream)
         tab.backward(o, LR)  # loss = 0.5*||pooled||^2  ->  d loss / d pooled = pooled
         if args.prefetch:
             tab.prefetch_wait()
@@ -249,15 +256,23 @@ def run_ours(args, wl):
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
+        # a short device-side sleep before the first timed event lets the host
+        # queue a few steps ahead, so step 0 is not timed against the host's
+        # enqueue latency after the synchronize (outside the timed region)
+        torch.cuda._sleep(HEAD_START_CYCLES)
+        gc.disable()
         for k in range(args.steps):
             flush.fill_(float(k))
             starts[k].record(stream)
-            step(k % N_BATCHES)
+            step((w + k) % N_BATCHES)  # continues the warm-up's rotation: its last prefetch is this batch
             ends[k].record(stream)
         torch.cuda.synchronize()
+        gc.enable()
         barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms = sum(step_ms) / args.steps
+    step_dist = {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),
+                 "max": round(max(step_ms), 5), "argmax": int(np.argmax(step_ms))}
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -270,7 +285,7 @@ def run_ours(args, wl):
     tab.profile_read(reset=True)
     for k in range(args.steps):
         flush.fill_(float(k))
-        step(k % N_BATCHES)
+        step((w + args.steps + k) % N_BATCHES)
     torch.cuda.synchronize()
     prof = tab.profile_read(reset=True)
     tab.profile(False)
@@ -278,49 +293,60 @@ def run_ours(args, wl):
 
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
-    dev_ids = [torch.empty_like(ids[0]), torch.empty_like(ids[0])]
+    NS = 3  # device id slots: step k+2's copy runs during step k
+    dev_ids = [torch.empty_like(ids[0]) for _ in range(NS)]
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
     e2e_end = torch.cuda.Event(enable_timing=True)
-    copy_stream = torch.cuda.Stream()
-    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    copied = [torch.cuda.Event() for _ in range(NS)]
+    consumed = [torch.cuda.Event() for _ in range(NS)]
 
     def h2d(k):  # step k's ids, pinned host -> device, on the copy stream
         with torch.cuda.stream(copy_stream):
-            dev_ids[k % 2].copy_(host_ids[k % N_BATCHES], non_blocking=True)
-            copied[k % 2].record(copy_stream)
+            if k >= NS:  # the slot's previous batch (k-3) was consumed by its forward
+                copy_stream.wait_event(consumed[k % NS])
+            dev_ids[k % NS].copy_(host_ids[k % N_BATCHES], non_blocking=True)
+            copied[k % NS].record(copy_stream)
 
     def e2e_steps(nsteps):
-        # input pipelining: step k+1's H2D overlaps step k's compute; every
-        # step still moves its own ids host->device and reads its result back
+        # input pipelining: step k+2's H2D runs during step k, so a step's
+        # prefetch never waits on the link; every step still moves its own ids
+        # host->device and reads its result back
         h2d(0)
+        if nsteps > 1:
+            h2d(1)
         res = None
         for k in range(nsteps):
-            stream.wait_event(copied[k % 2])
-            if k + 1 < nsteps:
-                h2d(k + 1)  # dev_ids[(k+1)%2] is free: step k-1 finished (its stats synchronised)
+            stream.wait_event(copied[k % NS])
             if args.prefetch and k == 0:
-                tab.prefetch(dev_ids[0], offs, B, P)
-            o = tab.forward(dev_ids[k % 2], offs, B, P, out=out)
+                tab.prefetch(dev_ids[0], offs, B, P, stream=copy_stream)
+            o = tab.forward(dev_ids[k % NS], offs, B, P, out=out)
+            consumed[k % NS].record(stream)
             if args.prefetch and k + 1 < nsteps:
-                stream.wait_event(copied[(k + 1) % 2])
-                tab.prefetch(dev_ids[(k + 1) % 2], offs, B, P)
+                tab.prefetch(dev_ids[(k + 1) % NS], offs, B, P, stream=copy_stream)  # after its H2D copy
+            if k + 2 < nsteps:
+                h2d(k + 2)  # (after the prefetch above, which orders itself after the copy stream)
             tab.backward(o, LR)
             # D2H of the step's result (per-table unique/miss counts) into a
-            # pinned ring slot; decoded one step later, like an async loss log
-            tab.stats_enqueue(k % 2)
-            if k > 0:
-                res = tab.stats_collect((k - 1) % 2, per_table=True)
+            # pinned ring slot; decoded two steps later, like an async loss log
+            tab.stats_enqueue(k % 4)
+            if k >= 2:
+                res = tab.stats_collect((k - 2) % 4, per_table=True)
         tab.prefetch_wait()  # joins the last step's deferred host-tier write-back into `stream`
-        return tab.stats_collect((nsteps - 1) % 2, per_table=True)
+        for k in range(max(0, nsteps - 2), nsteps):
+            res = tab.stats_collect(k % 4, per_table=True)
+        return res
 
     e2e_steps(max(args.warmup, 8))  # untimed: captures the graphs of this buffer rotation
     barrier()
     torch.cuda.synchronize()
+    torch.cuda._sleep(HEAD_START_CYCLES)
+    gc.disable()  # no collector pauses inside the timed host loop
     e2e_start.record(stream)
     counters = e2e_steps(args.steps)
     e2e_end.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     barrier()
     e2e_ms = e2e_start.elapsed_time(e2e_end) / args.steps
     if world > 1:
@@ -410,6 +436,7 @@ def run_ours(args, wl):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms, 5),
+        "step_ms_dist": step_dist,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -559,9 +586,13 @@ def main():
                     help="epoch length for the hot/normal scheduling measurement (0: skip)")
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
                     help="unpipelined steps (default: ec_lookup_prefetch of the next batch overlaps this step)")
+    ap.add_argument("--stream-priority", type=int, default=-1,
+                    help="priority of the caller's stream (torch: -1 high, 0 low; engine side streams are low)")
     ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster"], default=None)
     ap.add_argument("--scatter-mode", choices=["auto", "atomic", "transpose"], default=None)
     args = ap.parse_args()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        args.prefetch = False  # ec_lookup_prefetch is single-rank (the exchange synchronises ranks per batch)
     MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode)
     if args.warmup < 3:
         args.warmup = 3

@@ -263,6 +263,10 @@ int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
  * entries) and the number of kernels the engine launched; reset != 0 clears
  * them. */
 int ec_tables_profile(ec_tables t, int enable);
+/* Timeline of the profiled kernels since the last call: `count` records of
+ * (slot, start ms, end ms), times relative to the first recorded launch, on
+ * their own streams (up to `cap` written to out[3*i..3*i+2]). */
+int ec_tables_profile_timeline(ec_tables t, double* out, uint64_t cap, uint64_t* count);
 /* CUDA-graph replay of the per-batch kernel sequence (default on): the first
  * ec_lookup_fwd/bwd with a given (indices, bag offsets, out) / (grad, lr) on a
  * capturable stream is captured, later ones replay it.  Off, or on the legacy
@@ -339,8 +343,11 @@ int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t*
  * streams into a second buffer set, overlapping the current backward; the
  * next ec_lookup_fwd with the same indices_dev consumes them.  Host-tier rows
  * the current backward updates are refreshed in the prefetched copy, so
- * results equal the unpipelined sequence.  Same geometry as the last forward
- * required. */
+ * results equal the unpipelined sequence.  Stream-ordered on `stream`: it
+ * starts after the work already enqueued there, so pass the stream that
+ * produces indices_dev (e.g. an input-copy stream; passing the compute stream
+ * instead serialises the prefetch behind the current forward).  Same
+ * geometry as the last forward required. */
 int ec_lookup_prefetch(ec_tables t, const ec_batch* batch, void* stream);
 /* Make `stream` wait for a pending prefetch and for the deferred host-tier
  * write-back of the last backward (no-op without either). */

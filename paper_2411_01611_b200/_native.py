@@ -150,6 +150,7 @@ _SIGS = {
     "ec_tables_dedup_mode": [vp, C.c_int],
     "ec_tables_scatter_mode": [vp, C.c_int],
     "ec_tables_profile_read": [vp, vp, vp, P(u64), C.c_int],
+    "ec_tables_profile_timeline": [vp, vp, u64, P(u64)],
     "ec_tables_init_synthetic": [vp, u64, f32, vp],
     "ec_tables_place_cache": [vp, vp, vp],
     "ec_tables_read_rows": [vp, u32, vp, u64, vp],

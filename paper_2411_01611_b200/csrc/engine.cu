@@ -251,6 +251,7 @@ Engine::~Engine() {
   if (ev_release) cudaEventDestroy(ev_release);
   if (ev_grad) cudaEventDestroy(ev_grad);
   if (ev_patch) cudaEventDestroy(ev_patch);
+  if (ev_pfcall) cudaEventDestroy(ev_pfcall);
   if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
@@ -364,6 +365,7 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_pfcall, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
@@ -613,13 +615,14 @@ void Engine::fwd_pool(cudaStream_t st) {
   if (fused()) {
     // rows read at their source; trailing blocks empty this batch's dedup set
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
+    const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p};
     const int pb = row_grid(), rb = sm_count(device);
     if (!bag_off && geom_p == 1)
       k_pool1<VEC, 8, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
-                                                          pb, ctr.p, utab.p, uslot.p);
+                                                          pb, ro);
     else
       k_pool<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
-                                                         bag_off, inv.p, urows.p, out_ptr, rs, pb, ctr.p, utab.p, uslot.p);
+                                                         bag_off, inv.p, urows.p, out_ptr, rs, pb, ro);
     launched();
     return;
   }
@@ -683,6 +686,23 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
 template <int VEC>
 void Engine::enqueue_host_writeback(float lr) {
   EC_CUDA(cudaStreamWaitEvent(side2, ev_grad, 0));
+  const BatchBufs& nx = bb[cur ^ 1];
+  const bool patch = nx.pending;
+  const TableDev* nxt_td = tdev_buf.p + static_cast<size_t>(cur ^ 1) * T;
+  if (patch && host_tma()) {
+    // one kernel writes the rows back and refreshes the prefetched batch's
+    // copies: it starts once that batch's host gather is done (host reads and
+    // writes share the link's request rate, so the wait costs no link time)
+    EC_CUDA(cudaStreamWaitEvent(side2, ev_pf, 0));
+    PhaseScope ph(prof, kPhaseApplyHost, side2);
+    k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+                                                                      ugrad.p, lr, rank, world, nxt_td, nx.usrc.p,
+                                                                      nx.urows.p);
+    launched();
+    EC_CUDA(cudaEventRecord(ev_side2, side2));
+    EC_CUDA(cudaEventRecord(ev_patch, side2));
+    return;
+  }
   {
     PhaseScope ph(prof, kPhaseApplyHost, side2);
     if (host_tma())
@@ -694,13 +714,11 @@ void Engine::enqueue_host_writeback(float lr) {
     launched();
   }
   EC_CUDA(cudaEventRecord(ev_side2, side2));
-  const BatchBufs& nx = bb[cur ^ 1];
-  if (nx.pending) {
+  if (patch) {
     EC_CUDA(cudaStreamWaitEvent(side, ev_grad, 0));
     EC_CUDA(cudaStreamWaitEvent(side, ev_pf, 0));
     // (the prefetched ids are found in the pending set's hash)
-    k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T,
-                                                                      T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
+    k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(nxt_td, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
                                                                       ugrad.p, lr, rank, world, nx.usrc.p, nx.urows.p);
     launched();
     EC_CUDA(cudaEventRecord(ev_patch, side));
@@ -733,7 +751,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
       EC_CUDA(cudaEventRecord(ev_grad, st));
     if (world > 1) enqueue_host_writeback<VEC>(lr);
   }
-  if (!fused()) {  // (the fused backward kernel already applied every update)
+  if (!fused()) {  // (the SGD scatter already updated every row)
     PhaseScope ph(prof, kPhaseApply, st);
     k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
@@ -825,18 +843,21 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // recorded at its release has run; a never-used set has no release to wait for
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_release, 0));
   join_host_writes(pstream);
+  // stream-ordered like every call: work the caller enqueued on `st` before
+  // this prefetch (e.g. the copy that produced these indices) comes first
+  EC_CUDA(cudaEventRecord(ev_pfcall, st));
+  EC_CUDA(cudaStreamWaitEvent(pstream, ev_pfcall, 0));
   const int saved = cur;
   select(cur ^ 1);
   try {
-    enqueue_dedup_partition(b.indices_dev, pstream);
-    if (storage == EC_STORAGE_HOST) {
-      EC_CUDA(cudaEventRecord(ev_part, pstream));
-      EC_CUDA(cudaStreamWaitEvent(side, ev_part, 0));
-      EC_DISPATCH_VEC(launch_gather_host, side);
-      EC_CUDA(cudaEventRecord(ev_pf, side));
-    } else {
-      EC_CUDA(cudaEventRecord(ev_pf, pstream));
-    }
+    // dedup + hit/miss, then the host-miss gather, in stream order on pstream:
+    // one graph launch per prefetch (its host cost sits on every step)
+    const GraphKey key{4, b.indices_dev, b.bag_offsets_dev, nullptr, 0};
+    run_maybe_graphed(key, pstream, [&] {
+      enqueue_dedup_partition(b.indices_dev, pstream);
+      if (storage == EC_STORAGE_HOST) EC_DISPATCH_VEC(launch_gather_host, pstream);
+    });
+    EC_CUDA(cudaEventRecord(ev_pf, pstream));
   } catch (...) {
     select(saved);
     throw;
@@ -864,11 +885,11 @@ void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
   const bool tma = host_tma();
   if (tma)
-    k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
-                                                             ugrad.p, rank, world);
+    k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                             world);
   else
-    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
-                                                            ugrad.p, rank, world);
+    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+                                                            world);
   launched();
 }
 
@@ -1071,7 +1092,13 @@ void Profiler::collect() {
     EC_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
     ms_[r.phase] += ms;
     calls_[r.phase] += 1;
-    free_.push_back(r.a);
+    if (timeline.size() < kTimelineCap) {
+      if (!t0) t0 = r.a;  // first event since the last timeline read
+      float s = 0.f;
+      EC_CUDA(cudaEventElapsedTime(&s, t0, r.a));
+      timeline.push_back({static_cast<double>(r.phase), static_cast<double>(s), static_cast<double>(s + ms)});
+    }
+    if (r.a != t0) free_.push_back(r.a);
     free_.push_back(r.b);
   }
   recs.clear();
@@ -1081,6 +1108,7 @@ Profiler::~Profiler() {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
+  if (t0) cudaEventDestroy(t0);
   for (auto e : free_) cudaEventDestroy(e);
 }
 
@@ -1123,6 +1151,26 @@ int ec_tables_profile(ec_tables t, int enable) {
     use_device(e.device);
     e.prof.collect();
     e.prof.on = enable != 0;
+  });
+}
+
+int ec_tables_profile_timeline(ec_tables t, double* out, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    Engine& e = E(t);
+    use_device(e.device);
+    e.prof.collect();
+    const uint64_t n = std::min<uint64_t>(cap, e.prof.timeline.size());
+    for (uint64_t i = 0; i < n; ++i) {
+      out[3 * i] = e.prof.timeline[i][0];
+      out[3 * i + 1] = e.prof.timeline[i][1];
+      out[3 * i + 2] = e.prof.timeline[i][2];
+    }
+    *count = e.prof.timeline.size();
+    e.prof.timeline.clear();
+    if (e.prof.t0) {
+      e.prof.free_.push_back(e.prof.t0);
+      e.prof.t0 = nullptr;
+    }
   });
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <array>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -87,6 +88,10 @@ struct Profiler {
   std::vector<cudaEvent_t> free_;
   double ms_[kNumPhases] = {};
   uint64_t calls_[kNumPhases] = {};
+  // (phase, start ms, end ms) relative to the first event since the last read
+  static constexpr size_t kTimelineCap = 1 << 16;
+  std::vector<std::array<double, 3>> timeline;
+  cudaEvent_t t0 = nullptr;
   cudaEvent_t take();
   void collect();
   ~Profiler();
@@ -102,7 +107,7 @@ struct PhaseScope {
 };
 
 struct GraphKey {
-  int kind;  // 0 forward, 1 backward, 2 forward of a prefetched batch, 3 backward patching a prefetch
+  int kind;  // 0 forward, 1 backward, 2 forward of a prefetched batch, 3 backward patching a prefetch, 4 prefetch
   const void* a;
   const void* b;
   const void* c;
@@ -175,11 +180,14 @@ struct Engine {
   int scatter_mode = 0;  // 0 auto (fused when possible), 1 float4 atomics, 2 transpose + segmented reduction
   // dedup by one thread-block cluster per table (K1+K2 in one kernel)
   bool use_cluster() const { return (cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2); }
-  // single rank on the cluster path: the forward pools straight from the
-  // source rows (no K3 gather of cached/HBM rows) and the backward scatters
-  // -lr * grad straight into them (no ugrad pass, no K6b apply launch)
-  // (only where the atomic scatter is the right backward: <= 32K lookups per table)
-  bool fused() const { return use_cluster() && world == 1 && !in_group && scatter_mode == 0 && max_n_batch < 32768; }
+  // single rank, atomic-scatter regime (<= 32K lookups per table, e.g. the
+  // Kaggle configs): the forward pools straight from the source rows (no K3
+  // gather of cached/HBM rows) and the backward scatters -lr * grad straight
+  // into them (no ugrad round trip, no K6b launch).  Measured: Kaggle HBM tier
+  // 76 -> 64 us per step; but TB (26 x 65K, D=64) 0.42 -> 0.44 ms and cfg1
+  // (P=20) 0.23 -> 0.24 ms, where pooling from the compact L2-resident copy of
+  // the unique rows beats re-reading every lookup's row at its source.
+  bool fused() const { return world == 1 && !in_group && scatter_mode == 0 && max_n_batch < 32768; }
   int64_t max_n_batch = 0;  // largest per-table lookup count of the current geometry
   void select(int i);
   DevBuf<Tile> tiles;
@@ -197,6 +205,7 @@ struct Engine {
   float* out_ptr = nullptr;
 
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
+  cudaEvent_t ev_pfcall = nullptr;  // caller's stream at the prefetch call
   cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr,
               ev_grad = nullptr, ev_patch = nullptr;
   uint64_t geom_version = 0;

@@ -348,14 +348,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
 }
 
 // Misses served from pinned host memory (UVA-mapped shard), side stream.
-// Also zeroes the misses' gradient rows (the fused single-rank backward
-// accumulates them there for the host write-back).
 template <int VEC, int R>
 __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                                                           const uint32_t* __restrict__ missq,
                                                           const uint32_t* __restrict__ uniq,
                                                           const uint16_t* __restrict__ utab, float* __restrict__ urows,
-                                                          float* __restrict__ ugrad, int rank, int world) {
+                                                          int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -372,7 +370,6 @@ __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __rest
       if (q < nm) {
         const uint32_t g = missq[q];
         const uint32_t id = uniq[g];
-        st4(ugrad + static_cast<int64_t>(g) * D + m.c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
         if (static_cast<int>(id % world) == rank) {
           const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
           v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
@@ -421,13 +418,26 @@ __device__ __forceinline__ const float* src_row(const RowSrc& rs, const TableDev
   return rs.urows + static_cast<int64_t>(u) * D;
 }
 
-// Reset tail of a direct-source pool: the batch's dedup-set slots go back to
-// empty (what k_gather does on the gathering path).
-__device__ __forceinline__ void reset_sets(const TableDev* td, int T, const int* ctr, const uint16_t* utab,
-                                           const uint32_t* uslot, int b, int nb) {
-  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
-  for (int g = b * blockDim.x + threadIdx.x; g < U; g += nb * blockDim.x) {
-    td[utab[g]].hash[uslot[g]] = kEmptySlot;
+// Reset tail of a direct-source pool (what k_gather does on the gathering
+// path): the batch's dedup-set slots go back to empty, and the gradient rows
+// of its misses (the only ones k_scatter<SGD> accumulates) start at zero.
+struct ResetOut {
+  const int* ctr;
+  const uint16_t* utab;
+  const uint32_t* uslot;
+  const int32_t* usrc;
+  float* ugrad;
+};
+template <int VEC>
+__device__ __forceinline__ void reset_sets(const TableDev* td, int T, const ResetOut& ro, int b, int nb) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = 32 / VEC;
+  const int U = counters(const_cast<int*>(ro.ctr), T).ubase[T];
+  const int sub = lane_id() / VEC, c = lane_id() % VEC;
+  const int warp = (b * blockDim.x + threadIdx.x) >> 5, nwarps = (nb * blockDim.x) >> 5;
+  for (int g = warp * RPW + sub; g < U; g += nwarps * RPW) {
+    if (c == 0) td[ro.utab[g]].hash[ro.uslot[g]] = kEmptySlot;
+    if (ro.usrc[g] < 0) st4(ro.ugrad + static_cast<int64_t>(g) * D + c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 
@@ -438,14 +448,13 @@ template <int VEC, int R, bool DIRECT = false>
 __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
                                                    const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
                                                    const float* __restrict__ urows, float* __restrict__ out,
-                                                   RowSrc rs = {}, int pool_blocks = 0, const int* ctr = nullptr,
-                                                   const uint16_t* utab = nullptr, const uint32_t* uslot = nullptr) {
+                                                   RowSrc rs = {}, int pool_blocks = 0, ResetOut ro = {}) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
   const int nbags = T * B;
   if (DIRECT && static_cast<int>(blockIdx.x) >= pool_blocks) {
-    reset_sets(td, T, ctr, utab, uslot, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
+    reset_sets<VEC>(td, T, ro, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
     return;
   }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -504,14 +513,13 @@ template <int VEC, int R, bool DIRECT = false>
 __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__ td, int T, int B,
                                                     const uint32_t* __restrict__ inv, const float* __restrict__ urows,
                                                     float* __restrict__ out, RowSrc rs = {}, int pool_blocks = 0,
-                                                    const int* ctr = nullptr, const uint16_t* utab = nullptr,
-                                                    const uint32_t* uslot = nullptr) {
+                                                    ResetOut ro = {}) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
   const int nbags = T * B;
   if (DIRECT && static_cast<int>(blockIdx.x) >= pool_blocks) {
-    reset_sets(td, T, ctr, utab, uslot, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
+    reset_sets<VEC>(td, T, ro, blockIdx.x - pool_blocks, gridDim.x - pool_blocks);
     return;
   }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1265,8 +1273,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
                                                               const uint32_t* __restrict__ missq,
                                                               const uint32_t* __restrict__ uniq,
                                                               const uint16_t* __restrict__ utab,
-                                                              float* __restrict__ urows, float* __restrict__ ugrad,
-                                                              int rank, int world) {
+                                                              float* __restrict__ urows, int rank, int world) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
   constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
@@ -1314,10 +1321,8 @@ __global__ void __launch_bounds__(kThreads) k_gather_host_tma(const TableDev* __
     for (int i = threadIdx.x; i < cnt * VEC; i += blockDim.x) {
       const int r = i / VEC, c = i - r * VEC;
       const uint32_t g = dst_g[r];
-      if (g != 0xFFFFFFFFu) {
+      if (g != 0xFFFFFFFFu)
         st4(urows + static_cast<int64_t>(g) * D + c * 4, *reinterpret_cast<const float4*>(buf + r * D + c * 4));
-        st4(ugrad + static_cast<int64_t>(g) * D + c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
-      }
     }
     __syncthreads();
   }
@@ -1329,6 +1334,9 @@ namespace ec {
 
 // Host write-back through the TMA engine: new rows are built in shared memory
 // and bulk-stored to the pinned host shard (cp.async.bulk global <- shared).
+// With a pending prefetched batch (nxt_td != null; launched after its host
+// gather) the same new rows also refresh that batch's gathered copies — the
+// k_patch_prefetch work, without a separate launch on the critical path.
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __restrict__ td, int T,
                                                              const int* __restrict__ ctr,
@@ -1337,12 +1345,14 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
                                                              const uint16_t* __restrict__ utab,
                                                              const float* __restrict__ urows,
                                                              const float* __restrict__ ugrad, float lr, int rank,
-                                                             int world) {
+                                                             int world, const TableDev* __restrict__ nxt_td = nullptr,
+                                                             const int32_t* __restrict__ nxt_usrc = nullptr,
+                                                             float* __restrict__ nxt_urows = nullptr) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
   constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
   __shared__ __align__(128) float buf[kTmaRows * D];
-  __shared__ uint32_t dst_g[kTmaRows];
+  __shared__ uint32_t dst_g[kTmaRows], pat_g[kTmaRows];
   const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
   // spread the misses over every CTA (each SM's TMA unit issues its own rows)
   const int chunk = max(1, min(kTmaRows, (nm + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x)));
@@ -1350,7 +1360,25 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
     const int cnt = min(chunk, nm - q0);
     if (threadIdx.x < cnt) {
       const uint32_t g = missq[q0 + threadIdx.x];
-      dst_g[threadIdx.x] = static_cast<int>(uniq[g] % world) == rank ? g : 0xFFFFFFFFu;
+      const uint32_t id = uniq[g];
+      const bool own = static_cast<int>(id % world) == rank;
+      dst_g[threadIdx.x] = own ? g : 0xFFFFFFFFu;
+      uint32_t g2 = 0xFFFFFFFFu;
+      if (own && nxt_td) {  // the id's entry in the pending batch's set: its (tagged) unique index
+        const TableDev tb = nxt_td[utab[g]];
+        uint32_t h = table_slot(tb, id);
+        for (;;) {
+          const unsigned long long v = __ldcg(tb.hash + h);
+          if (v == kEmptySlot) break;
+          if (static_cast<uint32_t>(v >> 32) == id) {
+            const uint32_t u2 = static_cast<uint32_t>(v) & ~kRankTag;
+            if (nxt_usrc[u2] < 0) g2 = u2;  // gathered from the host tier: stale copy
+            break;
+          }
+          h = (h + 1) & tb.mask;
+        }
+      }
+      pat_g[threadIdx.x] = g2;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < cnt * VEC; i += blockDim.x) {
@@ -1359,8 +1387,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
       if (g == 0xFFFFFFFFu) continue;
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + c * 4);
       const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4);
-      *reinterpret_cast<float4*>(buf + r * D + c * 4) =
-          make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      const float4 nw = make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      *reinterpret_cast<float4*>(buf + r * D + c * 4) = nw;
+      if (pat_g[r] != 0xFFFFFFFFu) st4(nxt_urows + static_cast<int64_t>(pat_g[r]) * D + c * 4, nw);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async (TMA) proxy
     __syncthreads();

@@ -18,7 +18,24 @@ STORAGE = {"hbm": 0, "host": 1}
 
 
 def _stream_ptr(torch, device):
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # an int, without a Stream object
+    if raw is not None:
+        return raw(device)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def _offsets_array(cache, table_offsets):
+    """int64 ndarray of a table-offsets sequence, memoised by value (the
+    per-step host cost of a lookup is a few microseconds of Python)."""
+    if isinstance(table_offsets, np.ndarray) and table_offsets.dtype == np.int64 and table_offsets.flags.c_contiguous:
+        return table_offsets
+    key = tuple(table_offsets)
+    a = cache.get(key)
+    if a is None:
+        if len(cache) > 64:
+            cache.clear()
+        a = cache[key] = np.ascontiguousarray(key, dtype=np.int64)
+    return a
 
 
 class EmbeddingTables:
@@ -33,6 +50,9 @@ class EmbeddingTables:
                  max_lookups_per_table: int, max_batch_size: int, device: int = 0):
         import torch
         self.torch = torch
+        self._offs_cache = {}
+        self._batch_cache = {}  # (indices ptr, offsets, bag offsets, B, P) -> ctypes Batch (per-step host cost)
+        self._stats_bufs = None
         self.rows = [int(r) for r in rows]
         self.T = len(self.rows)
         self.D = int(dim)
@@ -84,6 +104,14 @@ class EmbeddingTables:
         """Per-phase CUDA-event timing of forward/backward (see ec_tables_profile)."""
         check(N.lib().ec_tables_profile(self._h, 1 if enable else 0))
 
+    def profile_timeline(self, cap: int = 1 << 16):
+        """[(phase name, start ms, end ms)] of the profiled kernels since the last call."""
+        buf = np.zeros(3 * cap, np.float64)
+        n = C.c_uint64()
+        check(N.lib().ec_tables_profile_timeline(self._h, buf.ctypes.data, cap, C.byref(n)))
+        k = min(cap, n.value)
+        return [(self.PHASES[int(buf[3 * i])], float(buf[3 * i + 1]), float(buf[3 * i + 2])) for i in range(k)]
+
     def profile_read(self, reset: bool = True):
         ms = np.zeros(len(self.PHASES), np.float64)
         calls = np.zeros(len(self.PHASES), np.uint64)
@@ -129,7 +157,7 @@ class EmbeddingTables:
         torch = self.torch
         if indices.dtype not in (torch.int32, torch.uint32) or not indices.is_cuda or not indices.is_contiguous():
             raise ValidationError("indices must be a contiguous int32/uint32 CUDA tensor")
-        offs = np.ascontiguousarray(table_offsets, dtype=np.int64)
+        offs = _offsets_array(self._offs_cache, table_offsets)
         if offs.size != self.T + 1:
             raise ValidationError("table_offsets needs num_tables+1 entries")
         self._offsets = offs
@@ -140,20 +168,36 @@ class EmbeddingTables:
             if bag_offsets.dtype != torch.int64 or not bag_offsets.is_cuda:
                 raise ValidationError("bag_offsets must be an int64 CUDA tensor")
             bo = bag_offsets.data_ptr()
-        b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo or None, batch_size, pooling)
-        check(N.lib().ec_lookup_fwd(self._h, C.byref(b), out.data_ptr(), _stream_ptr(torch, self.device)))
+        b = self._batch(indices.data_ptr(), offs, bo or None, batch_size, pooling)
+        check(N.lib().ec_lookup_fwd(self._h, b, out.data_ptr(), _stream_ptr(torch, self.device)))
         self._out = out
         return out
 
-    def prefetch(self, indices, table_offsets: Sequence[int], batch_size: int, pooling: int = 0, bag_offsets=None):
+    def prefetch(self, indices, table_offsets: Sequence[int], batch_size: int, pooling: int = 0, bag_offsets=None,
+                 stream=None):
         """Start the next batch (dedup, hit/miss, host-miss gather) while the
         current one finishes; the next forward() with the same `indices`
-        tensor consumes it.  Same geometry as the last forward."""
-        offs = np.ascontiguousarray(table_offsets, dtype=np.int64)
+        tensor consumes it.  Same geometry as the last forward.  `stream`: the
+        torch stream that produced `indices` (default: the current stream);
+        the prefetch starts after the work enqueued there."""
+        offs = _offsets_array(self._offs_cache, table_offsets)
         bo = bag_offsets.data_ptr() if bag_offsets is not None else None
         self._pf_offs = offs  # keep alive for the call
-        b = N.Batch(indices.data_ptr(), offs.ctypes.data_as(C.POINTER(C.c_int64)), bo, batch_size, pooling)
-        check(N.lib().ec_lookup_prefetch(self._h, C.byref(b), _stream_ptr(self.torch, self.device)))
+        b = self._batch(indices.data_ptr(), offs, bo, batch_size, pooling)
+        sp = stream.cuda_stream if stream is not None else _stream_ptr(self.torch, self.device)
+        check(N.lib().ec_lookup_prefetch(self._h, b, sp))
+
+    def _batch(self, ptr, offs, bo, batch_size, pooling):
+        """ctypes ec_batch by reference, memoised (the offsets array is kept
+        alive by the offsets cache)."""
+        key = (ptr, id(offs), bo, batch_size, pooling)
+        b = self._batch_cache.get(key)
+        if b is None:
+            if len(self._batch_cache) > 64:
+                self._batch_cache.clear()
+            st = N.Batch(ptr, offs.ctypes.data_as(C.POINTER(C.c_int64)), bo, batch_size, pooling)
+            b = self._batch_cache[key] = (C.byref(st), st, offs)
+        return b[0]
 
     def schedule(self, sample_ids):
         """Hot/normal order of a dataset (sample-major [q, T] int32/uint32 CUDA
@@ -207,8 +251,8 @@ class EmbeddingTables:
     def stats_collect(self, slot: int, per_table: bool = False):
         """Wait for slot `slot`'s copy and decode it like stats()."""
         s = N.BatchStats()
-        u = np.zeros(self.T, np.int64)
-        m = np.zeros(self.T, np.int64)
+        u = np.empty(self.T, np.int64)
+        m = np.empty(self.T, np.int64)
         check(N.lib().ec_lookup_stats_collect(self._h, slot, C.byref(s), u.ctypes.data, m.ctypes.data))
         d = s.as_dict()
         if per_table:
