@@ -308,7 +308,9 @@ def run_ours(args, wl):
             dev_ids[k % NS].copy_(host_ids[k % N_BATCHES], non_blocking=True)
             copied[k % NS].record(copy_stream)
 
-    def e2e_steps(nsteps):
+    e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+
+    def e2e_steps(nsteps, marks=None):
         # input pipelining: step k+2's H2D runs during step k, so a step's
         # prefetch never waits on the link; every step still moves its own ids
         # host->device and reads its result back
@@ -317,6 +319,8 @@ def run_ours(args, wl):
             h2d(1)
         res = None
         for k in range(nsteps):
+            if marks is not None:
+                marks[k].record(stream)
             stream.wait_event(copied[k % NS])
             if args.prefetch and k == 0:
                 tab.prefetch(dev_ids[0], offs, B, P, stream=copy_stream)
@@ -343,12 +347,16 @@ def run_ours(args, wl):
     torch.cuda._sleep(HEAD_START_CYCLES)
     gc.disable()  # no collector pauses inside the timed host loop
     e2e_start.record(stream)
-    counters = e2e_steps(args.steps)
+    counters = e2e_steps(args.steps, e2e_marks)
     e2e_end.record(stream)
     torch.cuda.synchronize()
     gc.enable()
     barrier()
     e2e_ms = e2e_start.elapsed_time(e2e_end) / args.steps
+    e2e_marks[args.steps] = e2e_end
+    e2e_step = [e2e_marks[k].elapsed_time(e2e_marks[k + 1]) for k in range(args.steps)]
+    e2e_dist = {"min": round(min(e2e_step), 5), "median": round(statistics.median(e2e_step), 5),
+                "max": round(max(e2e_step), 5), "argmax": int(np.argmax(e2e_step))}
     if world > 1:
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -452,7 +460,7 @@ def run_ours(args, wl):
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
                    "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
-                "ms_per_step": round(e2e_ms, 5),
+                "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
                 "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4)},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
@@ -588,7 +596,7 @@ def main():
                     help="unpipelined steps (default: ec_lookup_prefetch of the next batch overlaps this step)")
     ap.add_argument("--stream-priority", type=int, default=-1,
                     help="priority of the caller's stream (torch: -1 high, 0 low; engine side streams are low)")
-    ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster"], default=None)
+    ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster", "table"], default=None)
     ap.add_argument("--scatter-mode", choices=["auto", "atomic", "transpose"], default=None)
     args = ap.parse_args()
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:

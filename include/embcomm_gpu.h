@@ -273,12 +273,14 @@ int ec_tables_profile_timeline(ec_tables t, double* out, uint64_t cap, uint64_t*
  * stream, under profiling, inside an outer capture or with world > 1, kernels
  * are launched directly. */
 int ec_tables_use_graphs(ec_tables t, int enable);
-/* Dedup implementation: 0 (default, auto) one thread-block cluster per table
- * (insert, flags, scan, emit, inverse and hit/miss in one kernel) when the
- * tables fill the GPU (8*T >= SMs) and every table's batch has <= 32768
- * lookups, else the tile path; 1 forces the tile path (k_insert -> k_compact
- * -> k_inverse_partition); 2 forces the cluster kernel whenever every
- * table's batch has <= 131072 lookups.  Identical results. */
+/* Dedup implementation (identical results): 0 (default, auto) one
+ * thread-block cluster per table (insert, flags, scan, emit, inverse and
+ * hit/miss in one kernel) when the tables fill the GPU (8*T >= SMs) and every
+ * table's batch has <= 32768 lookups, else the tile path; 1 forces the tile
+ * path (k_insert -> k_compact -> k_inverse_partition); 2 forces the cluster
+ * kernel whenever every table's batch has <= 65536 lookups; 3 one CTA per
+ * table (k_dedup_table) whenever every batch has <= 16384 lookups.  Modes
+ * 2 and 3 need direct-mapped dedup sets (tables up to 2^27 rows). */
 int ec_tables_dedup_mode(ec_tables t, int mode);
 /* Gradient reduction per unique row (K6a): 1 one float4 atomic per lookup
  * after warp-level pre-aggregation; 2 transpose — lookups grouped by unique

@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -357,9 +358,17 @@ void Engine::create(const ec_tables_config& c) {
   }
   upload_tdev();
   select(cur);
-  EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-  EC_CUDA(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
-  EC_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  {
+    // stream priorities (lower number = higher priority); EC_PRIO="prefetch,side2"
+    // overrides the defaults for experiments
+    int lo = 0, hi = 0;
+    EC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    int pf_prio = lo, wb_prio = lo;
+    if (const char* v = std::getenv("EC_PRIO")) std::sscanf(v, "%d,%d", &pf_prio, &wb_prio);
+    EC_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+    EC_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, pf_prio));
+    EC_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, wb_prio));
+  }
   EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_release, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
@@ -540,6 +549,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   // of 8 CTAs per table); larger per-table batches need more items per thread.
   cluster_fits = nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * kClusterMaxItems;
   for (uint32_t t = 0; t < T; ++t) cluster_fits = cluster_fits && td_host[t].direct;
+  table_fits = cluster_fits && nmax <= static_cast<int64_t>(kTableThreads) * kTableMaxItems;
   cluster_ok = cluster_fits && static_cast<int64_t>(T) * kClusterCtas >= sm_count(device) &&
                nmax <= static_cast<int64_t>(kClusterCtas) * kClusterThreads * 8;
   cluster_items = 1;
@@ -988,6 +998,21 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
+  if (use_table_kernel()) {
+    EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
+    EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
+    PhaseScope ph(prof, kPhaseDedupCluster, st);
+    static bool attr_set[64] = {};
+    if (!attr_set[device & 63]) {
+      EC_CUDA(cudaFuncSetAttribute(k_dedup_table, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(table_smem_bytes())));
+      attr_set[device & 63] = true;
+    }
+    k_dedup_table<<<T, kTableThreads, table_smem_bytes(), st>>>(tdev.p, static_cast<int>(T), indices, tstat.p, ctr.p,
+                                                                uniq.p, uslot.p, utab.p, inv.p, usrc.p, missq.p);
+    launched();
+    return;
+  }
   if (use_cluster()) {
     // one thread-block cluster per table: K1 + K2 in a single kernel
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
@@ -1193,7 +1218,8 @@ int ec_tables_profile_read(ec_tables t, double* ms, uint64_t* calls, uint64_t* l
 
 int ec_tables_dedup_mode(ec_tables t, int mode) {
   return guard([&] {
-    if (mode < 0 || mode > 2) invalid("dedup mode: 0 auto, 1 tiles, 2 cluster per table (when it fits)");
+    if (mode < 0 || mode > 3)
+      invalid("dedup mode: 0 auto, 1 tiles, 2 cluster per table, 3 one CTA per table (when it fits)");
     Engine& e = E(t);
     e.dedup_mode = mode;
     e.clear_graphs();

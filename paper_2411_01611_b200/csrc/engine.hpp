@@ -168,7 +168,8 @@ struct Engine {
   bool cluster_fits = false;        // every table's batch fits one cluster
   bool cluster_ok = false;          // ... and the cluster path is the faster one
   int cluster_items = 1;            // positions per thread of the cluster kernel
-  int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path when it fits
+  int dedup_mode = 0;               // 0 auto, 1 tile path, 2 cluster path, 3 CTA-per-table path (when they fit)
+  bool table_fits = false;          // every table's batch fits one CTA (k_dedup_table)
   View<int> ctr, cnt, off, part;
   int* ctr_host = nullptr;  // pinned staging for ec_lookup_stats
   // ec_lookup_stats_enqueue ring: pinned counter copies + their completion events
@@ -179,7 +180,10 @@ struct Engine {
   View<uint2> list;
   int scatter_mode = 0;  // 0 auto (fused when possible), 1 float4 atomics, 2 transpose + segmented reduction
   // dedup by one thread-block cluster per table (K1+K2 in one kernel)
-  bool use_cluster() const { return (cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2); }
+  bool use_table_kernel() const { return table_fits && dedup_mode == 3; }
+  bool use_cluster() const {
+    return use_table_kernel() || (cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2);
+  }
   // single rank, atomic-scatter regime (<= 32K lookups per table, e.g. the
   // Kaggle configs): the forward pools straight from the source rows (no K3
   // gather of cached/HBM rows) and the backward scatters -lr * grad straight

@@ -823,7 +823,10 @@ __device__ unsigned long long* g_trace;
 namespace ec {
 
 namespace cg = cooperative_groups;
-constexpr int kClusterCtas = 8;
+#ifndef EC_CLUSTER_CTAS
+#define EC_CLUSTER_CTAS 8
+#endif
+constexpr int kClusterCtas = EC_CLUSTER_CTAS;
 constexpr int kClusterThreads = 512;
 constexpr int kClusterMaxItems = 16;     // per thread -> n_t <= 8 * 512 * 16 = 65536
 constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared memory
@@ -1035,6 +1038,213 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
       inv[tb.base + p0 + j] = id[j] == kEmptyKey ? kInvalidSlot : (((rep >> j) & 1) ? pf[j] : sval[id[j]]);
   EC_TRACE_AT(7);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // keep this CTA's smem alive for remote readers
+}
+
+}  // namespace ec
+
+// ===================================================================
+// K1 + K2 with ONE CTA per table, for small per-table batches (<= 16K
+// lookups: the Kaggle configs).  Same algorithm and output as the cluster
+// kernel, but every phase boundary is a __syncthreads -- all inserts into a
+// table's direct-mapped L2 set come from this CTA, so a CTA barrier orders
+// them -- and the kernel occupies T SMs instead of 8*T/2, leaving the rest of
+// the GPU to the pool/scatter/host kernels it overlaps in the pipelined step.
+//
+// Thread t owns positions [t*I, (t+1)*I) (I = ceil(n / threads) <= 32);
+// ids are staged in shared memory item-major (conflict-free) and processed
+// 8 per round.  Hot ids (< kTableLocal) are deduplicated in a direct-mapped
+// shared table (first position by atomicMin, later the unique index); colder
+// ids by one 64-bit atomicMin on their L2 slot.
+// ===================================================================
+namespace ec {
+
+constexpr int kTableThreads = 512;
+constexpr int kTableMaxItems = 32;       // n_t <= 16384
+constexpr uint32_t kTableLocal = 16384;  // hot ids in shared memory
+constexpr int kTableRound = 8;
+__host__ __device__ constexpr size_t table_smem_bytes() {
+  return (static_cast<size_t>(kTableThreads) * kTableMaxItems + kTableLocal) * sizeof(uint32_t);
+}
+
+__global__ void __launch_bounds__(kTableThreads, 1)
+    k_dedup_table(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
+                  unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
+                  uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
+                  int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t* s_id = smem;                                       // [I][threads]: ids, item-major
+  uint32_t* sval = smem + kTableThreads * kTableMaxItems;      // hot id -> first position, later unique index
+  __shared__ int sw[kTableThreads / 32];
+  __shared__ int s_base;
+  const int t = blockIdx.x;  // blocks dispatch in order: lower tables are running or done
+  Counters c = counters(ctr, T);
+  const TableDev tb = td[t];
+  const int n = static_cast<int>(tb.n);
+  const int I = (n + kTableThreads - 1) / kTableThreads;
+  const int tid = threadIdx.x;
+  const int p0 = tid * I;
+  const int my = max(0, min(I, n - p0));
+  const uint32_t nloc = tb.rows < kTableLocal ? static_cast<uint32_t>(tb.rows) : kTableLocal;
+  // ids -> shared (item-major), all of a thread's loads in flight at once;
+  // hot slots cleared meanwhile
+  if (my == I && I % 4 == 0 && ((tb.base + p0) & 3) == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(indices + tb.base + p0);
+#pragma unroll
+    for (int q0 = 0; q0 < kTableMaxItems / 4; q0 += 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (q0 + q) * 4 < I ? __ldg(src + q0 + q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = (q0 + q) * 4;
+        if (j < I) {
+          s_id[(j + 0) * kTableThreads + tid] = v[q].x;
+          s_id[(j + 1) * kTableThreads + tid] = v[q].y;
+          s_id[(j + 2) * kTableThreads + tid] = v[q].z;
+          s_id[(j + 3) * kTableThreads + tid] = v[q].w;
+        }
+      }
+    }
+  } else {
+    for (int r0 = 0; r0 < my; r0 += kTableRound) {
+      uint32_t v[kTableRound];
+#pragma unroll
+      for (int k = 0; k < kTableRound; ++k) v[k] = r0 + k < my ? __ldg(indices + tb.base + p0 + r0 + k) : 0u;
+#pragma unroll
+      for (int k = 0; k < kTableRound; ++k)
+        if (r0 + k < my) s_id[(r0 + k) * kTableThreads + tid] = v[k];
+    }
+  }
+  for (uint32_t i = tid; i < nloc; i += kTableThreads) sval[i] = kEmptyKey;
+  __syncthreads();
+
+  // ---- inserts: hot ids into shared memory, cold ids into the L2 set
+  for (int r0 = 0; r0 < I; r0 += kTableRound) {
+#pragma unroll
+    for (int k = 0; k < kTableRound; ++k) {
+      const int j = r0 + k;
+      uint32_t id = j < my ? s_id[j * kTableThreads + tid] : kEmptyKey;
+      if (j < my && id >= tb.rows) {
+        atomicExch(c.err, 1);
+        id = kEmptyKey;
+        s_id[j * kTableThreads + tid] = kEmptyKey;
+      }
+      const uint32_t key = id < nloc ? id : kEmptyKey;
+      const unsigned peers = __match_any_sync(kFull, key);
+      if (key != kEmptyKey) {
+        if (__ffs(peers) - 1 == lane_id()) atomicMin(sval + key, static_cast<uint32_t>(p0 + j));
+      } else if (id != kEmptyKey) {
+        atomicMin(tb.hash + id, (static_cast<unsigned long long>(id) << 32) | static_cast<uint32_t>(p0 + j));
+      }
+    }
+  }
+  __syncthreads();  // this CTA made every insert of the table
+
+  // ---- first occurrences (per-thread masks, I <= 32), CTA scan
+  uint32_t first = 0;
+  for (int r0 = 0; r0 < I; r0 += kTableRound) {
+    uint32_t w[kTableRound];
+#pragma unroll
+    for (int k = 0; k < kTableRound; ++k) {
+      const int j = r0 + k;
+      const uint32_t id = j < my ? s_id[j * kTableThreads + tid] : kEmptyKey;
+      w[k] = id == kEmptyKey ? kEmptyKey : id < nloc ? sval[id] : static_cast<uint32_t>(__ldcg(tb.hash + id));
+    }
+#pragma unroll
+    for (int k = 0; k < kTableRound; ++k)
+      if (w[k] == static_cast<uint32_t>(p0 + r0 + k)) first |= 1u << (r0 + k);
+  }
+  int total;
+  const int ex = block_exclusive_scan<kTableThreads>(__popc(first), sw, &total);
+
+  // ---- table base: publish, warp-parallel look-back over lower tables
+  if (tid < 32) {
+    if (tid == 0) publish(tstatus + t, (t == 0 ? kStatInc : kStatAgg) | static_cast<uint32_t>(total));
+    int excl = 0;
+    for (int k0 = t - 1; k0 >= 0; k0 -= 32) {
+      const int k = k0 - lane_id();
+      unsigned long long v = kStatInc;  // before table 0: an inclusive zero
+      if (k >= 0) {
+        do {
+          v = *reinterpret_cast<volatile unsigned long long*>(tstatus + k);
+        } while ((v >> 32) == 0);
+      }
+      const unsigned inc = __ballot_sync(kFull, (v >> 32) == 2);
+      const int stop = inc ? __ffs(inc) - 1 : 32;
+      excl += __reduce_add_sync(kFull, lane_id() <= stop ? static_cast<int>(static_cast<uint32_t>(v)) : 0);
+      if (inc) break;
+    }
+    if (tid == 0) {
+      if (t > 0) publish(tstatus + t, kStatInc | static_cast<uint32_t>(excl + total));
+      c.ubase[t] = excl;
+      if (t == T - 1) c.ubase[T] = excl + total;
+      s_base = excl;
+    }
+  }
+  __syncthreads();
+
+  // ---- emit the firsts (+ K2 partition), unique index into the hot slot / L2 tag
+  {
+    int g = s_base + ex;
+    for (int r0 = 0; r0 < I; r0 += kTableRound) {
+      uint32_t id[kTableRound];
+      int32_t rm[kTableRound];
+#pragma unroll
+      for (int k = 0; k < kTableRound; ++k) {
+        const int j = r0 + k;
+        id[k] = ((first >> j) & 1) ? s_id[j * kTableThreads + tid] : kEmptyKey;
+        rm[k] = id[k] != kEmptyKey ? __ldg(tb.remap + id[k]) : 0;
+      }
+      uint32_t missm = 0;
+#pragma unroll
+      for (int k = 0; k < kTableRound; ++k) {
+        if (id[k] == kEmptyKey) continue;
+        uniq[g] = id[k];
+        uslot[g] = id[k];
+        utab[g] = static_cast<uint16_t>(t);
+        usrc[g] = rm[k];  // a miss iff the id is not cached (core/src/simulator.cpp:99)
+        if (id[k] < nloc) sval[id[k]] = static_cast<uint32_t>(g);
+        tb.hash[id[k]] = (static_cast<unsigned long long>(id[k]) << 32) | kRankTag | static_cast<uint32_t>(g);
+        if (rm[k] < 0) missm |= 1u << k;
+        id[k] = static_cast<uint32_t>(g++);  // now the unique index
+      }
+      // miss queue: one atomic per warp and round
+      const int nm = __popc(missm);
+      int incl = nm;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane_id() >= o) incl += y;
+      }
+      const int wtot = __shfl_sync(kFull, incl, 31);
+      int qbase = 0;
+      if (lane_id() == 31 && wtot) {
+        qbase = atomicAdd(c.miss_total, wtot);
+        atomicAdd(c.M + t, wtot);
+      }
+      qbase = __shfl_sync(kFull, qbase, 31) + incl - nm;
+#pragma unroll
+      for (int k = 0; k < kTableRound; ++k)
+        if ((missm >> k) & 1) missq[qbase++] = id[k];
+    }
+  }
+  __syncthreads();  // hot slots and L2 tags hold unique indices
+
+  // ---- inverse
+  for (int r0 = 0; r0 < I; r0 += kTableRound) {
+    uint32_t g[kTableRound];
+#pragma unroll
+    for (int k = 0; k < kTableRound; ++k) {
+      const int j = r0 + k;
+      const uint32_t id = j < my ? s_id[j * kTableThreads + tid] : kEmptyKey;
+      g[k] = id == kEmptyKey ? kInvalidSlot
+             : id < nloc     ? sval[id]
+                             : static_cast<uint32_t>(__ldcg(tb.hash + id)) & ~kRankTag;
+    }
+#pragma unroll
+    for (int k = 0; k < kTableRound; ++k)
+      if (r0 + k < my) inv[tb.base + p0 + r0 + k] = g[k];
+  }
 }
 
 }  // namespace ec

@@ -93,8 +93,9 @@ class EmbeddingTables:
         check(N.lib().ec_tables_use_graphs(self._h, 1 if enable else 0))
 
     def dedup_mode(self, mode: str = "auto"):
-        """"auto" (cluster per table when the tables fill the GPU), "tiles", or "cluster"."""
-        check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1, "cluster": 2}[mode]))
+        """"auto" (cluster per table when the tables fill the GPU), "tiles", "cluster", or "table"
+        (one CTA per table, batches of <= 16384 lookups per table)."""
+        check(N.lib().ec_tables_dedup_mode(self._h, {"auto": 0, "tiles": 1, "cluster": 2, "table": 3}[mode]))
 
     def scatter_mode(self, mode: str = "auto"):
         """Backward gradient reduction: "auto", "atomic" or "transpose"."""

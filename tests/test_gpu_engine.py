@@ -73,7 +73,8 @@ def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=
 @pytest.mark.parametrize("storage,graphs,mode", [("hbm", False, "auto"), ("host", False, "auto"),
                                                  ("hbm", True, "auto"), ("host", True, "auto"),
                                                  ("hbm", False, "tiles"), ("host", True, "tiles"),
-                                                 ("hbm", False, "cluster"), ("host", True, "cluster")])
+                                                 ("hbm", False, "cluster"), ("host", True, "cluster"),
+                                                 ("hbm", False, "table"), ("host", True, "table")])
 def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs, mode):
     if graphs:  # CUDA-graph capture/replay needs a non-default stream
         with torch.cuda.stream(torch.cuda.Stream()):
@@ -203,15 +204,18 @@ def test_config1_full_size_counts_and_sets(ec, torch, ref, mode):
     tab.close()
 
 
-def test_config2_kaggle_shape_host_tier(ec, torch, ref):
+@pytest.mark.parametrize("mode", ["auto", "cluster", "table"])
+def test_config2_kaggle_shape_host_tier(ec, torch, ref, mode):
     """Config 2 (BASELINE.json configs[1]): 26 Kaggle-cardinality tables, D=16,
     b=16384, P=1, 256 MB HBM cache placed by global top-k probability, cold
-    rows in pinned host memory.  Counts vs reference, sets vs oracle."""
+    rows in pinned host memory.  Counts vs reference, sets vs oracle, every
+    dedup kernel that fits the shape."""
     D, B = 16, 16384
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in KAGGLE]
     ks = ec.place_topk_global(dists, (256 << 20) // (D * 4))
     caches = [d.top_ids(k) for d, k in zip(dists, ks)]
     tab = ec.EmbeddingTables(KAGGLE, D, storage="host", max_lookups_per_table=B, max_batch_size=B)
+    tab.dedup_mode(mode)
     tab.init_synthetic(3, 0.1)
     tab.place_cache(caches)
     ids, offs = make_ids(ec, torch, dists, [B] * 26, 555)
@@ -336,8 +340,9 @@ def test_skew_sweep_distributions(ec, torch, ref):
     tab.close()
 
 
-@pytest.mark.parametrize("n_max", [700, 8192, 16384, 32768, 65536])
-def test_cluster_dedup_every_width(ec, torch, ref, n_max):
+@pytest.mark.parametrize("mode,n_max", [("cluster", 700), ("cluster", 8192), ("cluster", 16384), ("cluster", 32768),
+                                        ("cluster", 65536), ("table", 700), ("table", 9000), ("table", 16384)])
+def test_cluster_dedup_every_width(ec, torch, ref, mode, n_max):
     """The cluster kernel at every positions-per-thread width (1..16): tiny
     tables (direct-mapped local set, thousands of repeats of 3 ids), mid-size
     tables (local hash), a 10M-row table, ragged per-table counts and an empty
@@ -352,7 +357,7 @@ def test_cluster_dedup_every_width(ec, torch, ref, n_max):
     # CSR: one bag per table holding all of its lookups
     bag = np.concatenate([[0], offs[1:]]).astype(np.int64)
     tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=n_max, max_batch_size=B)
-    tab.dedup_mode("cluster")
+    tab.dedup_mode(mode)
     tab.init_synthetic(4, 0.5)
     tab.place_cache(caches)
     ids, _ = make_ids(ec, torch, dists, n, 900 + n_max)

@@ -1,0 +1,88 @@
+"""Host time per call in bench.py's e2e loop (pinned H2D of ids, forward,
+prefetch, backward, async stats).  usage: python tools/e2ecost.py [workload] [steps]"""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2411_01611_b200 as ec  # noqa: E402
+
+wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "kaggle"]
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+torch.cuda.set_device(0)
+st = torch.cuda.Stream(priority=-1)
+torch.cuda.set_stream(st)
+tab, dists, caches, ks = bench.build_tables(ec, torch, wl, 0, 1, 0)
+ids, offs = bench.gen_batches(ec, torch, dists, wl, 0, bench.N_BATCHES)
+T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
+out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
+NB, NS = bench.N_BATCHES, 3
+cs = torch.cuda.Stream()
+host_ids = ids.cpu().pin_memory()
+dev_ids = [torch.empty_like(ids[0]) for _ in range(NS)]
+copied = [torch.cuda.Event() for _ in range(NS)]
+consumed = [torch.cuda.Event() for _ in range(NS)]
+acc = {}
+
+
+def tick(name, t0):
+    t1 = time.perf_counter()
+    acc.setdefault(name, []).append((t1 - t0) * 1e6)
+    return t1
+
+
+def h2d(k):
+    with torch.cuda.stream(cs):
+        if k >= NS:
+            cs.wait_event(consumed[k % NS])
+        dev_ids[k % NS].copy_(host_ids[k % NB], non_blocking=True)
+        copied[k % NS].record(cs)
+
+
+DO_H2D = os.environ.get("E2E_H2D", "1") == "1"
+DO_STATS = os.environ.get("E2E_STATS", "1") == "1"
+
+
+def run(n, rec):
+    h2d(0)
+    h2d(1)
+    tab.prefetch(dev_ids[0], offs, B, P, stream=cs)
+    for k in range(n):
+        t = time.perf_counter()
+        st.wait_event(copied[k % NS])
+        t = tick("wait_copy", t) if rec else t
+        o = tab.forward(dev_ids[k % NS], offs, B, P, out=out)
+        t = tick("forward", t) if rec else t
+        consumed[k % NS].record(st)
+        if k + 1 < n:
+            tab.prefetch(dev_ids[(k + 1) % NS], offs, B, P, stream=cs)
+        t = tick("prefetch", t) if rec else t
+        if k + 2 < n and DO_H2D:
+            h2d(k + 2)
+        t = tick("h2d", t) if rec else t
+        tab.backward(o, bench.LR)
+        t = tick("backward", t) if rec else t
+        if DO_STATS:
+            tab.stats_enqueue(k % 4)
+        t = tick("stats_enqueue", t) if rec else t
+        if k >= 2 and DO_STATS:
+            tab.stats_collect((k - 2) % 4, per_table=True)
+        t = tick("stats_collect", t) if rec else t
+    tab.prefetch_wait()
+    torch.cuda.synchronize()
+
+
+tab.backward(tab.forward(ids[0], offs, B, P, out=out), bench.LR)  # geometry for the first prefetch
+run(20, False)
+t0 = time.perf_counter()
+run(steps, True)
+t1 = time.perf_counter()
+print(f"{sys.argv[1:]} h2d={DO_H2D} stats={DO_STATS}: e2e wall {1e6 * (t1 - t0) / steps:.1f} us/step")
+for k, v in acc.items():
+    print(f"  {k:14s} mean {np.mean(v):7.1f}  median {np.median(v):7.1f}  p90 {np.percentile(v, 90):7.1f}")
+tab.close()

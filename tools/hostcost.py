@@ -22,6 +22,7 @@ ids, offs = bench.gen_batches(ec, torch, dists, wl, 0, bench.N_BATCHES)
 T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
 out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
 NB = bench.N_BATCHES
+cs = torch.cuda.Stream()  # input stream (as in bench.py)
 parts = {"forward": [], "prefetch": [], "backward": [], "wait": []}
 
 
@@ -29,7 +30,7 @@ def step(j, rec=False):
     t0 = time.perf_counter()
     o = tab.forward(ids[j % NB], offs, B, P, out=out)
     t1 = time.perf_counter()
-    tab.prefetch(ids[(j + 1) % NB], offs, B, P)
+    tab.prefetch(ids[(j + 1) % NB], offs, B, P, stream=cs)
     t2 = time.perf_counter()
     tab.backward(o, bench.LR)
     t3 = time.perf_counter()

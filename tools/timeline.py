@@ -20,11 +20,12 @@ T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
 out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
 flush = torch.empty(bench.FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 NB = bench.N_BATCHES
+cs = torch.cuda.Stream()  # input stream (as in bench.py): prefetches order after it only
 
 
 def step(j):
     o = tab.forward(ids[j % NB], offs, B, P, out=out)
-    tab.prefetch(ids[(j + 1) % NB], offs, B, P)
+    tab.prefetch(ids[(j + 1) % NB], offs, B, P, stream=cs)
     tab.backward(o, bench.LR)
     tab.prefetch_wait()
 
