@@ -169,7 +169,7 @@ def gen_batches(ec, torch, dists, wl, rank, nb):
     return ids, offs
 
 
-def phase_bytes(st, wl, T):
+def phase_bytes(st, wl, T, fused=False):
     """Algorithmic bytes per launch of each kernel (i = s = 4 B; definitions in
     DESIGN.md §4 following SURVEY.md §8d).  n lookups, U unique rows, H cache
     hits, M misses, row = D*4 bytes."""
@@ -186,7 +186,9 @@ def phase_bytes(st, wl, T):
         "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out
         "k_gather": U * 4 + hbm_src * row + U * row + U * row,       # usrc in, rows in, urows out, ugrad zeroed
         "k_gather_host": host_rows * (4 + row + row),  # missq in, host rows in (host link), urows out
-        "k_pool": n * 4 + n * row + B * T * row,       # inverse, rows, pooled out
+        # A_pool (rows read from the compact, L2-resident copy), or
+        # A_fused when the pool reads each unique row at its source (no K3 gather)
+        "k_pool": (U * 4 + U * row + n * 4 + B * T * row) if fused else (n * 4 + n * row + B * T * row),
         "k_scatter": B * T * row + n * 4 + n * row,    # grads in, inverse in, row-grad reductions
         "k_apply": (U - host_rows) * (4 + row * 3),    # usrc, urows, ugrad in, rows out
         "k_apply_host": host_rows * (4 + row * 3),
@@ -279,6 +281,30 @@ def run_ours(args, wl):
         ms = float(t.item())
     lookups_per_step = T * B * P
     value = lookups_per_step * world / (ms * 1e-3)
+
+    # ---- forward only (K1 -> K5 incl. the host-miss gather; SURVEY 8(d) reports
+    # lookups/s of the forward and of fwd+bwd), unpipelined, L2 flushed between
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if args.prefetch:
+        tab.prefetch_wait()
+    for k in range(args.warmup):
+        tab.forward(ids[k % N_BATCHES], offs, B, P, out=out)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(HEAD_START_CYCLES)
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        fwd_ev[k][0].record(stream)
+        tab.forward(ids[k % N_BATCHES], offs, B, P, out=out)
+        fwd_ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+    if world > 1:
+        t = torch.tensor([fwd_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        fwd_ms = float(t.item())
+    # restore the pipeline state of the stepping loop (a backward for the last forward)
+    tab.backward(out, LR)
+    torch.cuda.synchronize()
 
     # ---- phase profile pass (same steps, CUDA events per phase, live)
     tab.profile(True)
@@ -406,7 +432,8 @@ def run_ours(args, wl):
 
     # ---- roofline of the dominant kernel + whole-step algorithmic traffic
     import statistics as S
-    pb = [phase_bytes(s, wl, T) for s in stats]
+    fused = not prof["calls"].get("k_gather")  # single-rank fused path: no K3 gather launched
+    pb = [phase_bytes(s, wl, T, fused) for s in stats]
     mean_bytes = {k: S.mean(p[k] for p in pb) for k in pb[0]}
     pfile = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(pfile)) if os.path.exists(pfile) else {}
@@ -462,6 +489,9 @@ def run_ours(args, wl):
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
                 "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4)},
+        "fwd_only": {"value": round(lookups_per_step * world / (fwd_ms * 1e-3), 1), "unit": "lookups/s",
+                     "ms_per_step": round(fwd_ms, 5),
+                     "step": "forward only (dedup, hit/miss, host-miss gather, pool), unpipelined"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": round(dom_gbs / peak, 4), "traffic": traffic,

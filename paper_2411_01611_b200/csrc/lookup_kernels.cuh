@@ -389,8 +389,8 @@ __device__ __forceinline__ void bag_range(const TableDev* td, const int64_t* bag
   if (bag_off) {
     *lo = bag_off[static_cast<int64_t>(t) * B + s];
     *hi = bag_off[static_cast<int64_t>(t) * B + s + 1];
-  } else {
-    *lo = td[t].base + static_cast<int64_t>(s) * P;
+  } else {  // fixed pooling: table t's lookups start at t*B*P (ec_lookup_fwd checks n_t == B*P)
+    *lo = (static_cast<int64_t>(t) * B + s) * P;
     *hi = *lo + P;
   }
 }
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
       u[r] = kInvalidSlot;
       if (q < nbags) {
         const int s = q / T, t = q - s * T;
-        u[r] = __ldcs(inv + td[t].base + s);
+        u[r] = __ldcs(inv + static_cast<int64_t>(t) * B + s);  // pooling 1: table t's lookups start at t*B
       }
     }
     float4 v[R];
