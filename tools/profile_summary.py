@@ -27,7 +27,9 @@ for r in rows:
             name = d["Kernel Name"].split("(")[0].replace("void ", "")
             agg[name].append(float(d["Metric Value"].replace(",", "")))
 step_kernels = {k: v for k, v in agg.items() if not any(s in k for s in ("init_shard", "fill_cache", "set_remap",
-                                                                           "sample_stream", "FillFunctor", "Fill"))}
+                                                                           "sample_stream", "FillFunctor", "Fill", "spin_kernel",
+                                                                           "direct_copy", "arange", "k_classify",
+                                                                           "k_stable_order", "k_scan_", "k_gather_batch"))}
 tot = sum(sum(v) / len(v) for v in step_kernels.values()) or 1.0
 with open(prefix + "_launches.md", "w") as f:
     f.write(f"# ncu launch list summary ({launches})\n\n")
