@@ -187,7 +187,13 @@ int Engine::host_write_grid() const {
   }();
   return env > 0 ? env : host_grid();
 }
-int Engine::row_grid() const { return sm_count(device) * (storage == EC_STORAGE_HOST ? 3 : 4); }
+int Engine::row_grid() const {
+  static const int env = [] {
+    const char* v = std::getenv("EC_ROW_CTAS_PER_SM");
+    return v ? std::atoi(v) : 0;
+  }();
+  return sm_count(device) * (env > 0 ? env : storage == EC_STORAGE_HOST ? 3 : 4);
+}
 
 static uint32_t log2_ceil(uint64_t x) {
   uint32_t l = 0;
@@ -865,7 +871,9 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
     const GraphKey key{4, b.indices_dev, b.bag_offsets_dev, nullptr, 0};
     run_maybe_graphed(key, pstream, [&] {
       enqueue_dedup_partition(b.indices_dev, pstream);
-      if (storage == EC_STORAGE_HOST) EC_DISPATCH_VEC(launch_gather_host, pstream);
+      if (storage == EC_STORAGE_HOST) {
+        EC_DISPATCH_VEC(launch_gather_host, pstream);
+      }
     });
     EC_CUDA(cudaEventRecord(ev_pf, pstream));
   } catch (...) {

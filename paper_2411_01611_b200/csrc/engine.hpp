@@ -209,7 +209,8 @@ struct Engine {
   float* out_ptr = nullptr;
 
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
-  cudaEvent_t ev_pfcall = nullptr;  // caller's stream at the prefetch call
+  cudaEvent_t ev_pfcall = nullptr;   // caller's stream at the prefetch call
+
   cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr,
               ev_grad = nullptr, ev_patch = nullptr;
   uint64_t geom_version = 0;
