@@ -320,6 +320,8 @@ void Engine::create(const ec_tables_config& c) {
   // waits for the current batch's gather to clean the shared slots
   hash.alloc(2 * hash_off[T]);
   EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
+  idcnt.alloc(2 * hash_off[T]);
+  EC_CUDA(cudaMemset(idcnt.p, 0, idcnt.bytes()));
   const uint64_t N = max_n * T;
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
   for (BatchBufs& b : bb) {
@@ -356,6 +358,7 @@ void Engine::create(const ec_tables_config& c) {
     d.mask = static_cast<uint32_t>((1ull << hash_lg[t]) - 1);
     d.direct = hash_direct[t];
     d.pad_ = 0;
+    d.idcnt = idcnt.p + hash_off[t];
     d.remap = remap.p + remap_off[t];
     d.store = store_base + store_off[t] * D;
     d.rows = rows[t];
@@ -389,7 +392,10 @@ void Engine::create(const ec_tables_config& c) {
 void Engine::upload_tdev() {
   std::vector<TableDev> both(td_host);
   both.insert(both.end(), td_host.begin(), td_host.end());
-  for (uint32_t t = 0; t < T; ++t) both[T + t].hash += hash_off[T];
+  for (uint32_t t = 0; t < T; ++t) {
+    both[T + t].hash += hash_off[T];
+    both[T + t].idcnt += hash_off[T];
+  }
   EC_CUDA(cudaMemcpy(tdev_buf.p, both.data(), both.size() * sizeof(TableDev), cudaMemcpyHostToDevice));
 }
 
@@ -675,6 +681,11 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
     return;
   }
   if (!ntiles) return;
+  if (bb[cur].lists) {  // the forward grouped the lookups already (tile path)
+    k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p);
+    launched();
+    return;
+  }
   const int tgrid = std::min(ntiles, sm_count(device) * 8);
   k_bwd_count<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, inv.p, cnt.p);
   launched();
@@ -1036,26 +1047,40 @@ void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
     launched();
     return;
   }
+  const bool lists = lists_in_forward();
+  bb[cur].lists = lists;
   {
     if (ntiles) {
       {
         PhaseScope ph(prof, kPhaseInsert, st);
-        k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T));
+        k_insert<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T),
+                                              lists ? 1 : 0);
         launched();
       }
       PhaseScope ph(prof, kPhaseCompact, st);
       k_compact<<<ntiles, kThreads, 0, st>>>(tiles.p, tdev.p, indices, slot_of.p, status.p, ctr.p, static_cast<int>(T),
-                                             ntiles, tail_lo, uniq.p, uslot.p, utab.p);
+                                             ntiles, tail_lo, uniq.p, uslot.p, utab.p, lists ? cnt.p : nullptr);
       launched();
+      if (lists) {  // group offsets: exclusive scan of the per-unique counts (cnt becomes the fill cursor)
+        const int nparts = static_cast<int>((max_n * T + kScanTile) / kScanTile);
+        k_uscan_reduce<<<nparts, kScanThreads, 0, st>>>(cnt.p, ctr.p, static_cast<int>(T), part.p);
+        launched();
+        k_scan_partials<<<1, 1024, 0, st>>>(part.p, nparts, nullptr);
+        launched();
+        k_uscan_apply<<<nparts, kScanThreads, 0, st>>>(cnt.p, ctr.p, static_cast<int>(T), part.p, off.p);
+        launched();
+      }
     } else {
       EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     }
   }
   {
     PhaseScope ph(prof, kPhaseInversePartition, st);
+    GroupFill gf{};
+    if (lists) gf = GroupFill{list.p, off.p, cnt.p, bag_off, static_cast<int>(geom_b), static_cast<int>(geom_p)};
     k_inverse_partition<<<ntiles + sm_count(device) * 2, kThreads, 0, st>>>(tiles.p, tdev.p, slot_of.p, inv.p, ntiles,
                                                                           static_cast<int>(T), ctr.p, uniq.p, utab.p,
-                                                                          usrc.p, missq.p);
+                                                                          usrc.p, missq.p, gf);
     launched();
   }
 }

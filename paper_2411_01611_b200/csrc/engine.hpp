@@ -22,6 +22,7 @@ struct TableDev {
   int64_t n;                 // lookups of this table in the batch
   uint32_t direct;           // 1: `hash` is direct-mapped (slot = id, rows slots), no probing
   uint32_t pad_;
+  uint32_t* idcnt;           // per slot of `hash`: lookups of that id in the batch (tile path, grouped lists)
 };
 
 struct Tile {
@@ -66,6 +67,7 @@ struct BatchBufs {
   const uint32_t* indices = nullptr;  // batch held by a pending prefetch
   uint64_t geom_version = 0;
   bool pending = false;               // prefetched, not yet consumed by forward
+  bool lists = false;                 // its forward built the unique-grouped gradient lists
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
            utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + tstat.bytes() + ctr.bytes() +
@@ -145,6 +147,7 @@ struct Engine {
   float* store_base = nullptr;  // device-visible base of the shard
   DevBuf<int32_t> remap;
   DevBuf<unsigned long long> hash;
+  DevBuf<uint32_t> idcnt;  // parallel to hash: per-id lookup counts (self-cleaning with the slots)
   DevBuf<float> cache;
   DevBuf<uint32_t> cache_ids;
   DevBuf<uint16_t> cache_tab;
@@ -181,6 +184,12 @@ struct Engine {
   int scatter_mode = 0;  // 0 auto (fused when possible), 1 float4 atomics, 2 transpose + segmented reduction
   // dedup by one thread-block cluster per table (K1+K2 in one kernel)
   bool use_table_kernel() const { return table_fits && dedup_mode == 3; }
+  // backward reduction by transposition (lookups grouped by unique): auto at
+  // >= 32K lookups per table (measured in bwd_scatter)
+  bool transpose_regime() const { return scatter_mode == 2 || (scatter_mode == 0 && max_n_batch >= 32768); }
+  // the tile dedup path builds the grouped lists in the forward (counts in
+  // k_insert, offsets by scan, fill in k_inverse_partition)
+  bool lists_in_forward() const { return !use_cluster() && transpose_regime(); }
   bool use_cluster() const {
     return use_table_kernel() || (cluster_ok && dedup_mode == 0) || (cluster_fits && dedup_mode == 2);
   }

@@ -73,11 +73,36 @@ __device__ __forceinline__ uint32_t set_insert(const TableDev& t, uint32_t id, u
   return cur == kEmptySlot ? h : hash_insert_from(t.hash, t.mask, h, cur, id, lpos);
 }
 
+// grad-row index (bag) of lookup p in table t
+__device__ __forceinline__ int bag_of(const TableDev& tb, const int64_t* bag_off, int B, int P, int t, int64_t p) {
+  if (!bag_off) return static_cast<int>((p - tb.base) / P);
+  const int64_t* b = bag_off + static_cast<int64_t>(t) * B;  // last s with b[s] <= p
+  int lo = 0, hi = B;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (b[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Unique-grouped gradient list built by the forward's k_inverse_partition
+// (tile dedup path, transpose backward): lookups of unique u occupy
+// list[off[u] .. off[u+1]), as (u, grad row); `cursor` starts at zero.
+struct GroupFill {
+  uint2* list;  // null: not built here
+  const int* off;
+  int* cursor;
+  const int64_t* bag_off;
+  int B, P;
+};
+
+// With `count` set, also counts each id's lookups on its slot (idcnt, one
+// atomic per warp group) for the unique-grouped gradient lists.
 __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ tiles, const TableDev* __restrict__ td,
                                                      const uint32_t* __restrict__ indices,
                                                      uint32_t* __restrict__ slot_of,
                                                      unsigned long long* __restrict__ status, int* __restrict__ ctr,
-                                                     int T) {
+                                                     int T, int count) {
   const Tile tile = tiles[blockIdx.x];
   const TableDev t = td[tile.table];
   Counters c = counters(ctr, T);
@@ -128,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
       } else {
         slot = hash_insert_from(t.hash, t.mask, h[j], cur[j], id[j], static_cast<uint32_t>(p - t.base));
       }
+      if (count) atomicAdd(t.idcnt + slot, static_cast<uint32_t>(__popc(peers[j])));
     }
     slot = __shfl_sync(kFull, slot, leader);
     if (live[j]) slot_of[p] = slot;
@@ -158,7 +184,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
                                                       const uint32_t* __restrict__ slot_of,
                                                       unsigned long long* __restrict__ status, int* __restrict__ ctr,
                                                       int T, int ntiles, int tail_lo, uint32_t* __restrict__ uniq,
-                                                      uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab) {
+                                                      uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab,
+                                                      int* __restrict__ ucnt) {
   __shared__ int s_tile, s_excl;
   __shared__ int sw[kThreads / 32];
   Counters c = counters(ctr, T);
@@ -230,6 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
     uniq[g] = id;
     uslot[g] = h[j];
     utab[g] = static_cast<uint16_t>(tile.table);
+    if (ucnt) ucnt[g] = static_cast<int>(t.idcnt[h[j]]);  // lookups of this unique (k_insert counted them)
     // only this thread writes this slot; concurrent flag tests never match a tagged value
     t.hash[h[j]] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
   }
@@ -244,7 +272,7 @@ __global__ void __launch_bounds__(kThreads) k_inverse_partition(const Tile* __re
                                                                 int* __restrict__ ctr, const uint32_t* __restrict__ uniq,
                                                                 const uint16_t* __restrict__ utab,
                                                                 int32_t* __restrict__ usrc,
-                                                                uint32_t* __restrict__ missq) {
+                                                                uint32_t* __restrict__ missq, GroupFill gf) {
   if (static_cast<int>(blockIdx.x) < ntiles) {
     const Tile tile = tiles[blockIdx.x];
     const TableDev t = td[tile.table];
@@ -254,12 +282,28 @@ __global__ void __launch_bounds__(kThreads) k_inverse_partition(const Tile* __re
       const uint32_t off = j * kThreads + threadIdx.x;
       hs[j] = off < tile.count ? slot_of[tile.start + off] : kInvalidSlot;
     }
+    uint32_t u[kItems];
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const uint32_t off = j * kThreads + threadIdx.x;
-      if (off < tile.count)
-        inv[tile.start + off] = hs[j] == kInvalidSlot ? kInvalidSlot
-                                                      : static_cast<uint32_t>(__ldcg(t.hash + hs[j])) & ~kRankTag;
+      u[j] = hs[j] == kInvalidSlot ? kInvalidSlot : static_cast<uint32_t>(__ldcg(t.hash + hs[j])) & ~kRankTag;
+      if (off < tile.count) inv[tile.start + off] = u[j];
+    }
+    if (gf.list) {  // K6 grouping: lookup -> its unique's group (offsets from the scan of the counts)
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        const int64_t p = tile.start + j * kThreads + threadIdx.x;
+        const unsigned peers = __match_any_sync(kFull, u[j]);
+        const int leader = __ffs(peers) - 1;
+        int b0 = 0;
+        if (u[j] != kInvalidSlot && leader == lane_id()) b0 = atomicAdd(gf.cursor + u[j], __popc(peers));
+        b0 = __shfl_sync(kFull, b0, leader);
+        if (u[j] != kInvalidSlot) {
+          const int pos = gf.off[u[j]] + b0 + __popc(peers & ((1u << lane_id()) - 1));
+          gf.list[pos] = make_uint2(u[j], static_cast<uint32_t>(bag_of(t, gf.bag_off, gf.B, gf.P, static_cast<int>(tile.table), p)) *
+                                               static_cast<uint32_t>(T) + tile.table);
+        }
+      }
     }
     return;
   }
@@ -335,8 +379,10 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
           dst[r] = g;
         }
         if (m.c == 0) {
-          td[tab].hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
-          cnt[g] = 0;                           // backward occurrence count
+          const TableDev& tb = td[tab];
+          tb.hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
+          tb.idcnt[uslot[g]] = 0;
+          cnt[g] = 0;  // backward occurrence count
         }
         st4(ugrad + static_cast<int64_t>(g) * D + m.c * 4, zero);
       }
@@ -436,7 +482,11 @@ __device__ __forceinline__ void reset_sets(const TableDev* td, int T, const Rese
   const int sub = lane_id() / VEC, c = lane_id() % VEC;
   const int warp = (b * blockDim.x + threadIdx.x) >> 5, nwarps = (nb * blockDim.x) >> 5;
   for (int g = warp * RPW + sub; g < U; g += nwarps * RPW) {
-    if (c == 0) td[ro.utab[g]].hash[ro.uslot[g]] = kEmptySlot;
+    if (c == 0) {
+      const TableDev& tb = td[ro.utab[g]];
+      tb.hash[ro.uslot[g]] = kEmptySlot;
+      tb.idcnt[ro.uslot[g]] = 0;
+    }
     if (ro.usrc[g] < 0) st4(ro.ugrad + static_cast<int64_t>(g) * D + c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
@@ -767,7 +817,9 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
                              const uint16_t* __restrict__ utab, const uint32_t* __restrict__ uslot) {
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x) {
-    td[utab[g]].hash[uslot[g]] = kEmptySlot;
+    const TableDev& tb = td[utab[g]];
+    tb.hash[uslot[g]] = kEmptySlot;
+    tb.idcnt[uslot[g]] = 0;
   }
 }
 
@@ -1264,17 +1316,6 @@ __global__ void __launch_bounds__(kTableThreads, 1)
 namespace ec {
 
 
-// grad-row index (bag) of lookup p in table t
-__device__ __forceinline__ int bag_of(const TableDev& tb, const int64_t* bag_off, int B, int P, int t, int64_t p) {
-  if (!bag_off) return static_cast<int>((p - tb.base) / P);
-  const int64_t* b = bag_off + static_cast<int64_t>(t) * B;  // last s with b[s] <= p
-  int lo = 0, hi = B;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (b[mid] <= p) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
 __global__ void __launch_bounds__(kThreads) k_bwd_count(const Tile* __restrict__ tiles, int ntiles,
                                                         const uint32_t* __restrict__ inv, int* __restrict__ cnt) {

@@ -87,7 +87,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(rm, remap.data(), E * 4, cudaMemcpyHostToDevice));
     allocs.push_back(h);
     allocs.push_back(rm);
-    td[t] = TableDev{h, static_cast<uint32_t>(32 - bits), static_cast<uint32_t>(cap - 1), rm, nullptr, E, t * n, n, direct, 0};
+    td[t] = TableDev{h, static_cast<uint32_t>(32 - bits), static_cast<uint32_t>(cap - 1), rm, nullptr, E, t * n, n, direct, 0, nullptr};
   }
   const size_t N = ids.size();
   TableDev* dtd;
