@@ -220,6 +220,24 @@ int ec_estimate_distribution(const uint32_t* entry_ids_host, const uint64_t* ent
                              uint64_t num_entries, uint64_t total_accesses, uint64_t vocab, double smoothing,
                              ec_dist* out);
 
+/* ------------------------------------------ binary trace ingest (§8f row 4)
+ * The reference's Trace (core/include/embcomm/trace.hpp:18-30) in a mapped
+ * binary container instead of the desk-scale text format (trace.cpp:51-101):
+ * 40-byte little-endian header {char magic[8] "ECTRACE1"; uint32 version 1;
+ * uint32 0; int64 d; uint64 E; uint64 Q} then Q*d uint32 ids, sample-major.
+ * Validation mirrors parse_trace (d >= 1, 1 <= E <= 2^32-1, non-empty, every
+ * id < E; errors name the sample's text-format line, EC_EINVAL). */
+typedef struct ec_trace_s* ec_trace;
+int ec_trace_save_binary(const char* path, const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
+                         uint64_t vocab);
+int ec_trace_open_binary(const char* path, ec_trace* out);  /* mapped read-only */
+void ec_trace_destroy(ec_trace t);
+int ec_trace_info(ec_trace t, uint64_t* num_samples, int64_t* num_features, uint64_t* vocab);
+int ec_trace_ids(ec_trace t, const uint32_t** ids_host);  /* valid until ec_trace_destroy */
+/* samples [first, first+count) -> ids_dev (count*d ids) through pinned
+ * double-buffered staging on `stream`; returns when the copies are done */
+int ec_trace_upload(ec_trace t, uint64_t first, uint64_t count, uint32_t* ids_dev, void* stream);
+
 /* --------------------------------------------------------- lookup engine
  * No reference counterpart (SURVEY.md §2 "★ new"): row-wise sharded fp32
  * tables, a replicated HBM hot-row cache, per-table batch dedup (K1), hit/miss

@@ -304,6 +304,17 @@ def ref_delta_comm(dist, m, a, d_emb, eff, q, k):
             "delta_comm": out[3], "recommend": bool(out[4])}
 
 
+def ref_load_trace(path):
+    """The reference's parse_trace of a text trace file -> (d, vocab, ids)."""
+    d, vocab, n = C.c_int64(), C.c_uint64(), C.c_uint64()
+    _check(ref_lib().ref_load_trace(os.fsencode(path), C.byref(d), C.byref(vocab), None, C.c_uint64(0),
+                                    C.byref(n)))
+    ids = np.empty(n.value, np.uint32)
+    _check(ref_lib().ref_load_trace(os.fsencode(path), C.byref(d), C.byref(vocab), ids.ctypes.data_as(C.c_void_p),
+                                    C.c_uint64(ids.size), C.byref(n)))
+    return int(d.value), int(vocab.value), ids
+
+
 def ref_build_skew_table(ids, d, vocab):
     ids = np.ascontiguousarray(ids, dtype=np.uint32)
     oid = np.zeros(vocab, np.uint32)

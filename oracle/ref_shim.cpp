@@ -302,7 +302,18 @@ int ref_memory_io_proxy(void* h, int64_t q, int64_t b, int64_t d, const uint32_t
   });
 }
 
-// --- traces (core/src/trace.cpp:128-240)
+// --- traces (core/src/trace.cpp:51-240)
+// parse_trace of a text file: *d, *vocab, *n_ids; ids copied when cap allows
+int ref_load_trace(const char* path, int64_t* d, uint64_t* vocab, uint32_t* ids, uint64_t cap, uint64_t* n_ids) {
+  return guard([&] {
+    const Trace t = load_trace(path);
+    *d = t.num_features;
+    *vocab = t.vocab_size;
+    *n_ids = t.ids.size();
+    if (ids && cap >= t.ids.size()) std::copy(t.ids.begin(), t.ids.end(), ids);
+  });
+}
+
 // entries out: ids, counts, cum (cap = vocab); returns number of entries in *n_out
 int ref_build_skew_table(const uint32_t* ids, uint64_t n_samples, int64_t d, uint64_t vocab,
                          uint32_t* out_ids, uint64_t* out_counts, double* out_cum,

@@ -18,6 +18,7 @@ Torch is used only for device memory and streams in ``EmbeddingTables``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -36,7 +37,7 @@ __all__ = [
     "coalesced_epoch_cost", "cached_epoch_cost", "DeviceModel", "max_batch_size", "MarginalReport",
     "delta_comm", "CachePlan", "optimal_cache_size_scan", "optimal_cache_size_search", "memory_io_proxy",
     "place_topk_global", "expected_unique_many", "cost_curve", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
-    "SimResult", "measure_unique", "simulate_epoch", "Trace", "classify_samples", "build_schedule",
+    "SimResult", "measure_unique", "simulate_epoch", "Trace", "BinaryTrace", "classify_samples", "build_schedule",
     "SampleClasses", "BatchSchedule", "SkewTable", "build_skew_table", "estimate_distribution", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
 ]
 
@@ -474,6 +475,64 @@ class Trace:
     def sample(self, i: int) -> np.ndarray:
         d = self.num_features
         return np.asarray(self.ids)[i * d:(i + 1) * d]
+
+    def save_binary(self, path) -> None:
+        """Write the binary trace container (ec_trace_save_binary; SURVEY §8f
+        row 4): the reference's Trace without text parsing."""
+        ids = _u32(self.ids)
+        check(N.lib().ec_trace_save_binary(os.fsencode(path), ids.ctypes.data, self.num_samples(),
+                                           self.num_features, self.vocab_size))
+
+    @staticmethod
+    def load_binary(path) -> "BinaryTrace":
+        """Map a binary trace (validated like parse_trace); .trace() views it
+        as a Trace without copying."""
+        return BinaryTrace(path)
+
+
+class BinaryTrace:
+    """A mapped binary trace file (ec_trace_open_binary)."""
+
+    def __init__(self, path):
+        h = C.c_void_p()
+        check(N.lib().ec_trace_open_binary(os.fsencode(path), C.byref(h)))
+        self._h = h
+        q, d, e = C.c_uint64(), C.c_int64(), C.c_uint64()
+        check(N.lib().ec_trace_info(self._h, C.byref(q), C.byref(d), C.byref(e)))
+        self.num_samples, self.num_features, self.vocab_size = int(q.value), int(d.value), int(e.value)
+        p = C.c_void_p()
+        check(N.lib().ec_trace_ids(self._h, C.byref(p)))
+        n = self.num_samples * self.num_features
+        buf = (C.c_uint32 * n).from_address(p.value)
+        buf._owner = self  # views of the mapping keep the mapping alive
+        self._ids = np.frombuffer(buf, dtype=np.uint32)
+        self._ids.flags.writeable = False
+
+    def trace(self) -> Trace:
+        """Zero-copy read-only view of the mapped ids (the view keeps the
+        mapping alive)."""
+        return Trace(self.num_features, self.vocab_size, self._ids)
+
+    def upload(self, out, first: int = 0, count: Optional[int] = None) -> None:
+        """Samples [first, first+count) into a CUDA int32/uint32 tensor
+        (count*d ids, sample-major) via pinned double-buffered staging."""
+        import torch
+        count = self.num_samples - first if count is None else count
+        check(N.lib().ec_trace_upload(self._h, first, count, out.data_ptr(),
+                                      torch.cuda.current_stream(out.device).cuda_stream))
+
+    def close(self) -> None:
+        """Unmap now; only safe when no view from trace() is still in use."""
+        if self._h:
+            self._ids = None
+            N.lib().ec_trace_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def simulate_epoch(source, *args, device: int = 0) -> SimResult:

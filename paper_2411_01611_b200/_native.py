@@ -159,6 +159,12 @@ _SIGS = {
     "ec_lookup_bwd": [vp, vp, f32, vp],
     "ec_lookup_prefetch": [vp, P(Batch), vp],
     "ec_lookup_prefetch_wait": [vp, vp],
+    "ec_trace_save_binary": [C.c_char_p, vp, u64, i64, u64],
+    "ec_trace_open_binary": [C.c_char_p, P(vp)],
+    "ec_trace_destroy": [vp],
+    "ec_trace_info": [vp, P(u64), P(i64), P(u64)],
+    "ec_trace_ids": [vp, P(vp)],
+    "ec_trace_upload": [vp, u64, u64, vp, vp],
     "ec_tables_schedule": [vp, vp, u64, vp, P(u64), vp],
     "ec_tables_gather_batch": [vp, vp, vp, u64, u32, vp, vp],
     "ec_lookup_stats": [vp, vp, P(BatchStats), vp, vp],
@@ -181,6 +187,7 @@ _RESTYPE = {
     "ec_last_error": C.c_char_p, "ec_version": C.c_char_p, "ec_cost_units_note": C.c_char_p,
     "ec_rng_algorithm": C.c_char_p, "ec_substream_seed": u64, "ec_dist_size": u64,
     "ec_dist_destroy": None, "ec_sampler_destroy": None, "ec_tables_destroy": None, "ec_group_destroy": None,
+    "ec_trace_destroy": None,
 }
 
 _lib = None
