@@ -219,22 +219,24 @@ def run_ours(args, wl):
     # a prefetch is ordered after it, not after the compute stream's forward
     copy_stream = torch.cuda.Stream()
 
-    def step(j):
-        # pipelined training step: forward of batch j (its dedup, hit/miss and
-        # host-miss gather were prefetched during step j-1), prefetch of batch
-        # j+1 overlapping the backward of j, then a join so the step's window
-        # holds all of its work
-        o = tab.forward(ids[j], offs, B, P, out=out)
-        if args.prefetch:
-            tab.prefetch(ids[(j + 1) % N_BATCHES], offs, B, P, stream=copy_stream)
+    depth = args.prefetch_depth
+
+    def step(j, first=False):
+        # pipelined training step: forward of batch j (its dedup and hit/miss
+        # ran `depth` steps ago; its host-miss gather in the previous step),
+        # prefetch of batch j+depth overlapping the backward of j, then a join
+        # so the step's window holds all of its work
+        o = tab.forward(ids[j % N_BATCHES], offs, B, P, out=out)
+        for k in (range(1, depth + 1) if first else [depth] if depth else []):
+            tab.prefetch(ids[(j + k) % N_BATCHES], offs, B, P, stream=copy_stream)
         tab.backward(o, LR)  # loss = 0.5*||pooled||^2  ->  d loss / d pooled = pooled
-        if args.prefetch:
+        if depth:
             tab.prefetch_wait()
 
     # per-batch stats (deterministic per batch; outside any timed region)
     stats = []
     for j in range(N_BATCHES):
-        step(j)
+        step(j, first=j == 0)
         stats.append(tab.stats(per_table=True))
     def barrier():
         if world > 1:
@@ -251,7 +253,7 @@ def run_ours(args, wl):
         w = 0
         while w < args.warmup or time.time() - t_w < 0.5:
             flush.fill_(float(w))
-            step(w % N_BATCHES)
+            step(N_BATCHES + w)
             w += 1
             if w % 50 == 0:
                 torch.cuda.synchronize()
@@ -266,7 +268,7 @@ def run_ours(args, wl):
         for k in range(args.steps):
             flush.fill_(float(k))
             starts[k].record(stream)
-            step((w + k) % N_BATCHES)  # continues the warm-up's rotation: its last prefetch is this batch
+            step(N_BATCHES + w + k)  # continues the warm-up's rotation: its prefetches are these batches
             ends[k].record(stream)
         torch.cuda.synchronize()
         gc.enable()
@@ -285,8 +287,8 @@ def run_ours(args, wl):
     # ---- forward only (K1 -> K5 incl. the host-miss gather; SURVEY 8(d) reports
     # lookups/s of the forward and of fwd+bwd), unpipelined, L2 flushed between
     fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if args.prefetch:
-        tab.prefetch_wait()
+    if depth:
+        tab.prefetch_drop()
     for k in range(args.warmup):
         tab.forward(ids[k % N_BATCHES], offs, B, P, out=out)
     torch.cuda.synchronize()
@@ -311,7 +313,7 @@ def run_ours(args, wl):
     tab.profile_read(reset=True)
     for k in range(args.steps):
         flush.fill_(float(k))
-        step((w + args.steps + k) % N_BATCHES)
+        step(N_BATCHES + w + args.steps + k)
     torch.cuda.synchronize()
     prof = tab.profile_read(reset=True)
     tab.profile(False)
@@ -319,7 +321,7 @@ def run_ours(args, wl):
 
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
-    NS = 3  # device id slots: step k+2's copy runs during step k
+    NS = depth + 2  # device id slots: step k+depth+1's copy runs during step k
     dev_ids = [torch.empty_like(ids[0]) for _ in range(NS)]
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
@@ -329,7 +331,7 @@ def run_ours(args, wl):
 
     def h2d(k):  # step k's ids, pinned host -> device, on the copy stream
         with torch.cuda.stream(copy_stream):
-            if k >= NS:  # the slot's previous batch (k-3) was consumed by its forward
+            if k >= NS:  # the slot's previous batch was consumed by its forward
                 copy_stream.wait_event(consumed[k % NS])
             dev_ids[k % NS].copy_(host_ids[k % N_BATCHES], non_blocking=True)
             copied[k % NS].record(copy_stream)
@@ -337,25 +339,25 @@ def run_ours(args, wl):
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
 
     def e2e_steps(nsteps, marks=None):
-        # input pipelining: step k+2's H2D runs during step k, so a step's
+        # input pipelining: step k+depth+1's H2D runs during step k, so a
         # prefetch never waits on the link; every step still moves its own ids
         # host->device and reads its result back
-        h2d(0)
-        if nsteps > 1:
-            h2d(1)
+        tab.prefetch_drop()  # this loop primes its own pipeline
+        for k in range(min(nsteps, depth + 1)):
+            h2d(k)
+        for k in range(min(nsteps, depth)):
+            tab.prefetch(dev_ids[k % NS], offs, B, P, stream=copy_stream)
         res = None
         for k in range(nsteps):
             if marks is not None:
                 marks[k].record(stream)
             stream.wait_event(copied[k % NS])
-            if args.prefetch and k == 0:
-                tab.prefetch(dev_ids[0], offs, B, P, stream=copy_stream)
             o = tab.forward(dev_ids[k % NS], offs, B, P, out=out)
             consumed[k % NS].record(stream)
-            if args.prefetch and k + 1 < nsteps:
-                tab.prefetch(dev_ids[(k + 1) % NS], offs, B, P, stream=copy_stream)  # after its H2D copy
-            if k + 2 < nsteps:
-                h2d(k + 2)  # (after the prefetch above, which orders itself after the copy stream)
+            if depth and k + depth < nsteps:
+                tab.prefetch(dev_ids[(k + depth) % NS], offs, B, P, stream=copy_stream)  # after its H2D copy
+            if k + depth + 1 < nsteps:
+                h2d(k + depth + 1)  # (after the prefetch above, which orders itself after the copy stream)
             tab.backward(o, LR)
             # D2H of the step's result (per-table unique/miss counts) into a
             # pinned ring slot; decoded two steps later, like an async loss log
@@ -367,7 +369,7 @@ def run_ours(args, wl):
             res = tab.stats_collect(k % 4, per_table=True)
         return res
 
-    e2e_steps(max(args.warmup, 8))  # untimed: captures the graphs of this buffer rotation
+    e2e_steps(max(args.warmup, 12))  # untimed: captures the graphs of this buffer rotation
     barrier()
     torch.cuda.synchronize()
     torch.cuda._sleep(HEAD_START_CYCLES)
@@ -481,9 +483,10 @@ def run_ours(args, wl):
                    "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
                    "cache_rows": int(sum(ks)), "cache_bytes": int(sum(ks)) * D * 4, "cold_tier": wl["storage"],
                    "l2": "flushed between timed steps (256 MiB write outside the per-step events)",
-                   "step": ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD); pipelined: the next "
-                            "batch's dedup/hit-miss/host gather (ec_lookup_prefetch) overlaps this backward and "
-                            "is inside this step's window") if args.prefetch else
+                   "step": ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD); pipelined "
+                            f"(ec_lookup_prefetch depth {depth}): batch j+{depth}'s dedup/hit-miss and batch j+1's "
+                            "host-miss gather overlap this step and are inside its window, as is this step's "
+                            "host write-back") if depth else
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
                    "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
@@ -623,7 +626,9 @@ def main():
     ap.add_argument("--schedule-batches", type=int, default=32,
                     help="epoch length for the hot/normal scheduling measurement (0: skip)")
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
-                    help="unpipelined steps (default: ec_lookup_prefetch of the next batch overlaps this step)")
+                    help="unpipelined steps (default: ec_lookup_prefetch of later batches overlaps this step)")
+    ap.add_argument("--prefetch-depth", type=int, default=None,
+                    help="batches prefetched ahead (default 2 with the pinned-host tier, 1 with HBM)")
     ap.add_argument("--stream-priority", type=int, default=-1,
                     help="priority of the caller's stream (torch: -1 high, 0 low; engine side streams are low)")
     ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster", "table"], default=None)
@@ -631,6 +636,10 @@ def main():
     args = ap.parse_args()
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         args.prefetch = False  # ec_lookup_prefetch is single-rank (the exchange synchronises ranks per batch)
+    if args.prefetch_depth is None:
+        args.prefetch_depth = 2 if WORKLOADS[args.workload]["storage"] == "host" else 1
+    if not args.prefetch:
+        args.prefetch_depth = 0
     MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode)
     if args.warmup < 3:
         args.warmup = 3

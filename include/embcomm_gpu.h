@@ -361,7 +361,8 @@ int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t*
 /* Start the next batch while the current one finishes (single rank): its
  * dedup, hit/miss partition and pinned-host miss gather run on internal
  * streams into a second buffer set, overlapping the current backward; the
- * next ec_lookup_fwd with the same indices_dev consumes them.  Host-tier rows
+ * next ec_lookup_fwd with the same indices_dev consumes them (up to 2 batches
+ * may be pending; forwards consume them in prefetch order).  Host-tier rows
  * the current backward updates are refreshed in the prefetched copy, so
  * results equal the unpipelined sequence.  Stream-ordered on `stream`: it
  * starts after the work already enqueued there, so pass the stream that
@@ -372,6 +373,8 @@ int ec_lookup_prefetch(ec_tables t, const ec_batch* batch, void* stream);
 /* Make `stream` wait for a pending prefetch and for the deferred host-tier
  * write-back of the last backward (no-op without either). */
 int ec_lookup_prefetch_wait(ec_tables t, void* stream);
+/* Discard every pending prefetched batch (their buffer sets become free). */
+int ec_lookup_prefetch_drop(ec_tables t, void* stream);
 /* Backward of the last forward: grad_dev laid out like out_dev; applies
  * w <- w - lr * (sum of grads of every lookup of the row) to the cache copy
  * of cached rows and to the owning shard of the others (K6).  Single rank,

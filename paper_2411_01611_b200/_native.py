@@ -159,6 +159,7 @@ _SIGS = {
     "ec_lookup_bwd": [vp, vp, f32, vp],
     "ec_lookup_prefetch": [vp, P(Batch), vp],
     "ec_lookup_prefetch_wait": [vp, vp],
+    "ec_lookup_prefetch_drop": [vp, vp],
     "ec_trace_save_binary": [C.c_char_p, vp, u64, i64, u64],
     "ec_trace_open_binary": [C.c_char_p, P(vp)],
     "ec_trace_destroy": [vp],

@@ -255,11 +255,12 @@ Engine::~Engine() {
   if (ring_host) cudaFreeHost(ring_host);
   for (cudaEvent_t ev : ring_ev)
     if (ev) cudaEventDestroy(ev);
-  if (ev_release) cudaEventDestroy(ev_release);
+  for (BatchBufs& b : bb)
+    for (cudaEvent_t e : {b.ev_free, b.ev_ded, b.ev_pf})
+      if (e) cudaEventDestroy(e);
   if (ev_grad) cudaEventDestroy(ev_grad);
   if (ev_patch) cudaEventDestroy(ev_patch);
   if (ev_pfcall) cudaEventDestroy(ev_pfcall);
-  if (ev_pf) cudaEventDestroy(ev_pf);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
 }
@@ -318,9 +319,9 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
   // one dedup hash per batch-buffer set: a prefetched batch's dedup never
   // waits for the current batch's gather to clean the shared slots
-  hash.alloc(2 * hash_off[T]);
+  hash.alloc(kSets * hash_off[T]);
   EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
-  idcnt.alloc(2 * hash_off[T]);
+  idcnt.alloc(kSets * hash_off[T]);
   EC_CUDA(cudaMemset(idcnt.p, 0, idcnt.bytes()));
   const uint64_t N = max_n * T;
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
@@ -342,14 +343,19 @@ void Engine::create(const ec_tables_config& c) {
     b.part.alloc((N + kScanTile) / kScanTile + 1);
     EC_CUDA(cudaMemset(b.ctr.p, 0, b.ctr.bytes()));
   }
-  for (BatchBufs& b : bb) b.tstat.alloc(T);
+  for (BatchBufs& b : bb) {
+    b.tstat.alloc(T);
+    EC_CUDA(cudaEventCreateWithFlags(&b.ev_free, cudaEventDisableTiming));
+    EC_CUDA(cudaEventCreateWithFlags(&b.ev_ded, cudaEventDisableTiming));
+    EC_CUDA(cudaEventCreateWithFlags(&b.ev_pf, cudaEventDisableTiming));
+  }
   select(0);
   EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctr_host), counters_size(T) * sizeof(int), cudaHostAllocDefault));
   EC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ring_host), EC_STATS_SLOTS * counters_size(T) * sizeof(int),
                         cudaHostAllocDefault));
   for (cudaEvent_t& ev : ring_ev) EC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   tiles.alloc(max_tiles);
-  tdev_buf.alloc(2 * T);
+  tdev_buf.alloc(kSets * T);
   td_host.resize(T);
   for (uint32_t t = 0; t < T; ++t) {
     TableDev& d = td_host[t];
@@ -379,10 +385,8 @@ void Engine::create(const ec_tables_config& c) {
     EC_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, wb_prio));
   }
   EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
-  EC_CUDA(cudaEventCreateWithFlags(&ev_release, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
-  EC_CUDA(cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pfcall, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
@@ -390,13 +394,15 @@ void Engine::create(const ec_tables_config& c) {
 }
 
 void Engine::upload_tdev() {
-  std::vector<TableDev> both(td_host);
-  both.insert(both.end(), td_host.begin(), td_host.end());
-  for (uint32_t t = 0; t < T; ++t) {
-    both[T + t].hash += hash_off[T];
-    both[T + t].idcnt += hash_off[T];
-  }
-  EC_CUDA(cudaMemcpy(tdev_buf.p, both.data(), both.size() * sizeof(TableDev), cudaMemcpyHostToDevice));
+  std::vector<TableDev> all;
+  for (int k = 0; k < kSets; ++k)
+    for (uint32_t t = 0; t < T; ++t) {
+      TableDev d = td_host[t];
+      d.hash += k * hash_off[T];  // each set has its own dedup set and counters
+      d.idcnt += k * hash_off[T];
+      all.push_back(d);
+    }
+  EC_CUDA(cudaMemcpy(tdev_buf.p, all.data(), all.size() * sizeof(TableDev), cudaMemcpyHostToDevice));
 }
 
 void Engine::select(int i) {
@@ -422,8 +428,9 @@ void Engine::select(int i) {
 }
 
 uint64_t Engine::device_bytes() const {
-  return store_dev.bytes() + remap.bytes() + hash.bytes() + cache.bytes() + bb[0].bytes() + bb[1].bytes() +
-         tiles.bytes() + stiles.bytes() + cache_ids.bytes() + cache_tab.bytes() +
+  uint64_t sets = 0;
+  for (const BatchBufs& b : bb) sets += b.bytes();
+  return store_dev.bytes() + remap.bytes() + hash.bytes() + idcnt.bytes() + cache.bytes() + sets + tiles.bytes() + stiles.bytes() + cache_ids.bytes() + cache_tab.bytes() +
          exch_bytes();
 }
 
@@ -539,7 +546,7 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   bool same = have_geom && b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed;
   for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
   if (same) return;
-  if (bb[cur ^ 1].pending) drop_prefetch(st);
+  drop_prefetch(st);
   clear_graphs();
   ++geom_version;
   geom_off.assign(b.table_offsets_host, b.table_offsets_host + T + 1);
@@ -713,14 +720,16 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
 template <int VEC>
 void Engine::enqueue_host_writeback(float lr) {
   EC_CUDA(cudaStreamWaitEvent(side2, ev_grad, 0));
-  const BatchBufs& nx = bb[cur ^ 1];
-  const bool patch = nx.pending;
-  const TableDev* nxt_td = tdev_buf.p + static_cast<size_t>(cur ^ 1) * T;
+  // the next batch's copies of host rows, if its gather already ran
+  const int h = head_pending();
+  const bool patch = h >= 0 && bb[h].gathered;
+  const BatchBufs& nx = bb[patch ? h : cur];
+  const TableDev* nxt_td = tdev_buf.p + static_cast<size_t>(patch ? h : cur) * T;
   if (patch && host_tma()) {
     // one kernel writes the rows back and refreshes the prefetched batch's
     // copies: it starts once that batch's host gather is done (host reads and
     // writes share the link's request rate, so the wait costs no link time)
-    EC_CUDA(cudaStreamWaitEvent(side2, ev_pf, 0));
+    EC_CUDA(cudaStreamWaitEvent(side2, nx.ev_pf, 0));
     PhaseScope ph(prof, kPhaseApplyHost, side2);
     k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
                                                                       ugrad.p, lr, rank, world, nxt_td, nx.usrc.p,
@@ -743,7 +752,7 @@ void Engine::enqueue_host_writeback(float lr) {
   EC_CUDA(cudaEventRecord(ev_side2, side2));
   if (patch) {
     EC_CUDA(cudaStreamWaitEvent(side, ev_grad, 0));
-    EC_CUDA(cudaStreamWaitEvent(side, ev_pf, 0));
+    EC_CUDA(cudaStreamWaitEvent(side, nx.ev_pf, 0));
     // (the prefetched ids are found in the pending set's hash)
     k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(nxt_td, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
                                                                       ugrad.p, lr, rank, world, nx.usrc.p, nx.urows.p);
@@ -808,19 +817,58 @@ void Engine::forward_prologue(const ec_batch& b, float* out, cudaStream_t st) {
   out_ptr = out;
 }
 
+int Engine::head_pending() const {
+  int h = -1;
+  for (int k = 0; k < kSets; ++k)
+    if (bb[k].pending && (h < 0 || bb[k].seq < bb[h].seq)) h = k;
+  return h;
+}
+
+int Engine::free_set() const {
+  for (int k = 1; k < kSets; ++k) {
+    const int s = (cur + k) % kSets;
+    if (!bb[s].pending) return s;
+  }
+  return -1;
+}
+
+// Host-miss gather of a prefetched set whose dedup ran earlier (prefetch
+// depth >= 2): on `side` once its dedup is done and every host write-back
+// enqueued so far has landed -- so it reads current rows; only the backward
+// still to come before its forward is patched in (enqueue_host_writeback).
+void Engine::launch_pending_gather(int s) {
+  BatchBufs& b = bb[s];
+  if (b.gathered) return;
+  EC_CUDA(cudaStreamWaitEvent(side, b.ev_ded, 0));
+  EC_CUDA(cudaStreamWaitEvent(side, ev_side2, 0));
+  const int saved = cur;
+  select(s);
+  try {
+    EC_DISPATCH_VEC(launch_gather_host, side);
+  } catch (...) {
+    select(saved);
+    throw;
+  }
+  select(saved);
+  EC_CUDA(cudaEventRecord(b.ev_pf, side));
+  b.gathered = true;
+}
+
 void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   if (in_group) invalid("this rank belongs to a loopback group: use ec_group_lookup_fwd");
   forward_prologue(b, out, st);
-  BatchBufs& nx = bb[cur ^ 1];
-  if (nx.pending) {
+  const int h = head_pending();
+  if (h >= 0) {
+    BatchBufs& nx = bb[h];
     if (nx.indices == b.indices_dev && nx.geom_version == geom_version) {
       // dedup, hit/miss and host-miss gather already ran (ec_lookup_prefetch)
       nx.pending = false;
-      // everything enqueued so far (last batch's backward and its host-tier
-      // joins) used the outgoing set: the next prefetch may reuse it after this
-      EC_CUDA(cudaEventRecord(ev_release, st));
-      select(cur ^ 1);
-      EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
+      if (!nx.gathered) launch_pending_gather(h);  // (host tier, gather not started yet)
+      // everything enqueued so far (the outgoing batch's backward and host-tier
+      // joins) used the outgoing set: a prefetch may reuse it after this
+      EC_CUDA(cudaEventRecord(bb[cur].ev_free, st));
+      select(h);
+      EC_CUDA(cudaStreamWaitEvent(st, nx.ev_pf, 0));
       if (storage == EC_STORAGE_HOST) EC_CUDA(cudaStreamWaitEvent(st, ev_patch, 0));
       consuming_prefetch = true;
       try {
@@ -834,6 +882,10 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
         throw;
       }
       consuming_prefetch = false;
+      // the next prefetched batch's host gather starts now: first on the host
+      // link in this step, reading rows every earlier write-back has updated
+      const int h2 = head_pending();
+      if (h2 >= 0 && storage == EC_STORAGE_HOST) launch_pending_gather(h2);
       have_fwd = true;
       return;
     }
@@ -852,11 +904,14 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   have_fwd = true;
 }
 
-// Start the next batch early: dedup, hit/miss partition and (pinned-host
-// tier) the miss gather run on the prefetch/side streams into the other
-// buffer set, overlapping the current batch's backward.  Rows the current
-// backward then writes to the host tier are patched into the prefetched copy
-// (k_apply_host).  Single rank only; needs the current batch geometry.
+// Start a later batch early (single rank; the current batch geometry): its
+// dedup and hit/miss partition run on the prefetch stream into a free buffer
+// set.  Pinned-host tier: the next batch in line also gathers its host misses
+// right away; a batch further ahead (prefetch depth 2) gathers them when the
+// forward before it starts, so the host link carries that gather first in the
+// step.  Rows a backward writes to the host tier after a gather are patched
+// into the gathered copy.  Up to kSets-1 batches may be pending; forwards
+// consume them in prefetch order.
 void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   if (in_group || world > 1) invalid("prefetch is single-rank only");
   if (!have_geom || !b.indices_dev || !b.table_offsets_host) invalid("prefetch needs a batch with the current geometry");
@@ -865,48 +920,57 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   for (uint32_t t = 0; same && t <= T; ++t) same = geom_off[t] == b.table_offsets_host[t];
   if (!same) invalid("prefetch needs the geometry (offsets, batch size, pooling, bag offsets) of the last forward");
   use_device(device);
-  if (bb[cur ^ 1].pending) drop_prefetch(st);
-  // the other set (own hash, cleaned by its last gather) is free once the work
-  // recorded at its release has run; a never-used set has no release to wait for
-  EC_CUDA(cudaStreamWaitEvent(pstream, ev_release, 0));
+  const int s = free_set();
+  if (s < 0) invalid("prefetch: " + std::to_string(kSets - 1) + " batches already pending (consume one first)");
+  const bool next_in_line = head_pending() < 0;
+  // the set (own hash, emptied by its last pool/gather) is free once its last
+  // batch's main-stream work and host-tier write-back have run
+  EC_CUDA(cudaStreamWaitEvent(pstream, bb[s].ev_free, 0));
   join_host_writes(pstream);
   // stream-ordered like every call: work the caller enqueued on `st` before
   // this prefetch (e.g. the copy that produced these indices) comes first
   EC_CUDA(cudaEventRecord(ev_pfcall, st));
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_pfcall, 0));
+  const bool gather_now = storage == EC_STORAGE_HOST && next_in_line;
   const int saved = cur;
-  select(cur ^ 1);
+  select(s);
   try {
-    // dedup + hit/miss, then the host-miss gather, in stream order on pstream:
-    // one graph launch per prefetch (its host cost sits on every step)
-    const GraphKey key{4, b.indices_dev, b.bag_offsets_dev, nullptr, 0};
+    // dedup + hit/miss (+ the host-miss gather when next in line), in stream
+    // order on pstream: one graph launch per prefetch
+    const GraphKey key{gather_now ? 4 : 5, b.indices_dev, b.bag_offsets_dev, nullptr, 0};
     run_maybe_graphed(key, pstream, [&] {
       enqueue_dedup_partition(b.indices_dev, pstream);
-      if (storage == EC_STORAGE_HOST) {
-        EC_DISPATCH_VEC(launch_gather_host, pstream);
-      }
+      if (gather_now) EC_DISPATCH_VEC(launch_gather_host, pstream);
     });
-    EC_CUDA(cudaEventRecord(ev_pf, pstream));
+    EC_CUDA(cudaEventRecord(bb[s].ev_ded, pstream));
+    EC_CUDA(cudaEventRecord(bb[s].ev_pf, pstream));
   } catch (...) {
     select(saved);
     throw;
   }
-  bb[cur].pending = true;
-  bb[cur].indices = b.indices_dev;
-  bb[cur].geom_version = geom_version;
+  BatchBufs& nb = bb[s];
+  nb.pending = true;
+  nb.gathered = storage != EC_STORAGE_HOST || gather_now;
+  nb.seq = ++pf_seq;
+  nb.indices = b.indices_dev;
+  nb.geom_version = geom_version;
   select(saved);
 }
 
+// Drop every pending prefetch (a forward of another batch, a new geometry).
 void Engine::drop_prefetch(cudaStream_t st) {
-  BatchBufs& nx = bb[cur ^ 1];
-  if (!nx.pending) return;
-  EC_CUDA(cudaStreamWaitEvent(st, ev_pf, 0));
-  join_host_writes(st);
-  k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev_buf.p + static_cast<size_t>(cur ^ 1) * T, T, nx.ctr.p,
-                                                      nx.utab.p, nx.uslot.p);
-  launched();
-  EC_CUDA(cudaEventRecord(ev_release, st));  // the set is free again
-  nx.pending = false;
+  for (int k = 0; k < kSets; ++k) {
+    BatchBufs& nx = bb[k];
+    if (!nx.pending) continue;
+    EC_CUDA(cudaStreamWaitEvent(st, nx.gathered ? nx.ev_pf : nx.ev_ded, 0));
+    join_host_writes(st);
+    k_clear_hash<<<sm_count(device) * 2, 256, 0, st>>>(tdev_buf.p + static_cast<size_t>(k) * T, T, nx.ctr.p, nx.utab.p,
+                                                        nx.uslot.p);
+    launched();
+    EC_CUDA(cudaEventRecord(nx.ev_free, st));  // the set is free again
+    nx.pending = false;
+    nx.gathered = false;
+  }
 }
 
 template <int VEC>
@@ -1093,7 +1157,8 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   if (world == 1) {
     uint32_t lr_bits;
     std::memcpy(&lr_bits, &lr, sizeof(lr_bits));
-    const GraphKey key{bb[cur ^ 1].pending ? 3 : 1, grad, bag_off, out_ptr, lr_bits};
+    const int h = head_pending();
+    const GraphKey key{h >= 0 && bb[h].gathered ? 3 : 1, grad, bag_off, out_ptr, lr_bits};
     run_maybe_graphed(key, st, [&] { scatter_and_apply_local(grad, lr, st); });
     // host-tier write-back left running: it overlaps the next forward and is
     // joined by whatever next reuses this set or the host tier
@@ -1354,11 +1419,20 @@ int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t*
   });
 }
 
+int ec_lookup_prefetch_drop(ec_tables t, void* stream) {
+  return guard([&] {
+    Engine& e = E(t);
+    use_device(e.device);
+    e.drop_prefetch(as_stream(stream));
+  });
+}
+
 int ec_lookup_prefetch_wait(ec_tables t, void* stream) {
   return guard([&] {
     Engine& e = E(t);
     use_device(e.device);
-    if (e.bb[e.cur ^ 1].pending) EC_CUDA(cudaStreamWaitEvent(as_stream(stream), e.ev_pf, 0));
+    for (BatchBufs& b : e.bb)
+      if (b.pending) EC_CUDA(cudaStreamWaitEvent(as_stream(stream), b.gathered ? b.ev_pf : b.ev_ded, 0));
     e.join_host_writes(as_stream(stream));
   });
 }

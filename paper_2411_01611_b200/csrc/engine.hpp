@@ -67,6 +67,11 @@ struct BatchBufs {
   const uint32_t* indices = nullptr;  // batch held by a pending prefetch
   uint64_t geom_version = 0;
   bool pending = false;               // prefetched, not yet consumed by forward
+  bool gathered = false;              // its pinned-host miss gather was launched (ev_pf)
+  uint64_t seq = 0;                   // prefetch order (the smallest pending seq is consumed next)
+  cudaEvent_t ev_free = nullptr;      // main-stream work of its last batch done (set reusable)
+  cudaEvent_t ev_ded = nullptr;       // its prefetch's dedup done
+  cudaEvent_t ev_pf = nullptr;        // its prefetch complete (dedup + host gather)
   bool lists = false;                 // its forward built the unique-grouped gradient lists
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
@@ -157,11 +162,16 @@ struct Engine {
   float synth_scale = 0.f;
   bool synth_valid = false;
 
-  // Per-batch state, double-buffered so the next batch can be prefetched
-  // (dedup, hit/miss, host-miss gather) while the current one runs backward.
-  // The View members below point at the selected set (select()).
-  BatchBufs bb[2];
+  // Per-batch state in a ring of kSets buffer sets, so up to kSets-1 next
+  // batches can be prefetched (dedup, hit/miss, host-miss gather) while the
+  // current one runs.  The View members below point at the selected set.
+  static constexpr int kSets = 3;
+  BatchBufs bb[kSets];
   int cur = 0;
+  uint64_t pf_seq = 0;
+  int head_pending() const;  // the pending set the next forward consumes, or -1
+  int free_set() const;      // a set neither current nor pending, or -1
+  void launch_pending_gather(int s);
   View<uint32_t> slot_of, inv, uniq, uslot, missq;
   View<int32_t> usrc;
   View<uint16_t> utab;
@@ -205,7 +215,7 @@ struct Engine {
   void select(int i);
   DevBuf<Tile> tiles;
   DevBuf<int4> stiles;                // scatter tiles (table, bag lo, bag hi, -)
-  DevBuf<TableDev> tdev_buf;  // two copies of the table descriptors, one per batch-buffer set (own hash each)
+  DevBuf<TableDev> tdev_buf;  // kSets copies of the table descriptors, one per batch-buffer set (own hash each)
   View<TableDev> tdev;        // the selected set's copy
   std::vector<TableDev> td_host;
   int ntiles = 0, nstiles = 0, tail_lo = 0;
@@ -220,7 +230,7 @@ struct Engine {
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
   cudaEvent_t ev_pfcall = nullptr;   // caller's stream at the prefetch call
 
-  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr, ev_release = nullptr, ev_pf = nullptr,
+  cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr,
               ev_grad = nullptr, ev_patch = nullptr;
   uint64_t geom_version = 0;
   bool consuming_prefetch = false;

@@ -221,6 +221,10 @@ class EmbeddingTables:
                                              out.data_ptr(), _stream_ptr(torch, self.device)))
         return out
 
+    def prefetch_drop(self):
+        """Discard pending prefetched batches."""
+        check(N.lib().ec_lookup_prefetch_drop(self._h, _stream_ptr(self.torch, self.device)))
+
     def prefetch_wait(self):
         """Make the current stream wait for a pending prefetch and the last
         backward's deferred host-tier write-back."""

@@ -252,11 +252,13 @@ def test_async_stats_ring_matches_sync_stats(ec, torch):
     tab.close()
 
 
-@pytest.mark.parametrize("storage,graphs", [("host", False), ("host", True), ("hbm", True)])
-def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
-    """fwd(j) -> prefetch(j+1) -> bwd(j) gives the same outputs and final rows
-    as the unpipelined fwd/bwd sequence (cold rows updated by bwd(j) that
-    batch j+1 already gathered are refreshed)."""
+@pytest.mark.parametrize("storage,graphs,depth", [("host", False, 1), ("host", True, 1), ("hbm", True, 1),
+                                                 ("host", False, 2), ("host", True, 2), ("hbm", True, 2)])
+def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs, depth):
+    """fwd(j) -> prefetch(j+depth) -> bwd(j) gives the same outputs and final
+    rows as the unpipelined fwd/bwd sequence: cold rows updated by bwd(j) that
+    batch j+1 already gathered are refreshed; a batch prefetched two ahead
+    gathers its host rows only after every earlier write-back."""
     rows, D, B, P = [3000, 800, 50], 8, 128, 3
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.0)) for r in rows]
     caches = [d.top_ids(k) for d, k in zip(dists, [30, 10, 5])]
@@ -275,8 +277,10 @@ def test_prefetch_pipeline_matches_sequential(ec, torch, storage, graphs):
         for j in range(nb):
             o = tab.forward(batches[j], offs, B, P)
             outs.append(o.clone())
-            if pipelined and j + 1 < nb:
-                tab.prefetch(batches[j + 1], offs, B, P)
+            if pipelined:
+                # keep `depth` batches in flight: after batch 0, prefetch up to j+depth
+                for k in range(j + 1 if j == 0 else j + depth, min(nb, j + depth + 1)):
+                    tab.prefetch(batches[k], offs, B, P)
             tab.backward(grads[j], 0.5)
         torch.cuda.synchronize()
         final = [tab.read_rows(t, np.arange(rows[t])) for t in range(len(rows))]
