@@ -333,7 +333,7 @@ def run_ours(args, wl):
         with torch.cuda.stream(copy_stream):
             if k >= NS:  # the slot's previous batch was consumed by its forward
                 copy_stream.wait_event(consumed[k % NS])
-            dev_ids[k % NS].copy_(host_ids[k % N_BATCHES], non_blocking=True)
+            ec.copy_async(dev_ids[k % NS], host_ids[k % N_BATCHES], copy_stream)
             copied[k % NS].record(copy_stream)
 
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]

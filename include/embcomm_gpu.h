@@ -234,6 +234,9 @@ int ec_trace_open_binary(const char* path, ec_trace* out);  /* mapped read-only 
 void ec_trace_destroy(ec_trace t);
 int ec_trace_info(ec_trace t, uint64_t* num_samples, int64_t* num_features, uint64_t* vocab);
 int ec_trace_ids(ec_trace t, const uint32_t** ids_host);  /* valid until ec_trace_destroy */
+/* stream-ordered copy between UVA addresses (pinned host <-> device), e.g. a
+ * step's ids onto the GPU: cudaMemcpyAsync(cudaMemcpyDefault) in one call */
+int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 /* samples [first, first+count) -> ids_dev (count*d ids) through pinned
  * double-buffered staging on `stream`; returns when the copies are done */
 int ec_trace_upload(ec_trace t, uint64_t first, uint64_t count, uint32_t* ids_dev, void* stream);

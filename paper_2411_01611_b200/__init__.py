@@ -37,7 +37,7 @@ __all__ = [
     "coalesced_epoch_cost", "cached_epoch_cost", "DeviceModel", "max_batch_size", "MarginalReport",
     "delta_comm", "CachePlan", "optimal_cache_size_scan", "optimal_cache_size_search", "memory_io_proxy",
     "place_topk_global", "expected_unique_many", "cost_curve", "SplitMix64", "substream_seed", "DiscreteSampler", "sample_batch", "Stat",
-    "SimResult", "measure_unique", "simulate_epoch", "Trace", "BinaryTrace", "classify_samples", "build_schedule",
+    "SimResult", "measure_unique", "simulate_epoch", "Trace", "BinaryTrace", "copy_async", "classify_samples", "build_schedule",
     "SampleClasses", "BatchSchedule", "SkewTable", "build_skew_table", "estimate_distribution", "EmbeddingTables", "EmbeddingGroup", "shard_rows", "exchange_plan",
 ]
 
@@ -488,6 +488,18 @@ class Trace:
         """Map a binary trace (validated like parse_trace); .trace() views it
         as a Trace without copying."""
         return BinaryTrace(path)
+
+
+def copy_async(dst, src, stream=None) -> None:
+    """dst.copy_(src, non_blocking=True) for contiguous same-size tensors (pinned
+    host <-> device) through one ec_copy_async call: an input pipeline's copy
+    without the framework dispatch cost."""
+    import torch
+    nbytes = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() != nbytes or not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValidationError("copy_async needs contiguous tensors of equal byte size")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    check(N.lib().ec_copy_async(dst.data_ptr(), src.data_ptr(), nbytes, s.cuda_stream))
 
 
 class BinaryTrace:

@@ -163,20 +163,23 @@ int Engine::host_grid() const {
   }();
   if (env > 0) return env;
   // TMA path: the copy engine holds the row reads, so CTAs are cheap -- 2 per
-  // SM keep 16 KiB each in flight (measured best of 74/148/296).
-  // LSU path: 32 CTAs x 256 threads keep ~8k row reads in flight, enough to
-  // saturate the host link for 64-256 B rows, while leaving the L2/HBM request
-  // queues to the main-stream kernels (measured: 8 CTAs starve the link, >= 148
-  // slow the concurrent HBM gather 4x)
-  return host_tma() ? sm_count(device) * 2 : 32;
+  // SM keep 16 KiB each in flight.
+  // LSU path (default): 16 CTAs x 256 threads keep ~4k row reads in flight --
+  // the host link is request-rate bound (~215 M rows/s, profiles/hostlink_probe.txt)
+  // and deeper queues only stall the concurrent pool/dedup/scatter.  Measured
+  // on the pipelined Kaggle step: 12/16/24/32 CTAs 0.099-0.103/0.100-0.104/
+  // 0.103-0.110/0.107-0.113 ms; 8 CTAs starve the link (0.109), TMA at 296
+  // CTAs 0.105-0.107 with the pool slowed 14 -> 30 us.
+  return host_tma() ? sm_count(device) * 2 : 16;
 }
-// Host-link row traffic goes through the TMA bulk-copy engine unless
-// EC_HOST_TMA=0: its reads do not occupy the LSU/L1 miss queues, so the
-// concurrent HBM gather runs at its isolated speed (35 -> 14 us, Kaggle).
+// Host-link row traffic goes through SM loads/stores (k_gather_host /
+// k_apply_host) unless EC_HOST_TMA=1 selects the TMA bulk-copy kernels; with
+// the single-rank fused path there is no concurrent HBM gather to protect, and
+// a bounded number of in-flight rows interferes least with the pipeline.
 bool Engine::host_tma() {
   static const bool on = [] {
     const char* v = std::getenv("EC_HOST_TMA");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }
@@ -261,6 +264,7 @@ Engine::~Engine() {
   if (ev_grad) cudaEventDestroy(ev_grad);
   if (ev_patch) cudaEventDestroy(ev_patch);
   if (ev_pfcall) cudaEventDestroy(ev_pfcall);
+  if (ev_gate) cudaEventDestroy(ev_gate);
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   destroy_comm();
 }
@@ -388,6 +392,7 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pfcall, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_gate, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
@@ -833,12 +838,15 @@ int Engine::free_set() const {
 }
 
 // Host-miss gather of a prefetched set whose dedup ran earlier (prefetch
-// depth >= 2): on `side` once its dedup is done and every host write-back
+// depth >= 2): on `side` once its dedup is done, every host write-back
 // enqueued so far has landed -- so it reads current rows; only the backward
-// still to come before its forward is patched in (enqueue_host_writeback).
+// still to come before its forward is patched in (enqueue_host_writeback) --
+// and the caller's stream has reached this call (`gate`: the gather belongs to
+// the step that starts here, not to the gap before it).
 void Engine::launch_pending_gather(int s) {
   BatchBufs& b = bb[s];
   if (b.gathered) return;
+  EC_CUDA(cudaStreamWaitEvent(side, ev_gate, 0));  // recorded by the forward at its start
   EC_CUDA(cudaStreamWaitEvent(side, b.ev_ded, 0));
   EC_CUDA(cudaStreamWaitEvent(side, ev_side2, 0));
   const int saved = cur;
@@ -863,6 +871,7 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     if (nx.indices == b.indices_dev && nx.geom_version == geom_version) {
       // dedup, hit/miss and host-miss gather already ran (ec_lookup_prefetch)
       nx.pending = false;
+      EC_CUDA(cudaEventRecord(ev_gate, st));  // this step starts here
       if (!nx.gathered) launch_pending_gather(h);  // (host tier, gather not started yet)
       // everything enqueued so far (the outgoing batch's backward and host-tier
       // joins) used the outgoing set: a prefetch may reuse it after this

@@ -229,6 +229,7 @@ struct Engine {
 
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
   cudaEvent_t ev_pfcall = nullptr;   // caller's stream at the prefetch call
+  cudaEvent_t ev_gate = nullptr;     // caller's stream at the forward that starts a pending gather
 
   cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr,
               ev_grad = nullptr, ev_patch = nullptr;

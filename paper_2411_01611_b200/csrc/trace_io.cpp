@@ -109,6 +109,16 @@ struct ec_trace_s {
 
 extern "C" {
 
+// Stream-ordered copy between any two UVA addresses (pinned host <-> device):
+// the input-pipeline primitive of a training loop, with one call's host cost.
+int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+  return guard([&] {
+    if (!bytes) return;
+    if (!dst || !src) invalid("null argument");
+    EC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  });
+}
+
 int ec_trace_save_binary(const char* path, const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
                          uint64_t vocab) {
   return guard([&] {

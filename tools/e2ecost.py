@@ -40,7 +40,7 @@ def h2d(k):
     with torch.cuda.stream(cs):
         if k >= NS:
             cs.wait_event(consumed[k % NS])
-        dev_ids[k % NS].copy_(host_ids[k % NB], non_blocking=True)
+        ec.copy_async(dev_ids[k % NS], host_ids[k % NB], cs)
         copied[k % NS].record(cs)
 
 

@@ -1,5 +1,5 @@
 """Per-kernel timeline of pipelined bench steps (profiling on: direct launches,
-CUDA events on each kernel's own stream).  usage: python tools/timeline.py [workload] [steps]"""
+CUDA events on each kernel's own stream).  usage: python tools/timeline.py [workload] [steps] [prefetch depth]"""
 import os
 import sys
 
@@ -12,6 +12,7 @@ import paper_2411_01611_b200 as ec  # noqa: E402
 
 wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "kaggle"]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+depth = int(sys.argv[3]) if len(sys.argv) > 3 else (2 if wl["storage"] == "host" else 1)
 torch.cuda.set_device(0)
 torch.cuda.set_stream(torch.cuda.Stream())
 tab, dists, caches, ks = bench.build_tables(ec, torch, wl, 0, 1, 0)
@@ -23,24 +24,28 @@ NB = bench.N_BATCHES
 cs = torch.cuda.Stream()  # input stream (as in bench.py): prefetches order after it only
 
 
-def step(j):
+def step(j, first=False):
     o = tab.forward(ids[j % NB], offs, B, P, out=out)
-    tab.prefetch(ids[(j + 1) % NB], offs, B, P, stream=cs)
+    for k in (range(1, depth + 1) if first else [depth]):
+        tab.prefetch(ids[(j + k) % NB], offs, B, P, stream=cs)
     tab.backward(o, bench.LR)
     tab.prefetch_wait()
 
 
 for j in range(4):
-    step(j)
+    step(j, first=j == 0)
 torch.cuda.synchronize()
 tab.profile(True)
 tab.profile_timeline()
-for j in range(steps):
+for j in range(4, 4 + steps):
     flush.fill_(float(j))
     step(j)
 torch.cuda.synchronize()
 tl = tab.profile_timeline()
 tab.profile(False)
+if os.environ.get("TL_ALL"):
+    for k, s0, e0 in sorted(tl, key=lambda r: r[1]):
+        print(f"  {k:22s} {1e3 * s0:9.1f} .. {1e3 * e0:9.1f} us")
 # step boundaries: each step's pool starts its forward
 starts = [s for (k, s, e) in tl if k == "k_pool"]
 for i in range(len(starts) - 2, len(starts)):
