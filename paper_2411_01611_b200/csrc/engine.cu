@@ -377,17 +377,9 @@ void Engine::create(const ec_tables_config& c) {
   }
   upload_tdev();
   select(cur);
-  {
-    // stream priorities (lower number = higher priority); EC_PRIO="prefetch,side2"
-    // overrides the defaults for experiments
-    int lo = 0, hi = 0;
-    EC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    int pf_prio = lo, wb_prio = lo;
-    if (const char* v = std::getenv("EC_PRIO")) std::sscanf(v, "%d,%d", &pf_prio, &wb_prio);
-    EC_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
-    EC_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, pf_prio));
-    EC_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, wb_prio));
-  }
+  EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  EC_CUDA(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
+  EC_CUDA(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side2, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
