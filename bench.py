@@ -55,6 +55,7 @@ SEED = 20241101
 N_BATCHES = 4          # distinct batches cycled through the timed steps
 FLUSH_BYTES = 256 << 20  # > 126 MB L2, written between timed steps
 HEAD_START_CYCLES = 2_000_000  # ~1 ms device sleep before a timed loop (see run_ours)
+HOST_LINK_ROWS_PER_S = 215e6  # measured random-row request rate of the pinned-host link (hostlink_bench)
 LR = 0.01
 MODES = {}  # kernel-variant overrides for experiments (--dedup-mode / --scatter-mode)
 
@@ -463,6 +464,7 @@ def run_ours(args, wl):
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(dom)
     step_alg = sum(mean_bytes.values())
+    link_ms = sum(phases[k]["ms_per_call"] for k in ("k_gather_host", "k_apply_host") if k in phases)
 
     s0 = stats[0]
     res = {
@@ -502,6 +504,16 @@ def run_ours(args, wl):
                      "traffic_source": (f"profiles/{args.workload}_traffic.json (ncu --set full, dram read+write "
                                         "bytes per launch)") if traffic else None,
                      "peak_source": peak_src},
+        # the pinned-host tier's bound: the host link serves ~215 M row requests/s
+        # (reads and writes share it; tools/hostlink_bench.cu, profiles/hostlink_probe.txt)
+        "host_link": ({"bound": "host-link request rate", "rows_per_step": int(2 * s0["miss_rows"]),
+                       "achieved_rows_per_s": round(2 * s0["miss_rows"] / (link_ms * 1e-3), 1),
+                       "peak_rows_per_s": HOST_LINK_ROWS_PER_S,
+                       "frac": round(2 * s0["miss_rows"] / (link_ms * 1e-3) / HOST_LINK_ROWS_PER_S, 3),
+                       "link_ms_per_step": round(link_ms, 5), "share_of_step": round(link_ms / ms, 3),
+                       "note": "host-miss gather + write-back kernel times per step (live events), "
+                               "peak measured with random 64 B rows on this pool"}
+                      if wl["storage"] == "host" and link_ms else None),
         "step_alg_bytes": int(step_alg),
         "step_alg_gbs": round(step_alg / (ms * 1e-3) / 1e9, 1),
         "phases": phases,
