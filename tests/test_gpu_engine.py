@@ -372,3 +372,34 @@ def test_cluster_dedup_every_width(ec, torch, ref, mode, n_max):
                     ref=ref)  # (one bag of up to 64K rows: pooled sums are covered by the other tests)
         tab.backward(torch.zeros(B, len(rows) * D, device="cuda"), 0.0)
     tab.close()
+
+
+def test_copy_async_and_prefetch_drop(ec, torch):
+    """ec_copy_async moves pinned host ids to the device in stream order; a
+    dropped prefetch frees its set and the next forward recomputes the batch."""
+    rows, D, B = [500, 40], 8, 64
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    ids, offs = make_ids(ec, torch, dists, [B] * 2, 31)
+    host = ids.cpu().pin_memory()
+    dev = torch.empty_like(ids)
+    s = torch.cuda.Stream()
+    ec.copy_async(dev, host, s)
+    s.synchronize()
+    assert torch.equal(dev, ids)
+    with pytest.raises(ec.ValidationError):
+        ec.copy_async(dev[:-1], host, s)
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=B, max_batch_size=B)
+    tab.init_synthetic(1, 0.1)
+    ref_out = tab.forward(ids, offs, B, 1).clone()
+    ids2, _ = make_ids(ec, torch, dists, [B] * 2, 32)
+    tab.prefetch(ids2, offs, B, 1)
+    tab.prefetch(ids, offs, B, 1)
+    with pytest.raises(ec.ValidationError):
+        tab.prefetch(ids2, offs, B, 1)  # two batches already pending
+    tab.prefetch_drop()
+    out = tab.forward(ids, offs, B, 1)  # recomputed, not consumed out of order
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref_out)
+    u, _ = O.dedup(ids.cpu().numpy().view(np.uint32)[:B])
+    assert (tab.export_unique(0) == u).all()
+    tab.close()
