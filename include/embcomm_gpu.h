@@ -443,6 +443,25 @@ int ec_group_create(ec_tables* members, int n, ec_group* out);
 void ec_group_destroy(ec_group g);
 int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs_dev, void* stream);
 int ec_group_lookup_bwd(ec_group g, const float* const* grads_dev, float lr, void* stream);
+/* Switch a group to the peer-memory exchange (enable != 0): remote rows are
+ * loaded straight from the owner's shard inside the gather kernel, owner
+ * updates are atomics into the owner's rows, hot-row gradient lists are
+ * published and applied in rank order, and the ranks meet at device-side
+ * barriers (flag words) instead of copies.  HBM-resident shards only.  The
+ * same kernels run across processes after ec_tables_p2p_export/import. */
+int ec_group_set_p2p(ec_group g, int enable);
+
+/* Multi-process peer-memory exchange (one process per GPU on one NVLink
+ * domain).  Replaces the NCCL all-to-all exchange of
+ * core/src/dist_embedding.cpp (forward :70-136, backward :138-206) with loads
+ * and atomics over NVLink.  export: this rank's peer-visible allocations as
+ * CUDA IPC handles (blob == NULL -> *len only); the caller all-gathers the
+ * blobs (rank-major, *len bytes each) and passes them to import, after which
+ * ec_lookup_fwd/bwd use the peer path (no ec_tables_set_comm needed).  Every
+ * rank must call fwd/bwd the same number of times: each step ends at a
+ * device-side barrier. */
+int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len);
+int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len);
 
 #ifdef __cplusplus
 }

@@ -601,16 +601,6 @@ void Engine::set_geometry(const ec_batch& b, cudaStream_t st) {
   have_geom = true;
 }
 
-#define EC_DISPATCH_VEC(FN, ...)                                                  \
-  switch (D / 4) {                                                                \
-    case 1: FN<1>(__VA_ARGS__); break;                                            \
-    case 2: FN<2>(__VA_ARGS__); break;                                            \
-    case 4: FN<4>(__VA_ARGS__); break;                                            \
-    case 8: FN<8>(__VA_ARGS__); break;                                            \
-    case 16: FN<16>(__VA_ARGS__); break;                                          \
-    case 32: FN<32>(__VA_ARGS__); break;                                          \
-    default: invalid("dim must be 4, 8, 16, 32, 64 or 128 for the lookup kernels"); \
-  }
 
 // K3 for rows this rank holds: pinned-host misses on the side stream, cache
 // hits and local-HBM misses on the main stream.
@@ -629,7 +619,8 @@ void Engine::fwd_gather_local(cudaStream_t st) {
   if (fused()) return;  // the pool reads cached / HBM rows where they are
   PhaseScope ph(prof, kPhaseGather, st);
   k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
-                                              ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+                                              ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world,
+                                              p2p_peers(), p2p_shard_off());
   launched();
 }
 
@@ -896,6 +887,12 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   if (world == 1) {
     const GraphKey key{0, b.indices_dev, b.bag_offsets_dev, out, 0};
     run_maybe_graphed(key, st, [&] { enqueue_forward(b.indices_dev, st); });
+  } else if (p2p_on()) {
+    p2p_fwd_begin(st);  // every rank applied the previous step
+    enqueue_dedup_partition(b.indices_dev, st);
+    gather_local(st);  // K4 fused: remote misses are loads from their owners' shards
+    p2p_signal(2, st);
+    pool(st);
   } else {
     enqueue_dedup_partition(b.indices_dev, st);
     gather_local(st);
@@ -988,6 +985,10 @@ void Engine::launch_gather_host(cudaStream_t s) {
 }
 
 void Engine::gather_local(cudaStream_t st) { EC_DISPATCH_VEC(fwd_gather_local, st); }
+void Engine::scatter_grads(const float* grad, cudaStream_t st) {
+  use_device(device);
+  EC_DISPATCH_VEC(bwd_scatter, grad, st);
+}
 
 // Debug/parity export on the fused path: copy the current batch's cached and
 // HBM rows into the compact buffer as K3 would (pinned-host misses are there
@@ -1164,6 +1165,11 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
     // host-tier write-back left running: it overlaps the next forward and is
     // joined by whatever next reuses this set or the host tier
     if (storage == EC_STORAGE_HOST) EC_DISPATCH_VEC(enqueue_host_writeback, lr);
+  } else if (p2p_on()) {
+    EC_DISPATCH_VEC(bwd_scatter, grad, st);
+    p2p_bwd_publish(lr, st);  // hits -> own list, misses -> owners' rows (NVLink atomics)
+    p2p_signal(0, st);
+    p2p_bwd_finish(lr, st);   // every rank's list, in rank order, into the cache replica
   } else {
     scatter_and_apply_local(grad, lr, st);
     exchange_bwd(lr, st);  // remote misses -> owners, replicated hot rows in rank order
@@ -1460,6 +1466,13 @@ static void decode_stats(Engine& e, int* h, uint64_t lookups, uint64_t wire_rows
   s.model_bytes = s.miss_rows * e.D * sizeof(float) + s.index_units * sizeof(uint32_t);
   s.wire_rows = wire_rows;
   s.wire_bytes = wire_bytes;
+  if (e.p2p_on()) {
+    // peer-memory exchange: rows this rank pulled (device count), their
+    // gradient atomics back, and its hot list read by every other rank
+    const uint64_t rowb = static_cast<uint64_t>(e.D) * sizeof(float);
+    s.wire_rows = static_cast<uint64_t>(*c.wire);
+    s.wire_bytes = 2 * s.wire_rows * rowb + s.hit_rows * (4 + rowb) * static_cast<uint64_t>(e.world - 1);
+  }
   *out = s;
 }
 

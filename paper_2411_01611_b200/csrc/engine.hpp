@@ -33,14 +33,28 @@ struct Tile {
 };
 
 // Per-batch device counters, one int array:
-//   M[T] ubase[T+1] miss_total tile_counter err   (err last: survives resets)
+//   M[T] ubase[T+1] miss_total tile_counter wire err   (err last: survives resets)
+// wire: rows pulled from peer shards by the P2P exchange.
 struct Counters {
-  int *M, *ubase, *miss_total, *tile_counter, *err;
+  int *M, *ubase, *miss_total, *tile_counter, *wire, *err;
 };
 __host__ __device__ inline Counters counters(int* p, int T) {
-  return Counters{p, p + T, p + 2 * T + 1, p + 2 * T + 2, p + 2 * T + 3};
+  return Counters{p, p + T, p + 2 * T + 1, p + 2 * T + 2, p + 2 * T + 3, p + 2 * T + 4};
 }
-inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 4; }
+inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 5; }
+
+// What a rank sees of a peer for the peer-memory exchange (K4 over NVLink
+// loads/stores/atomics): the peer's HBM shard and its published hot-row
+// gradient list, and the flag words the peer waits on.
+constexpr int kP2PBarriers = 3;  // device barriers per step of the peer-memory exchange
+
+struct PeerView {
+  float* store;             // the peer's whole shard (row = shard_off[peer][t] + id / world)
+  const uint32_t* pub_slot; // its hot list: cache slots ...
+  const float* pub_grad;    // ... and their gradient rows
+  const int* pub_cnt;       // ... and its length
+  unsigned* flags;          // the peer's barrier words: [2 * world] (B1 by rank, then B2 by rank)
+};
 
 struct Exchange;  // exchange.cu
 
@@ -279,6 +293,7 @@ struct Engine {
   void join_host_writes(cudaStream_t st);
   void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
   void gather_for_export();
+  void scatter_grads(const float* grad, cudaStream_t st);
   template <int VEC>
   void export_gather();
   float bwd_lr = 0.f;  // learning rate of the backward being enqueued
@@ -304,7 +319,33 @@ struct Engine {
   uint64_t exch_bytes() const;
   void exchange_fwd(cudaStream_t st);
   void exchange_bwd(float lr, cudaStream_t st);
+  // peer-memory exchange (exchange.cu)
+  bool p2p_on() const;
+  const PeerView* p2p_peers() const;
+  const int64_t* p2p_shard_off() const;
+  void p2p_alloc();
+  void p2p_set_peers(const std::vector<PeerView>& v);
+  PeerView p2p_self() const;
+  void p2p_fwd_begin(cudaStream_t st);
+  void p2p_bwd_publish(float lr, cudaStream_t st);
+  template <int VEC> void p2p_publish(float lr, cudaStream_t st);
+  void p2p_signal(int b, cudaStream_t st);
+  void p2p_wait(int b, unsigned epoch, cudaStream_t st);
+  void p2p_bwd_finish(float lr, cudaStream_t st);
+  template <int VEC> void p2p_hot(float lr, cudaStream_t st);
 };
+
+// Instantiate FN<VEC> for the row width (D/4 float4 lanes per row).
+#define EC_DISPATCH_VEC(FN, ...)                                                  \
+  switch (D / 4) {                                                                \
+    case 1: FN<1>(__VA_ARGS__); break;                                            \
+    case 2: FN<2>(__VA_ARGS__); break;                                            \
+    case 4: FN<4>(__VA_ARGS__); break;                                            \
+    case 8: FN<8>(__VA_ARGS__); break;                                            \
+    case 16: FN<16>(__VA_ARGS__); break;                                          \
+    case 32: FN<32>(__VA_ARGS__); break;                                          \
+    default: invalid("dim must be 4, 8, 16, 32, 64 or 128 for the lookup kernels"); \
+  }
 
 }  // namespace ec
 

@@ -58,7 +58,19 @@ struct Exchange {
   std::vector<int64_t> scnt, soff, rcnt, roff, hcnt, hoff;
   int64_t nsend = 0, nrecv = 0, nhot_all = 0;
 
+  // peer-memory (P2P) exchange: every rank's shard and hot list visible here
+  bool p2p = false;
+  unsigned epoch = 0;               // steps started (barrier generations)
+  DevBuf<PeerView> peers;           // [W]
+  std::vector<PeerView> peers_host;
+  DevBuf<uint32_t> pub_slot;        // this rank's published hot list
+  DevBuf<float> pub_grad;
+  DevBuf<int> pub_cnt;
+  DevBuf<unsigned> flags;           // [2W] barrier words peers write into
+  std::vector<void*> ipc_opened;    // peer allocations mapped by cudaIpcOpenMemHandle
+
   ~Exchange() {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (comm) ncclCommDestroy(comm);
     if (allcnt_host) cudaFreeHost(allcnt_host);
   }
@@ -167,6 +179,90 @@ __global__ void k_rows_sgd(float* __restrict__ rows, const uint32_t* __restrict_
     v.w -= lr * gv.w;
     *w = v;
   }
+}
+
+// ---- P2P exchange kernels
+// Backward, after the gradient reduction: cache hits go to this rank's
+// published hot list (applied by every rank in rank order); misses update
+// their owner's shard row in place with -lr*g (float atomics: the owner's row
+// may receive several ranks' updates in one step; it is not replicated).
+template <int VEC>
+__global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                            const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                            const int32_t* __restrict__ usrc, const float* __restrict__ ugrad, float lr,
+                            const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, int rank,
+                            int world, uint32_t* __restrict__ pub_slot, float* __restrict__ pub_grad,
+                            int* __restrict__ pub_cnt) {
+  constexpr int D = VEC * 4;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int sub = lane_id() / VEC, c = lane_id() % VEC;
+  constexpr int RPW = 32 / VEC;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g0 = warp * RPW; g0 < U; g0 += nwarps * RPW) {  // warp-uniform trip count (ballots inside)
+    const int g = g0 + sub;
+    const bool live = g < U;
+    const int32_t s = live ? usrc[g] : -1;
+    const float4 gv = live ? ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // hits: one list slot per row (lane c == 0 of the row's group claims it)
+    const bool hit = live && s >= 0;
+    const unsigned hb = __ballot_sync(kFull, hit && c == 0);
+    int b0 = 0;
+    if (hb && lane_id() == __ffs(hb) - 1) b0 = atomicAdd(pub_cnt, __popc(hb));
+    b0 = __shfl_sync(kFull, b0, __ffs(hb ? hb : 1u) - 1);
+    const int pos = b0 + __popc(hb & ((1u << (sub * VEC)) - 1));
+    if (hit) {
+      if (c == 0) pub_slot[pos] = static_cast<uint32_t>(s);
+      st4(pub_grad + static_cast<int64_t>(pos) * D + c * 4, gv);
+    } else if (live) {
+      const uint32_t id = uniq[g];
+      const int t = utab[g];
+      const int o = static_cast<int>(id % world);
+      float* row = peers[o].store + (shard_off[static_cast<int64_t>(o) * (T + 1) + t] + id / world) * D + c * 4;
+      atomicAdd(row + 0, -lr * gv.x);
+      atomicAdd(row + 1, -lr * gv.y);
+      atomicAdd(row + 2, -lr * gv.z);
+      atomicAdd(row + 3, -lr * gv.w);
+    }
+  }
+}
+
+// One source rank's published hot gradients into this rank's cache replica
+// (launched for p = 0..world-1: every replica sees the same order).
+template <int VEC>
+__global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float* __restrict__ cache, float lr) {
+  constexpr int D = VEC * 4;
+  const PeerView pv = peers[p];
+  const int n = *reinterpret_cast<const volatile int*>(pv.pub_cnt);
+  const int64_t total = static_cast<int64_t>(n) * VEC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / VEC;
+    const int c = static_cast<int>(i - k * VEC);
+    float* w = cache + static_cast<int64_t>(pv.pub_slot[k]) * D + c * 4;
+    const float4 gv = *reinterpret_cast<const float4*>(pv.pub_grad + k * D + c * 4);
+    float4 v = *reinterpret_cast<const float4*>(w);
+    v = make_float4(v.x - lr * gv.x, v.y - lr * gv.y, v.z - lr * gv.z, v.w - lr * gv.w);
+    st4(w, v);
+  }
+}
+
+// Device barrier over peer memory, split in two so a loopback group can
+// enqueue every rank's signal before any rank's wait on one stream.
+// Barrier b (0: hot lists published, 1: step applied, 2: forward reads done)
+// of generation `epoch`.
+__global__ void k_p2p_signal(const PeerView* __restrict__ peers, int world, int rank, int b, unsigned epoch) {
+  if (threadIdx.x >= world) return;
+  __threadfence_system();  // this rank's writes of the step before the word
+  unsigned* f = peers[threadIdx.x].flags + b * world + rank;
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+}
+__global__ void k_p2p_wait(const unsigned* __restrict__ flags, int world, int b, unsigned epoch) {
+  if (threadIdx.x >= world) return;
+  const unsigned* f = flags + b * world + threadIdx.x;
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  } while (static_cast<int>(v - epoch) < 0);
+  __threadfence_system();
 }
 
 static int grid_rows(int64_t n, int vec4, int device) {
@@ -333,8 +429,99 @@ void Engine::ex_apply_bwd(float lr, cudaStream_t st) {
   }
 }
 
+// ------------------------------------------------------------ P2P driver
+// Per step (generation e = ++epoch): forward waits barrier 1 of e-1 (every
+// rank applied the previous step), pulls remote rows in k_gather and signals
+// barrier 2 (its reads of peers' shards are done); backward waits barrier 2
+// (nobody still reads the rows it is about to update), publishes its hot list
+// and updates owners' rows by atomics, signals barrier 0, waits for it,
+// applies every rank's list in rank order, signals barrier 1.
+// No host synchronisation, no NCCL call.
+bool Engine::p2p_on() const { return ex != nullptr && ex->p2p; }
+const PeerView* Engine::p2p_peers() const { return p2p_on() ? ex->peers.p : nullptr; }
+const int64_t* Engine::p2p_shard_off() const { return p2p_on() ? ex->shard_off.p : nullptr; }
+
+void Engine::p2p_alloc() {
+  if (storage != EC_STORAGE_HBM) invalid("the peer-memory exchange needs the cold tier in HBM");
+  if (!ex) ex_init(world);
+  Exchange& x = *ex;
+  const size_t N = max_n * T;
+  if (x.pub_slot.n < N) x.pub_slot.alloc(N);
+  if (x.pub_grad.n < N * D) x.pub_grad.alloc(N * D);
+  if (!x.pub_cnt.n) {
+    x.pub_cnt.alloc(1);
+    EC_CUDA(cudaMemset(x.pub_cnt.p, 0, sizeof(int)));
+  }
+  if (x.flags.n < static_cast<size_t>(kP2PBarriers * x.W)) {
+    x.flags.alloc(kP2PBarriers * x.W);
+    EC_CUDA(cudaMemset(x.flags.p, 0, x.flags.bytes()));
+  }
+}
+
+PeerView Engine::p2p_self() const {
+  return PeerView{store_dev.p, ex->pub_slot.p, ex->pub_grad.p, ex->pub_cnt.p, ex->flags.p};
+}
+
+void Engine::p2p_set_peers(const std::vector<PeerView>& v) {
+  Exchange& x = *ex;
+  if (static_cast<int>(v.size()) != x.W) invalid("peer table needs one entry per rank");
+  x.peers_host = v;
+  x.peers.alloc(v.size());
+  EC_CUDA(cudaMemcpy(x.peers.p, v.data(), v.size() * sizeof(PeerView), cudaMemcpyHostToDevice));
+  // flags were zeroed at allocation and only ever grow (generation numbers):
+  // re-importing keeps the epoch, so a peer's early signal is never wiped
+  x.p2p = true;
+  clear_graphs();
+}
+
+void Engine::p2p_signal(int b, cudaStream_t st) {
+  k_p2p_signal<<<1, 32, 0, st>>>(ex->peers.p, ex->W, rank, b, ex->epoch);
+  launched();
+}
+void Engine::p2p_wait(int b, unsigned epoch, cudaStream_t st) {
+  k_p2p_wait<<<1, 32, 0, st>>>(ex->flags.p, ex->W, b, epoch);
+  launched();
+}
+
+void Engine::p2p_fwd_begin(cudaStream_t st) {
+  Exchange& x = *ex;
+  ++x.epoch;
+  p2p_wait(1, x.epoch - 1, st);
+  last_wire_rows = 0;  // (counted on the device: Counters::wire)
+  last_wire_bytes = 0;
+}
+
+template <int VEC>
+void Engine::p2p_publish(float lr, cudaStream_t st) {
+  Exchange& x = *ex;
+  p2p_wait(2, x.epoch, st);  // every rank's forward reads of step e are done
+  EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
+  k_p2p_apply<VEC><<<row_grid(), 256, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, usrc.p,
+                                                   ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.pub_slot.p,
+                                                   x.pub_grad.p, x.pub_cnt.p);
+  launched();
+}
+void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
+  PhaseScope ph(prof, kPhaseExchange, st);
+  EC_DISPATCH_VEC(p2p_publish, lr, st);
+}
+
+template <int VEC>
+void Engine::p2p_hot(float lr, cudaStream_t st) {
+  for (int p = 0; p < ex->W; ++p) {
+    k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr);
+    launched();
+  }
+}
+void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
+  PhaseScope ph(prof, kPhaseExchange, st);
+  p2p_wait(0, ex->epoch, st);
+  EC_DISPATCH_VEC(p2p_hot, lr, st);
+  p2p_signal(1, st);
+}
+
 // ------------------------------------------------------------ NCCL driver
-bool Engine::comm_ready() const { return ex != nullptr && (ex->comm != nullptr || in_group); }
+bool Engine::comm_ready() const { return ex != nullptr && (ex->comm != nullptr || in_group || ex->p2p); }
 
 void Engine::attach_comm(const uint8_t* id128) {
   use_device(device);
@@ -492,6 +679,19 @@ int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs,
     if (!g) invalid("null group");
     cudaStream_t st = as_stream(stream);
     const int W = static_cast<int>(g->members.size());
+    if (g->members[0]->e.p2p_on()) {  // peer-memory exchange: the same kernels as across GPUs
+      for (int r = 0; r < W; ++r) {
+        Engine& e = g->members[r]->e;
+        e.forward_prologue(batches[r], outs[r], st);
+        e.p2p_fwd_begin(st);
+        e.enqueue_dedup_partition(batches[r].indices_dev, st);
+        e.gather_local(st);
+        e.p2p_signal(2, st);
+        e.pool(st);
+        e.have_fwd = true;
+      }
+      return;
+    }
     for (int r = 0; r < W; ++r) {
       Engine& e = g->members[r]->e;
       e.forward_prologue(batches[r], outs[r], st);
@@ -544,6 +744,19 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
     cudaStream_t st = as_stream(stream);
     const int W = static_cast<int>(g->members.size());
     const size_t D = g->members[0]->e.D;
+    if (g->members[0]->e.p2p_on()) {
+      // every rank's signal of barrier 0 precedes every rank's wait on one stream
+      for (int r = 0; r < W; ++r) {
+        Engine& e = g->members[r]->e;
+        if (!e.have_fwd) invalid("ec_group_lookup_bwd needs a preceding forward");
+        if (!grads[r]) invalid("null gradient");
+        e.scatter_grads(grads[r], st);
+        e.p2p_bwd_publish(lr, st);
+        e.p2p_signal(0, st);
+      }
+      for (int r = 0; r < W; ++r) g->members[r]->e.p2p_bwd_finish(lr, st);
+      return;
+    }
     for (int r = 0; r < W; ++r) {
       Engine& e = g->members[r]->e;
       if (!e.have_fwd) invalid("ec_group_lookup_bwd needs a preceding forward");
@@ -567,6 +780,77 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
         }
       }
     for (int r = 0; r < W; ++r) g->members[r]->e.ex_apply_bwd(lr, st);
+  });
+}
+
+// Loopback group on the peer-memory exchange: every member sees the others'
+// shards and hot lists directly (same device), through the kernels a
+// multi-process job uses over NVLink (ec_tables_p2p_export/import).
+int ec_group_set_p2p(ec_group g, int enable) {
+  return guard([&] {
+    if (!g) invalid("null group");
+    if (!enable) {
+      for (auto m : g->members)
+        if (m->e.ex) m->e.ex->p2p = false;
+      return;
+    }
+    std::vector<PeerView> views;
+    for (auto m : g->members) {
+      use_device(m->e.device);
+      m->e.p2p_alloc();
+      views.push_back(m->e.p2p_self());
+    }
+    for (auto m : g->members) m->e.p2p_set_peers(views);
+  });
+}
+
+// Multi-process: this rank's peer-visible allocations as CUDA IPC handles
+// (shard, hot list, its length, barrier words), to be all-gathered and
+// passed to every rank's ec_tables_p2p_import.
+int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len) {
+  return guard([&] {
+    if (!t) invalid("null tables handle");
+    Engine& e = t->e;
+    use_device(e.device);
+    e.p2p_alloc();
+    void* ptrs[5] = {e.store_dev.p, e.ex->pub_slot.p, e.ex->pub_grad.p, e.ex->pub_cnt.p, e.ex->flags.p};
+    *len = sizeof(ptrs) / sizeof(ptrs[0]) * sizeof(cudaIpcMemHandle_t);
+    if (!blob) return;
+    if (cap < *len) invalid("p2p export blob needs " + std::to_string(*len) + " bytes");
+    for (int k = 0; k < 5; ++k) {
+      cudaIpcMemHandle_t h;
+      EC_CUDA(cudaIpcGetMemHandle(&h, ptrs[k]));
+      std::memcpy(blob + k * sizeof(h), &h, sizeof(h));
+    }
+  });
+}
+
+int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
+  return guard([&] {
+    if (!t || !blobs) invalid("null argument");
+    Engine& e = t->e;
+    if (e.world < 2) invalid("the peer-memory exchange needs world > 1");
+    if (blob_len != 5 * sizeof(cudaIpcMemHandle_t)) invalid("unexpected p2p blob size");
+    use_device(e.device);
+    e.p2p_alloc();
+    std::vector<PeerView> views(e.world);
+    for (int p = 0; p < e.world; ++p) {
+      if (p == e.rank) {
+        views[p] = e.p2p_self();
+        continue;
+      }
+      void* ptrs[5];
+      for (int k = 0; k < 5; ++k) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, blobs + p * blob_len + k * sizeof(h), sizeof(h));
+        EC_CUDA(cudaIpcOpenMemHandle(&ptrs[k], h, cudaIpcMemLazyEnablePeerAccess));
+        e.ex->ipc_opened.push_back(ptrs[k]);
+      }
+      views[p] = PeerView{static_cast<float*>(ptrs[0]), static_cast<const uint32_t*>(ptrs[1]),
+                          static_cast<const float*>(ptrs[2]), static_cast<const int*>(ptrs[3]),
+                          static_cast<unsigned*>(ptrs[4])};
+    }
+    e.p2p_set_peers(views);
   });
 }
 

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     if (threadIdx.x == 0) {
       *c.miss_total = 0;
       *c.tile_counter = 0;
+      *c.wire = 0;
     }
   }
   uint32_t id[kItems];
@@ -343,20 +344,27 @@ struct RowMap {
   __device__ RowMap() : sub(lane_id() / VEC), c(lane_id() % VEC) {}
 };
 
+// With `peers` (the P2P exchange, HBM shards), misses owned by another rank
+// are read straight from that rank's shard over NVLink: the forward exchange
+// is this kernel's remote loads -- no request/response round, no host sync.
 template <int VEC, int R>
-__global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+__global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict__ td, int T, int* __restrict__ ctr,
                                                      const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                                                      const uint32_t* __restrict__ uslot,
                                                      const int32_t* __restrict__ usrc, const float* __restrict__ cache,
                                                      float* __restrict__ urows, float* __restrict__ ugrad,
-                                                     int* __restrict__ cnt, int local_hbm, int rank, int world) {
+                                                     int* __restrict__ cnt, int local_hbm, int rank, int world,
+                                                     const PeerView* __restrict__ peers = nullptr,
+                                                     const int64_t* __restrict__ shard_off = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
-  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const Counters cs = counters(ctr, T);
+  const int U = cs.ubase[T];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  int remote = 0;
   for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
     float4 v[R];
     int dst[R];
@@ -372,7 +380,13 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
           src = cache + static_cast<int64_t>(s) * D;
         } else if (local_hbm) {
           const uint32_t id = uniq[g];
-          if (static_cast<int>(id % world) == rank) src = td[tab].store + static_cast<int64_t>(id / world) * D;
+          const int o = static_cast<int>(id % world);
+          if (o == rank) {
+            src = td[tab].store + static_cast<int64_t>(id / world) * D;
+          } else if (peers) {
+            src = peers[o].store + (shard_off[static_cast<int64_t>(o) * (T + 1) + tab] + id / world) * D;
+            remote += m.c == 0;
+          }
         }
         if (src) {
           v[r] = ldg4(src + m.c * 4);
@@ -390,6 +404,10 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+  if (peers) {
+    remote = __reduce_add_sync(kFull, remote);
+    if (remote && lane_id() == 0) atomicAdd(cs.wire, remote);
   }
 }
 

@@ -302,6 +302,24 @@ class EmbeddingTables:
         buf = (C.c_uint8 * 128)(*uid)
         check(N.lib().ec_tables_attach_comm(self._h, buf))
 
+    def p2p_export(self) -> bytes:
+        """This rank's peer-visible allocations as CUDA IPC handles (one
+        process per GPU); all-gather them and pass the list to p2p_import."""
+        n = C.c_uint64()
+        check(N.lib().ec_tables_p2p_export(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(N.lib().ec_tables_p2p_export(self._h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def p2p_import(self, blobs: Sequence[bytes]):
+        """Switch to the peer-memory exchange with every rank's export blob
+        (rank order).  Each step then ends at a device-side barrier."""
+        if len(blobs) != self.world or len({len(b) for b in blobs}) != 1:
+            raise ValueError("p2p_import needs one equal-sized blob per rank")
+        raw = b"".join(blobs)
+        buf = (C.c_uint8 * len(raw)).from_buffer_copy(raw)
+        check(N.lib().ec_tables_p2p_import(self._h, buf, len(blobs[0])))
+
 
 
 def shard_rows(rows: Sequence[int], world: int, rank: int) -> list[int]:
@@ -326,12 +344,14 @@ class EmbeddingGroup:
     device, driven in lock step (same routing / serve / gradient return /
     rank-ordered replica update as the NCCL path, device copies as transport)."""
 
-    def __init__(self, members: Sequence[EmbeddingTables]):
+    def __init__(self, members: Sequence[EmbeddingTables], p2p: bool = False):
         self.members = list(members)
         arr = (C.c_void_p * len(self.members))(*[m._h.value for m in self.members])
         h = C.c_void_p()
         check(N.lib().ec_group_create(arr, len(self.members), C.byref(h)))
         self._h = h
+        if p2p:  # peer-memory exchange (the multi-process NVLink kernels, loopback)
+            check(N.lib().ec_group_set_p2p(self._h, 1))
 
     def close(self):
         if getattr(self, "_h", None):
