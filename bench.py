@@ -66,6 +66,14 @@ def batch_seed(rank, j, t):
     return substream_seed(substream_seed(substream_seed(SEED, rank), j), t)
 
 
+def all_max(torch, x: float) -> float:
+    """Max over ranks (the device timings' reduction)."""
+    dev = "cpu" if torch.distributed.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -133,6 +141,15 @@ def make_dist(ec, wl, rows, t):
     return ec.EmbeddingDistribution.from_probabilities(p)
 
 
+def exchange_kind(wl):
+    """N>1 transport: peer memory (loads / atomics over NVLink, device
+    barriers, no host sync) for HBM shards; NCCL all-to-all for the pinned-host
+    tier (host memory is not IPC-shareable)."""
+    if MODES.get("exchange", "auto") != "auto":
+        return MODES["exchange"]
+    return "p2p" if wl["storage"] == "hbm" else "nccl"
+
+
 def build_tables(ec, torch, wl, rank, world, device):
     rows, D, B, P = wl["rows"], wl["dim"], wl["batch"], wl["pooling"]
     dists = [make_dist(ec, wl, r, t) for t, r in enumerate(rows)]
@@ -148,7 +165,14 @@ def build_tables(ec, torch, wl, rank, world, device):
         tab.dedup_mode(MODES["dedup"])
     if MODES.get("scatter"):
         tab.scatter_mode(MODES["scatter"])
-    if world > 1:
+    if world > 1 and exchange_kind(wl) == "p2p":
+        # peer-memory exchange: shards, hot lists and barrier words shared by CUDA IPC
+        import torch.distributed as dist
+        blobs = [None] * world
+        dist.all_gather_object(blobs, tab.p2p_export())
+        tab.p2p_import(blobs)
+        dist.barrier()
+    elif world > 1:
         import torch.distributed as dist
         uid = [ec.EmbeddingTables.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -200,7 +224,15 @@ def run_ours(args, wl):
     import torch
     import paper_2411_01611_b200 as ec
     rank, world, local = env_rank()
-    if world > 1:
+    if world > 1 and torch.cuda.device_count() < world:
+        # functional check of the N>1 path with ranks sharing GPUs (gloo
+        # plumbing); its timings are not a scaling measurement
+        local = local % torch.cuda.device_count()
+        print(f"bench: {world} ranks share {torch.cuda.device_count()} GPU(s); timings are not per-GPU",
+              file=sys.stderr)
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    elif world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -279,9 +311,7 @@ def run_ours(args, wl):
     step_dist = {"min": round(min(step_ms), 5), "median": round(statistics.median(step_ms), 5),
                  "max": round(max(step_ms), 5), "argmax": int(np.argmax(step_ms))}
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = all_max(torch, ms)
     lookups_per_step = T * B * P
     value = lookups_per_step * world / (ms * 1e-3)
 
@@ -302,9 +332,7 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
     if world > 1:
-        t = torch.tensor([fwd_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        fwd_ms = float(t.item())
+        fwd_ms = all_max(torch, fwd_ms)
     # restore the pipeline state of the stepping loop (a backward for the last forward)
     tab.backward(out, LR)
     torch.cuda.synchronize()
@@ -387,9 +415,7 @@ def run_ours(args, wl):
     e2e_dist = {"min": round(min(e2e_step), 5), "median": round(statistics.median(e2e_step), 5),
                 "max": round(max(e2e_step), 5), "argmax": int(np.argmax(e2e_step))}
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = all_max(torch, e2e_ms)
 
     # ---- hot/normal scheduling (paper §Experiment Settings):
     # one epoch of EPOCH_BATCHES batches timed in dataset order and in the
@@ -490,7 +516,8 @@ def run_ours(args, wl):
                             "host-miss gather overlap this step and are inside its window, as is this step's "
                             "host write-back") if depth else
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
-                   "parallelism": f"row-sharded x{world}, owner = id % {world}" if world > 1 else "single GPU"},
+                   "parallelism": f"row-sharded x{world}, owner = id % {world}, {exchange_kind(wl)} exchange"
+                   if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
                 "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4)},
@@ -645,6 +672,8 @@ def main():
                     help="priority of the caller's stream (torch: -1 high, 0 low; engine side streams are low)")
     ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster", "table"], default=None)
     ap.add_argument("--scatter-mode", choices=["auto", "atomic", "transpose"], default=None)
+    ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="N>1 transport (auto: p2p for HBM shards, nccl for the pinned-host tier)")
     args = ap.parse_args()
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         args.prefetch = False  # ec_lookup_prefetch is single-rank (the exchange synchronises ranks per batch)
@@ -652,7 +681,7 @@ def main():
         args.prefetch_depth = 2 if WORKLOADS[args.workload]["storage"] == "host" else 1
     if not args.prefetch:
         args.prefetch_depth = 0
-    MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode)
+    MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode, exchange=args.exchange)
     if args.warmup < 3:
         args.warmup = 3
     wl = WORKLOADS[args.workload]

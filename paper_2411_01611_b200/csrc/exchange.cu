@@ -61,6 +61,7 @@ struct Exchange {
   // peer-memory (P2P) exchange: every rank's shard and hot list visible here
   bool p2p = false;
   unsigned epoch = 0;               // steps started (barrier generations)
+  bool step_open = false;           // a forward whose step was not applied yet
   DevBuf<PeerView> peers;           // [W]
   std::vector<PeerView> peers_host;
   DevBuf<uint32_t> pub_slot;        // this rank's published hot list
@@ -255,13 +256,24 @@ __global__ void k_p2p_signal(const PeerView* __restrict__ peers, int world, int 
   unsigned* f = peers[threadIdx.x].flags + b * world + rank;
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
 }
+constexpr uint64_t kP2PTimeoutNs = 60ull * 1000 * 1000 * 1000;
 __global__ void k_p2p_wait(const unsigned* __restrict__ flags, int world, int b, unsigned epoch) {
   if (threadIdx.x >= world) return;
   const unsigned* f = flags + b * world + threadIdx.x;
   unsigned v;
-  do {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (unsigned k = 1;; ++k) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-  } while (static_cast<int>(v - epoch) < 0);
+    if (static_cast<int>(v - epoch) >= 0) break;
+    if ((k & 1023) == 0) {  // a peer that never arrives (died, or called fwd/bwd fewer times)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > kP2PTimeoutNs) {
+        printf("embcomm p2p: barrier %d generation %u: rank %d never arrived\n", b, epoch, threadIdx.x);
+        __trap();  // fail the step loudly instead of hanging the GPU
+      }
+    }
+  }
   __threadfence_system();
 }
 
@@ -483,9 +495,19 @@ void Engine::p2p_wait(int b, unsigned epoch, cudaStream_t st) {
   launched();
 }
 
+// A forward with no backward after it (evaluation) still has to release the
+// peers waiting for its step to be applied: nothing was, so barrier 1 only.
+void Engine::p2p_close_open(cudaStream_t st) {
+  if (!ex->step_open) return;
+  p2p_signal(1, st);
+  ex->step_open = false;
+}
+
 void Engine::p2p_fwd_begin(cudaStream_t st) {
   Exchange& x = *ex;
+  p2p_close_open(st);
   ++x.epoch;
+  x.step_open = true;
   p2p_wait(1, x.epoch - 1, st);
   last_wire_rows = 0;  // (counted on the device: Counters::wire)
   last_wire_bytes = 0;
@@ -502,6 +524,7 @@ void Engine::p2p_publish(float lr, cudaStream_t st) {
   launched();
 }
 void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
+  if (!ex->step_open) invalid("the peer-memory exchange takes one backward per forward");
   PhaseScope ph(prof, kPhaseExchange, st);
   EC_DISPATCH_VEC(p2p_publish, lr, st);
 }
@@ -518,6 +541,7 @@ void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
   p2p_wait(0, ex->epoch, st);
   EC_DISPATCH_VEC(p2p_hot, lr, st);
   p2p_signal(1, st);
+  ex->step_open = false;
 }
 
 // ------------------------------------------------------------ NCCL driver
@@ -680,6 +704,7 @@ int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs,
     cudaStream_t st = as_stream(stream);
     const int W = static_cast<int>(g->members.size());
     if (g->members[0]->e.p2p_on()) {  // peer-memory exchange: the same kernels as across GPUs
+      for (int r = 0; r < W; ++r) g->members[r]->e.p2p_close_open(st);  // every signal before any wait
       for (int r = 0; r < W; ++r) {
         Engine& e = g->members[r]->e;
         e.forward_prologue(batches[r], outs[r], st);

@@ -146,3 +146,39 @@ def test_group_p2p_rejects_host_tier(ec, torch):
         ec.EmbeddingGroup(ms, p2p=True)
     for m in ms:
         m.close()
+
+
+def test_group_p2p_forward_only_steps(ec, torch):
+    """Evaluation forwards (no backward) release the peers' barriers; a second
+    backward of one forward is refused (its updates would race the peers'
+    next forward)."""
+    world, rows, D, B = 2, [300, 50], 8, 16
+    ms = [ec.EmbeddingTables(rows, D, rank=r, world=world, max_lookups_per_table=B, max_batch_size=B)
+          for r in range(world)]
+    for m in ms:
+        m.init_synthetic(3, 1.0)
+    g = ec.EmbeddingGroup(ms, p2p=True)
+    offs = np.array([0, B, 2 * B], np.int64)
+    ids = [torch.randint(0, 50, (2 * B,), dtype=torch.int32, device="cuda") for _ in range(world)]
+    first = [o.clone() for o in g.forward(ids, offs, B, 1)]
+    for _ in range(3):  # forward-only steps: identical outputs, nothing applied
+        again = g.forward(ids, offs, B, 1)
+        for a, b in zip(first, again):
+            assert torch.equal(a, b)
+    g.backward([torch.ones_like(o) for o in first], 0.5)
+    with pytest.raises(ec.ValidationError):
+        g.backward([torch.ones_like(o) for o in first], 0.5)
+    after = g.forward(ids, offs, B, 1)
+    torch.cuda.synchronize()
+    # every looked-up row moved by -0.5 * (its count over both ranks); pooled
+    # outputs (sum pooling, P = 1) shift by exactly that
+    for r in range(world):
+        for t in range(2):
+            col = slice(t * D, (t + 1) * D)
+            seg = torch.cat([i[t * B:(t + 1) * B] for i in ids])
+            cnt = torch.bincount(seg.long(), minlength=rows[t]).float()
+            exp = first[r][:, col] - 0.5 * cnt[ids[r][t * B:(t + 1) * B].long()][:, None]
+            torch.testing.assert_close(after[r][:, col], exp, rtol=1e-5, atol=1e-5)
+    g.close()
+    for m in ms:
+        m.close()
