@@ -452,9 +452,10 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads_dev, float lr, voi
 int ec_group_set_p2p(ec_group g, int enable);
 
 /* Multi-process peer-memory exchange (one process per GPU on one NVLink
- * domain).  Replaces the NCCL all-to-all exchange of
- * core/src/dist_embedding.cpp (forward :70-136, backward :138-206) with loads
- * and atomics over NVLink.  export: this rank's peer-visible allocations as
+ * domain).  The reference has no exchange code: it prices one (the E minus C
+ * rows of cached_epoch_cost, core/src/cost_model.cpp:88-111) and SURVEY.md
+ * 8(e) plans it as NCCL all-to-alls (ec_tables_attach_comm).  This transport
+ * replaces those all-to-alls with loads and atomics over NVLink.  export: this rank's peer-visible allocations as
  * CUDA IPC handles (blob == NULL -> *len only); the caller all-gathers the
  * blobs (rank-major, *len bytes each) and passes them to import, after which
  * ec_lookup_fwd/bwd use the peer path (no ec_tables_set_comm needed).  Every
