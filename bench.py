@@ -142,12 +142,12 @@ def make_dist(ec, wl, rows, t):
 
 
 def exchange_kind(wl):
-    """N>1 transport: peer memory (loads / atomics over NVLink, device
-    barriers, no host sync) for HBM shards; NCCL all-to-all for the pinned-host
-    tier (host memory is not IPC-shareable)."""
+    """N>1 transport: peer memory by default (remote rows loaded in the gather
+    kernels, owner updates by NVLink atomics / owner inboxes, device barriers,
+    no host sync); NCCL all-to-alls with one host sync per step on request."""
     if MODES.get("exchange", "auto") != "auto":
         return MODES["exchange"]
-    return "p2p" if wl["storage"] == "hbm" else "nccl"
+    return "p2p"
 
 
 def build_tables(ec, torch, wl, rank, world, device):
@@ -673,7 +673,7 @@ def main():
     ap.add_argument("--dedup-mode", choices=["auto", "tiles", "cluster", "table"], default=None)
     ap.add_argument("--scatter-mode", choices=["auto", "atomic", "transpose"], default=None)
     ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
-                    help="N>1 transport (auto: p2p for HBM shards, nccl for the pinned-host tier)")
+                    help="N>1 transport (auto: p2p)")
     args = ap.parse_args()
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         args.prefetch = False  # ec_lookup_prefetch is single-rank (the exchange synchronises ranks per batch)

@@ -447,8 +447,11 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads_dev, float lr, voi
  * loaded straight from the owner's shard inside the gather kernel, owner
  * updates are atomics into the owner's rows, hot-row gradient lists are
  * published and applied in rank order, and the ranks meet at device-side
- * barriers (flag words) instead of copies.  HBM-resident shards only.  The
- * same kernels run across processes after ec_tables_p2p_export/import. */
+ * barriers (flag words) instead of copies.  Pinned-host shards: every rank
+ * reads remote owners' rows from their (shared, memfd-backed) host shards over
+ * its own link, and sends miss gradients to the owner's inbox, applied by the
+ * owner in rank order.  The same kernels run across processes after
+ * ec_tables_p2p_export/import. */
 int ec_group_set_p2p(ec_group g, int enable);
 
 /* Multi-process peer-memory exchange (one process per GPU on one NVLink

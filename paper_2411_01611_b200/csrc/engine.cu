@@ -32,6 +32,7 @@
 //   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
 //            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
 #include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -210,10 +211,41 @@ static uint32_t log2_ceil(uint64_t x) {
 // then touch far fewer page translations than with 4 KiB pages, which
 // otherwise throttle the HBM kernels running beside them.  EC_HOST_ALLOC=cuda
 // selects plain cudaHostAlloc.
-void* alloc_host_tier(uint64_t bytes, bool* mmapped) {
+//
+// With `shared_fd` (a rank of a multi-process job on the peer-memory
+// exchange) the shard is a memfd mapping instead, so that peers on this node
+// can map it too (/proc/<pid>/fd/<fd>) and read its rows over their own link.
+void* alloc_host_tier(uint64_t bytes, bool* mmapped, int* shared_fd) {
   const char* mode = std::getenv("EC_HOST_ALLOC");
   void* p = nullptr;
   *mmapped = false;
+  if (shared_fd) {
+    const uint64_t huge = 2ull << 20;
+    const uint64_t len = (bytes + huge - 1) / huge * huge;
+    int fd = memfd_create("embcomm_host_tier", MFD_CLOEXEC | MFD_HUGETLB);
+    if (fd >= 0 && ftruncate(fd, static_cast<off_t>(len)) != 0) {
+      close(fd);
+      fd = -1;
+    }
+    if (fd >= 0) {  // hugetlb pages may still be short: try to map
+      p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_POPULATE, fd, 0);
+      if (p == MAP_FAILED) {
+        close(fd);
+        fd = -1;
+      }
+    }
+    if (fd < 0) {
+      fd = memfd_create("embcomm_host_tier", MFD_CLOEXEC);
+      if (fd < 0 || ftruncate(fd, static_cast<off_t>(len)) != 0) invalid("cannot create the shared host tier");
+      p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      if (p == MAP_FAILED) invalid("cannot map the shared host tier");
+      madvise(p, len, MADV_HUGEPAGE);
+    }
+    EC_CUDA(cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    *mmapped = true;
+    *shared_fd = fd;
+    return p;
+  }
   if (!mode || std::strcmp(mode, "cuda") != 0) {
     const uint64_t huge = 2ull << 20;
     const uint64_t len = (bytes + huge - 1) / huge * huge;
@@ -265,8 +297,9 @@ Engine::~Engine() {
   if (ev_patch) cudaEventDestroy(ev_patch);
   if (ev_pfcall) cudaEventDestroy(ev_pfcall);
   if (ev_gate) cudaEventDestroy(ev_gate);
+  destroy_comm();  // (unmaps the peers' shards first)
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
-  destroy_comm();
+  if (store_host_fd >= 0) close(store_host_fd);
 }
 
 void Engine::create(const ec_tables_config& c) {
@@ -316,7 +349,8 @@ void Engine::create(const ec_tables_config& c) {
     store_base = store_dev.p;
   } else {
     store_host_bytes = std::max<uint64_t>(store_elems, 1) * sizeof(float);
-    store_host = static_cast<float*>(alloc_host_tier(store_host_bytes, &store_host_mmapped));
+    store_host = static_cast<float*>(
+        alloc_host_tier(store_host_bytes, &store_host_mmapped, world > 1 ? &store_host_fd : nullptr));
     EC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&store_base), store_host, 0));
   }
   remap.alloc(remap_off[T]);
@@ -891,8 +925,8 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     p2p_fwd_begin(st);  // every rank applied the previous step
     enqueue_dedup_partition(b.indices_dev, st);
     gather_local(st);  // K4 fused: remote misses are loads from their owners' shards
+    pool(st);          // (joins the host-row gather of the side stream)
     p2p_signal(2, st);
-    pool(st);
   } else {
     enqueue_dedup_partition(b.indices_dev, st);
     gather_local(st);
@@ -975,12 +1009,12 @@ template <int VEC>
 void Engine::launch_gather_host(cudaStream_t s) {
   PhaseScope ph(prof, kPhaseGatherHost, s);
   const bool tma = host_tma();
-  if (tma)
+  if (tma && !p2p_on())
     k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
                                                              world);
-  else
+  else  // (peer exchange: remote owners' rows from their shared host shards, over this GPU's link)
     k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
-                                                            world);
+                                                            world, p2p_peers(), p2p_shard_off());
   launched();
 }
 

@@ -53,7 +53,12 @@ struct PeerView {
   const uint32_t* pub_slot; // its hot list: cache slots ...
   const float* pub_grad;    // ... and their gradient rows
   const int* pub_cnt;       // ... and its length
-  unsigned* flags;          // the peer's barrier words: [2 * world] (B1 by rank, then B2 by rank)
+  unsigned* flags;          // the peer's barrier words: [kP2PBarriers * world]
+  // pinned-host shards: the owner's inbox of miss-row gradients, one segment
+  // per source rank ([world][cap] row indices / gradient rows, [world] counts)
+  uint32_t* inbox_idx;
+  float* inbox_grad;
+  int* inbox_cnt;
 };
 
 struct Exchange;  // exchange.cu
@@ -163,6 +168,7 @@ struct Engine {
   float* store_host = nullptr;  // pinned, mapped
   uint64_t store_host_bytes = 0;
   bool store_host_mmapped = false;
+  int store_host_fd = -1;  // memfd of a shared host shard (world > 1)
   float* store_base = nullptr;  // device-visible base of the shard
   DevBuf<int32_t> remap;
   DevBuf<unsigned long long> hash;

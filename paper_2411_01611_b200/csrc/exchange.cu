@@ -27,6 +27,10 @@
 // step — the data path is shared, only the byte movement differs.
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -69,9 +73,19 @@ struct Exchange {
   DevBuf<int> pub_cnt;
   DevBuf<unsigned> flags;           // [2W] barrier words peers write into
   std::vector<void*> ipc_opened;    // peer allocations mapped by cudaIpcOpenMemHandle
+  // pinned-host shards: miss gradients sent to this rank as owner
+  DevBuf<uint32_t> inbox_idx;       // [W * cap]
+  DevBuf<float> inbox_grad;         // [W * cap * D]
+  DevBuf<int> inbox_cnt;            // [W]
+  int64_t inbox_cap = 0;
+  std::vector<std::pair<void*, size_t>> host_maps;  // peers' host shards mapped here
 
   ~Exchange() {
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    for (auto& m : host_maps) {
+      cudaHostUnregister(m.first);
+      munmap(m.first, m.second);
+    }
     if (comm) ncclCommDestroy(comm);
     if (allcnt_host) cudaFreeHost(allcnt_host);
   }
@@ -193,7 +207,7 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
                             const int32_t* __restrict__ usrc, const float* __restrict__ ugrad, float lr,
                             const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, int rank,
                             int world, uint32_t* __restrict__ pub_slot, float* __restrict__ pub_grad,
-                            int* __restrict__ pub_cnt) {
+                            int* __restrict__ pub_cnt, int64_t inbox_cap) {
   constexpr int D = VEC * 4;
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   const int sub = lane_id() / VEC, c = lane_id() % VEC;
@@ -214,16 +228,50 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
     if (hit) {
       if (c == 0) pub_slot[pos] = static_cast<uint32_t>(s);
       st4(pub_grad + static_cast<int64_t>(pos) * D + c * 4, gv);
-    } else if (live) {
-      const uint32_t id = uniq[g];
-      const int t = utab[g];
-      const int o = static_cast<int>(id % world);
-      float* row = peers[o].store + (shard_off[static_cast<int64_t>(o) * (T + 1) + t] + id / world) * D + c * 4;
-      atomicAdd(row + 0, -lr * gv.x);
-      atomicAdd(row + 1, -lr * gv.y);
-      atomicAdd(row + 2, -lr * gv.z);
-      atomicAdd(row + 3, -lr * gv.w);
     }
+    // misses: the owner's row (index in its shard)
+    const bool miss = live && s < 0;
+    const uint32_t id = miss ? uniq[g] : 0;
+    const int o = static_cast<int>(id % world);
+    const int64_t row = miss ? shard_off[static_cast<int64_t>(o) * (T + 1) + utab[g]] + id / world : 0;
+    if (inbox_cap) {
+      // pinned-host shards (no float atomics over PCIe): append to the
+      // owner's inbox segment for this source rank; the owner applies the
+      // segments in rank order
+      int ip = 0;
+      if (miss && c == 0) ip = atomicAdd(peers[o].inbox_cnt + rank, 1);
+      ip = __shfl_sync(kFull, ip, sub * VEC);
+      if (miss) {
+        const int64_t k = static_cast<int64_t>(rank) * inbox_cap + ip;
+        if (c == 0) peers[o].inbox_idx[k] = static_cast<uint32_t>(row);
+        st4(peers[o].inbox_grad + k * D + c * 4, gv);
+      }
+    } else if (miss) {  // HBM shards: straight into the owner's row
+      float* w = peers[o].store + row * D + c * 4;
+      atomicAdd(w + 0, -lr * gv.x);
+      atomicAdd(w + 1, -lr * gv.y);
+      atomicAdd(w + 2, -lr * gv.z);
+      atomicAdd(w + 3, -lr * gv.w);
+    }
+  }
+}
+
+// Owner side, pinned-host shards: source rank p's miss gradients into this
+// rank's shard (launched for p = 0..world-1; rows are unique within one
+// source's segment, so each launch is a plain read-modify-write).
+template <int VEC>
+__global__ void k_p2p_inbox_apply(const uint32_t* __restrict__ idx, const float* __restrict__ grad,
+                                  const int* __restrict__ cnt, float* __restrict__ store, float lr) {
+  constexpr int D = VEC * 4;
+  const int64_t total = static_cast<int64_t>(*cnt) * VEC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / VEC;
+    const int c = static_cast<int>(i - k * VEC);
+    float* w = store + static_cast<int64_t>(idx[k]) * D + c * 4;
+    const float4 gv = ldg4(grad + k * D + c * 4);
+    float4 v = *reinterpret_cast<const float4*>(w);
+    v = make_float4(v.x - lr * gv.x, v.y - lr * gv.y, v.z - lr * gv.z, v.w - lr * gv.w);
+    st4(w, v);
   }
 }
 
@@ -454,10 +502,17 @@ const PeerView* Engine::p2p_peers() const { return p2p_on() ? ex->peers.p : null
 const int64_t* Engine::p2p_shard_off() const { return p2p_on() ? ex->shard_off.p : nullptr; }
 
 void Engine::p2p_alloc() {
-  if (storage != EC_STORAGE_HBM) invalid("the peer-memory exchange needs the cold tier in HBM");
+  if (storage == EC_STORAGE_HOST && store_host_fd < 0) invalid("host shard is not shareable (world must be > 1)");
   if (!ex) ex_init(world);
   Exchange& x = *ex;
   const size_t N = max_n * T;
+  if (storage == EC_STORAGE_HOST && x.inbox_cap < static_cast<int64_t>(N)) {
+    x.inbox_cap = static_cast<int64_t>(N);
+    x.inbox_idx.alloc(x.W * N);
+    x.inbox_grad.alloc(x.W * N * D);
+    x.inbox_cnt.alloc(x.W);
+    EC_CUDA(cudaMemset(x.inbox_cnt.p, 0, x.inbox_cnt.bytes()));
+  }
   if (x.pub_slot.n < N) x.pub_slot.alloc(N);
   if (x.pub_grad.n < N * D) x.pub_grad.alloc(N * D);
   if (!x.pub_cnt.n) {
@@ -471,7 +526,8 @@ void Engine::p2p_alloc() {
 }
 
 PeerView Engine::p2p_self() const {
-  return PeerView{store_dev.p, ex->pub_slot.p, ex->pub_grad.p, ex->pub_cnt.p, ex->flags.p};
+  return PeerView{store_base, ex->pub_slot.p, ex->pub_grad.p, ex->pub_cnt.p, ex->flags.p,
+                  ex->inbox_idx.p, ex->inbox_grad.p, ex->inbox_cnt.p};
 }
 
 void Engine::p2p_set_peers(const std::vector<PeerView>& v) {
@@ -520,7 +576,8 @@ void Engine::p2p_publish(float lr, cudaStream_t st) {
   EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
   k_p2p_apply<VEC><<<row_grid(), 256, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, usrc.p,
                                                    ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.pub_slot.p,
-                                                   x.pub_grad.p, x.pub_cnt.p);
+                                                   x.pub_grad.p, x.pub_cnt.p,
+                                                   storage == EC_STORAGE_HOST ? x.inbox_cap : 0);
   launched();
 }
 void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
@@ -531,6 +588,16 @@ void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
 
 template <int VEC>
 void Engine::p2p_hot(float lr, cudaStream_t st) {
+  Exchange& x = *ex;
+  if (x.inbox_cap && storage == EC_STORAGE_HOST) {  // owner: every source's miss gradients, rank order
+    for (int p = 0; p < x.W; ++p) {
+      k_p2p_inbox_apply<VEC><<<host_grid(), 256, 0, st>>>(x.inbox_idx.p + p * x.inbox_cap,
+                                                          x.inbox_grad.p + p * x.inbox_cap * D, x.inbox_cnt.p + p,
+                                                          store_base, lr);
+      launched();
+    }
+    EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append again after barrier 2
+  }
   for (int p = 0; p < ex->W; ++p) {
     k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr);
     launched();
@@ -711,8 +778,8 @@ int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs,
         e.p2p_fwd_begin(st);
         e.enqueue_dedup_partition(batches[r].indices_dev, st);
         e.gather_local(st);
-        e.p2p_signal(2, st);
         e.pool(st);
+        e.p2p_signal(2, st);  // after the pool: it joins the side stream's host-row reads
         e.have_fwd = true;
       }
       return;
@@ -829,23 +896,43 @@ int ec_group_set_p2p(ec_group g, int enable) {
   });
 }
 
-// Multi-process: this rank's peer-visible allocations as CUDA IPC handles
-// (shard, hot list, its length, barrier words), to be all-gathered and
-// passed to every rank's ec_tables_p2p_import.
+// Multi-process: this rank's peer-visible allocations, to be all-gathered
+// and passed to every rank's ec_tables_p2p_import.  Blob: CUDA IPC handles of
+// {shard (HBM), hot list, its gradients, its length, barrier words, inbox
+// indices, inbox gradients, inbox counts} (unused ones zero), then the host
+// shard's memfd as {pid, fd, bytes} (pinned-host tier; zeros for HBM).
+namespace {
+constexpr int kP2PHandles = 8;
+struct HostSeg {
+  int64_t pid, fd;
+  uint64_t bytes;
+  int64_t present;
+};
+constexpr uint64_t kP2PBlob = kP2PHandles * sizeof(cudaIpcMemHandle_t) + sizeof(HostSeg);
+}  // namespace
+
 int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len) {
   return guard([&] {
-    if (!t) invalid("null tables handle");
+    if (!t || !len) invalid("null argument");
     Engine& e = t->e;
     use_device(e.device);
     e.p2p_alloc();
-    void* ptrs[5] = {e.store_dev.p, e.ex->pub_slot.p, e.ex->pub_grad.p, e.ex->pub_cnt.p, e.ex->flags.p};
-    *len = sizeof(ptrs) / sizeof(ptrs[0]) * sizeof(cudaIpcMemHandle_t);
+    *len = kP2PBlob;
     if (!blob) return;
-    if (cap < *len) invalid("p2p export blob needs " + std::to_string(*len) + " bytes");
-    for (int k = 0; k < 5; ++k) {
+    if (cap < kP2PBlob) invalid("p2p export blob needs " + std::to_string(kP2PBlob) + " bytes");
+    std::memset(blob, 0, kP2PBlob);
+    const Exchange& x = *e.ex;
+    void* ptrs[kP2PHandles] = {e.store_dev.p, x.pub_slot.p,  x.pub_grad.p,   x.pub_cnt.p,
+                               x.flags.p,     x.inbox_idx.p, x.inbox_grad.p, x.inbox_cnt.p};
+    for (int k = 0; k < kP2PHandles; ++k) {
+      if (!ptrs[k]) continue;
       cudaIpcMemHandle_t h;
       EC_CUDA(cudaIpcGetMemHandle(&h, ptrs[k]));
       std::memcpy(blob + k * sizeof(h), &h, sizeof(h));
+    }
+    if (e.storage == EC_STORAGE_HOST) {
+      const HostSeg hs{static_cast<int64_t>(getpid()), e.store_host_fd, e.store_host_bytes, 1};
+      std::memcpy(blob + kP2PHandles * sizeof(cudaIpcMemHandle_t), &hs, sizeof(hs));
     }
   });
 }
@@ -855,25 +942,50 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
     if (!t || !blobs) invalid("null argument");
     Engine& e = t->e;
     if (e.world < 2) invalid("the peer-memory exchange needs world > 1");
-    if (blob_len != 5 * sizeof(cudaIpcMemHandle_t)) invalid("unexpected p2p blob size");
+    if (blob_len != kP2PBlob) invalid("unexpected p2p blob size");
     use_device(e.device);
     e.p2p_alloc();
+    Exchange& x = *e.ex;
     std::vector<PeerView> views(e.world);
     for (int p = 0; p < e.world; ++p) {
       if (p == e.rank) {
         views[p] = e.p2p_self();
         continue;
       }
-      void* ptrs[5];
-      for (int k = 0; k < 5; ++k) {
+      const uint8_t* b = blobs + p * blob_len;
+      void* ptrs[kP2PHandles] = {};
+      const cudaIpcMemHandle_t zero{};
+      for (int k = 0; k < kP2PHandles; ++k) {
         cudaIpcMemHandle_t h;
-        std::memcpy(&h, blobs + p * blob_len + k * sizeof(h), sizeof(h));
+        std::memcpy(&h, b + k * sizeof(h), sizeof(h));
+        if (std::memcmp(&h, &zero, sizeof(h)) == 0) continue;
         EC_CUDA(cudaIpcOpenMemHandle(&ptrs[k], h, cudaIpcMemLazyEnablePeerAccess));
-        e.ex->ipc_opened.push_back(ptrs[k]);
+        x.ipc_opened.push_back(ptrs[k]);
       }
-      views[p] = PeerView{static_cast<float*>(ptrs[0]), static_cast<const uint32_t*>(ptrs[1]),
-                          static_cast<const float*>(ptrs[2]), static_cast<const int*>(ptrs[3]),
-                          static_cast<unsigned*>(ptrs[4])};
+      HostSeg hs;
+      std::memcpy(&hs, b + kP2PHandles * sizeof(cudaIpcMemHandle_t), sizeof(hs));
+      if (hs.present != (e.storage == EC_STORAGE_HOST ? 1 : 0)) invalid("ranks disagree on the storage tier");
+      if (hs.present) {  // the peer's shard, mapped here and read over this GPU's own link
+        const std::string path = "/proc/" + std::to_string(hs.pid) + "/fd/" + std::to_string(hs.fd);
+        const int fd = open(path.c_str(), O_RDWR);
+        if (fd < 0) invalid("cannot open peer host shard " + path + " (peers must share a node)");
+        const uint64_t huge = 2ull << 20;
+        const size_t maplen = (hs.bytes + huge - 1) / huge * huge;
+        void* m = mmap(nullptr, maplen, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) invalid("cannot map peer host shard " + path);
+        if (cudaHostRegister(m, maplen, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+          cudaGetLastError();
+          munmap(m, maplen);
+          invalid("cannot register peer host shard " + path);
+        }
+        x.host_maps.emplace_back(m, maplen);
+        EC_CUDA(cudaHostGetDevicePointer(&ptrs[0], m, 0));
+      }
+      views[p] = PeerView{static_cast<float*>(ptrs[0]),        static_cast<const uint32_t*>(ptrs[1]),
+                          static_cast<const float*>(ptrs[2]),  static_cast<const int*>(ptrs[3]),
+                          static_cast<unsigned*>(ptrs[4]),     static_cast<uint32_t*>(ptrs[5]),
+                          static_cast<float*>(ptrs[6]),        static_cast<int*>(ptrs[7])};
     }
     e.p2p_set_peers(views);
   });

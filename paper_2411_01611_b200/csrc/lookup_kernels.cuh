@@ -417,11 +417,15 @@ __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __rest
                                                           const uint32_t* __restrict__ missq,
                                                           const uint32_t* __restrict__ uniq,
                                                           const uint16_t* __restrict__ utab, float* __restrict__ urows,
-                                                          int rank, int world) {
+                                                          int rank, int world,
+                                                          const PeerView* __restrict__ peers = nullptr,
+                                                          const int64_t* __restrict__ shard_off = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
-  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const Counters cs = counters(const_cast<int*>(ctr), T);
+  const int nm = *cs.miss_total;
+  int remote = 0;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
@@ -434,8 +438,15 @@ __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __rest
       if (q < nm) {
         const uint32_t g = missq[q];
         const uint32_t id = uniq[g];
-        if (static_cast<int>(id % world) == rank) {
-          const float* src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+        const int o = static_cast<int>(id % world);
+        const float* src = nullptr;
+        if (o == rank) {
+          src = td[utab[g]].store + static_cast<int64_t>(id / world) * D;
+        } else if (peers) {
+          src = peers[o].store + (shard_off[static_cast<int64_t>(o) * (T + 1) + utab[g]] + id / world) * D;
+          remote += m.c == 0;
+        }
+        if (src) {
           v[r] = *reinterpret_cast<const float4*>(src + m.c * 4);
           dst[r] = static_cast<int>(g);
         }
@@ -444,6 +455,10 @@ __global__ void __launch_bounds__(kThreads) k_gather_host(const TableDev* __rest
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (dst[r] >= 0) st4(urows + static_cast<int64_t>(dst[r]) * D + m.c * 4, v[r]);
+  }
+  if (peers) {
+    remote = __reduce_add_sync(kFull, remote);
+    if (remote && lane_id() == 0) atomicAdd(cs.wire, remote);
   }
 }
 

@@ -39,7 +39,8 @@ def _current_rows(members, t, ids, world, cached):
 
 
 @pytest.mark.parametrize("world,storage,p2p", [(2, "hbm", False), (3, "host", False), (4, "hbm", False),
-                                               (2, "hbm", True), (3, "hbm", True), (4, "hbm", True)])
+                                               (2, "hbm", True), (3, "hbm", True), (4, "hbm", True),
+                                               (2, "host", True), (3, "host", True)])
 def test_group_forward_backward(ec, torch, ref, world, storage, p2p):
     rows, D, B, P = [5000, 37, 20000, 1], 16, 64, 5
     n = B * P
@@ -137,15 +138,6 @@ def test_group_rejects_direct_calls(ec, torch):
     g.close()
     with pytest.raises(ec.ValidationError):  # world 2 without a transport
         ms[0].forward(ids, [0, 8], 8, 1)
-
-
-def test_group_p2p_rejects_host_tier(ec, torch):
-    ms = [ec.EmbeddingTables([100], 4, storage="host", rank=r, world=2, max_lookups_per_table=8, max_batch_size=8)
-          for r in range(2)]
-    with pytest.raises(ec.ValidationError):
-        ec.EmbeddingGroup(ms, p2p=True)
-    for m in ms:
-        m.close()
 
 
 def test_group_p2p_forward_only_steps(ec, torch):

@@ -31,11 +31,11 @@ def _free_port():
     return p
 
 
-def _setup(ec, rank, world):
+def _setup(ec, rank, world, storage):
     n = B * P
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in ROWS]
     caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, [40, 3, 200])]
-    m = ec.EmbeddingTables(ROWS, D, storage="hbm", rank=rank, world=world, max_lookups_per_table=n, max_batch_size=B)
+    m = ec.EmbeddingTables(ROWS, D, storage=storage, rank=rank, world=world, max_lookups_per_table=n, max_batch_size=B)
     m.init_synthetic(SEED, 0.1)
     return m, dists, caches
 
@@ -62,7 +62,7 @@ def _probe(m, rank, world, caches):
     return out
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, storage):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -71,7 +71,7 @@ def _worker(rank, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     try:
         import paper_2411_01611_b200 as ec
-        m, dists, caches = _setup(ec, rank, WORLD)
+        m, dists, caches = _setup(ec, rank, WORLD, storage)
         m.place_cache(caches)
         blobs = [None] * WORLD
         dist.all_gather_object(blobs, m.p2p_export())
@@ -95,11 +95,12 @@ def _worker(rank, port, q):
         dist.destroy_process_group()
 
 
-def test_p2p_ipc_two_processes_match_loopback(ec):
+@pytest.mark.parametrize("storage", ["hbm", "host"])
+def test_p2p_ipc_two_processes_match_loopback(ec, storage):
     import torch
     import torch.multiprocessing as mp
     # expected: the loopback group (staged copies) in this process
-    members, dists, caches = zip(*[_setup(ec, r, WORLD) for r in range(WORLD)])
+    members, dists, caches = zip(*[_setup(ec, r, WORLD, storage) for r in range(WORLD)])
     group = ec.EmbeddingGroup(members)
     for m in members:
         m.place_cache(caches[0])
@@ -120,7 +121,7 @@ def test_p2p_ipc_two_processes_match_loopback(ec):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, storage)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = {}
