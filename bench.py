@@ -165,14 +165,31 @@ def build_tables(ec, torch, wl, rank, world, device):
         tab.dedup_mode(MODES["dedup"])
     if MODES.get("scatter"):
         tab.scatter_mode(MODES["scatter"])
+    p2p_ok = False
     if world > 1 and exchange_kind(wl) == "p2p":
-        # peer-memory exchange: shards, hot lists and barrier words shared by CUDA IPC
+        # peer-memory exchange: shards, hot lists and barrier words shared by
+        # CUDA IPC (host shards by memfd); every rank must succeed, else NCCL
         import torch.distributed as dist
-        blobs = [None] * world
-        dist.all_gather_object(blobs, tab.p2p_export())
-        tab.p2p_import(blobs)
+        err = None
+        try:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, tab.p2p_export())
+            tab.p2p_import(blobs)
+        except ec.EmbcommError as e:
+            err = str(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        p2p_ok = not any(errs)
+        if not p2p_ok:
+            if MODES.get("exchange") == "p2p":
+                raise RuntimeError(f"peer-memory exchange unavailable: {errs}")
+            if rank == 0:
+                print(f"bench: peer-memory exchange unavailable ({[e for e in errs if e][0]}); using NCCL",
+                      file=sys.stderr)
+            tab.p2p_disable()
         dist.barrier()
-    elif world > 1:
+    MODES["exchange_used"] = "p2p" if p2p_ok else "nccl"
+    if world > 1 and not p2p_ok:
         import torch.distributed as dist
         uid = [ec.EmbeddingTables.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -516,7 +533,7 @@ def run_ours(args, wl):
                             "host-miss gather overlap this step and are inside its window, as is this step's "
                             "host write-back") if depth else
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
-                   "parallelism": f"row-sharded x{world}, owner = id % {world}, {exchange_kind(wl)} exchange"
+                   "parallelism": f"row-sharded x{world}, owner = id % {world}, {MODES.get('exchange_used')} exchange"
                    if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,

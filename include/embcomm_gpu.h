@@ -466,6 +466,9 @@ int ec_group_set_p2p(ec_group g, int enable);
  * device-side barrier. */
 int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len);
 int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len);
+/* Back to the transport set by ec_tables_attach_comm (e.g. when some rank's
+ * import failed: every rank must use the same transport). */
+int ec_tables_p2p_disable(ec_tables t);
 
 #ifdef __cplusplus
 }

@@ -187,6 +187,7 @@ _SIGS = {
     "ec_group_set_p2p": [vp, C.c_int],
     "ec_tables_p2p_export": [vp, vp, u64, P(u64)],
     "ec_tables_p2p_import": [vp, vp, u64],
+    "ec_tables_p2p_disable": [vp],
 }
 _RESTYPE = {
     "ec_last_error": C.c_char_p, "ec_version": C.c_char_p, "ec_cost_units_note": C.c_char_p,

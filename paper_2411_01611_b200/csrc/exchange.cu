@@ -937,6 +937,13 @@ int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len
   });
 }
 
+int ec_tables_p2p_disable(ec_tables t) {
+  return guard([&] {
+    if (!t) invalid("null tables handle");
+    if (t->e.ex) t->e.ex->p2p = false;
+  });
+}
+
 int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
   return guard([&] {
     if (!t || !blobs) invalid("null argument");

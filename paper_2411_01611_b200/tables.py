@@ -320,6 +320,11 @@ class EmbeddingTables:
         buf = (C.c_uint8 * len(raw)).from_buffer_copy(raw)
         check(N.lib().ec_tables_p2p_import(self._h, buf, len(blobs[0])))
 
+    def p2p_disable(self):
+        """Leave the peer-memory exchange (every rank must, e.g. after some
+        rank's import failed); attach_comm then selects NCCL."""
+        check(N.lib().ec_tables_p2p_disable(self._h))
+
 
 
 def shard_rows(rows: Sequence[int], world: int, rank: int) -> list[int]:
