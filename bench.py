@@ -270,6 +270,8 @@ def run_ours(args, wl):
     copy_stream = torch.cuda.Stream()
 
     depth = args.prefetch_depth
+    if world > 1 and MODES.get("exchange_used") != "p2p":
+        depth = 0  # ec_lookup_prefetch needs the peer-memory exchange at N>1
 
     def step(j, first=False):
         # pipelined training step: forward of batch j (its dedup and hit/miss
@@ -531,7 +533,10 @@ def run_ours(args, wl):
                    "step": ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD); pipelined "
                             f"(ec_lookup_prefetch depth {depth}): batch j+{depth}'s dedup/hit-miss and batch j+1's "
                             "host-miss gather overlap this step and are inside its window, as is this step's "
-                            "host write-back") if depth else
+                            "host write-back") if depth and world == 1 else
+                           ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD) + peer exchange; "
+                            "pipelined (ec_lookup_prefetch depth 1): batch j+1's dedup/hit-miss overlaps this step "
+                            "and is inside its window") if depth else
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
                    "parallelism": f"row-sharded x{world}, owner = id % {world}, {MODES.get('exchange_used')} exchange"
                    if world > 1 else "single GPU"},
@@ -692,10 +697,9 @@ def main():
     ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
                     help="N>1 transport (auto: p2p)")
     args = ap.parse_args()
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        args.prefetch = False  # ec_lookup_prefetch is single-rank (the exchange synchronises ranks per batch)
-    if args.prefetch_depth is None:
-        args.prefetch_depth = 2 if WORKLOADS[args.workload]["storage"] == "host" else 1
+    multi = int(os.environ.get("WORLD_SIZE", "1")) > 1
+    if args.prefetch_depth is None:  # (N>1: the next batch's dedup only; rows are read after the step barrier)
+        args.prefetch_depth = 2 if WORKLOADS[args.workload]["storage"] == "host" and not multi else 1
     if not args.prefetch:
         args.prefetch_depth = 0
     MODES.update(dedup=args.dedup_mode, scatter=args.scatter_mode, exchange=args.exchange)

@@ -885,6 +885,20 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
   const int h = head_pending();
   if (h >= 0) {
     BatchBufs& nx = bb[h];
+    if (nx.indices == b.indices_dev && nx.geom_version == geom_version && world > 1) {
+      // peer exchange: only the dedup / hit-miss ran ahead; rows are read
+      // once every rank applied the previous step
+      nx.pending = false;
+      EC_CUDA(cudaEventRecord(bb[cur].ev_free, st));
+      select(h);
+      EC_CUDA(cudaStreamWaitEvent(st, nx.ev_ded, 0));
+      p2p_fwd_begin(st);
+      gather_local(st);
+      pool(st);
+      p2p_signal(2, st);
+      have_fwd = true;
+      return;
+    }
     if (nx.indices == b.indices_dev && nx.geom_version == geom_version) {
       // dedup, hit/miss and host-miss gather already ran (ec_lookup_prefetch)
       nx.pending = false;
@@ -945,7 +959,8 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
 // into the gathered copy.  Up to kSets-1 batches may be pending; forwards
 // consume them in prefetch order.
 void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
-  if (in_group || world > 1) invalid("prefetch is single-rank only");
+  if (in_group || (world > 1 && !p2p_on()))
+    invalid("prefetch needs a single rank or the peer-memory exchange");
   if (!have_geom || !b.indices_dev || !b.table_offsets_host) invalid("prefetch needs a batch with the current geometry");
   bool same = b.batch_size == geom_b && b.pooling == geom_p && (b.bag_offsets_dev == nullptr) == geom_fixed &&
               b.bag_offsets_dev == bag_off;
@@ -963,7 +978,8 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // this prefetch (e.g. the copy that produced these indices) comes first
   EC_CUDA(cudaEventRecord(ev_pfcall, st));
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_pfcall, 0));
-  const bool gather_now = storage == EC_STORAGE_HOST && next_in_line;
+  // (peer exchange: rows are read after the step's barrier, in the forward)
+  const bool gather_now = storage == EC_STORAGE_HOST && next_in_line && world == 1;
   const int saved = cur;
   select(s);
   try {
@@ -982,7 +998,7 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   }
   BatchBufs& nb = bb[s];
   nb.pending = true;
-  nb.gathered = storage != EC_STORAGE_HOST || gather_now;
+  nb.gathered = storage != EC_STORAGE_HOST || gather_now || world > 1;
   nb.seq = ++pf_seq;
   nb.indices = b.indices_dev;
   nb.geom_version = geom_version;

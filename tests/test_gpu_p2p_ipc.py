@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ROWS, D, B, P, SEED, LR = [5000, 37, 20000], 16, 64, 5, 7, 0.25
-WORLD, STEPS = 2, 2
+WORLD, STEPS = 2, 3
 PROBE = 400  # rows per table read back at the end
 
 
@@ -62,7 +62,7 @@ def _probe(m, rank, world, caches):
     return out
 
 
-def _worker(rank, port, q, storage):
+def _worker(rank, port, q, storage, prefetch):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -79,9 +79,12 @@ def _worker(rank, port, q, storage):
         dist.barrier()
         offs = np.arange(len(ROWS) + 1, dtype=np.int64) * (B * P)
         outs = []
+        batches = [_batch(ec, torch, dists, rank, step) for step in range(STEPS)]
         for step in range(STEPS):
-            ids, grad = _batch(ec, torch, dists, rank, step)
+            ids, grad = batches[step]
             outs.append(m.forward(ids, offs, B, P).cpu().numpy())
+            if prefetch and step + 1 < STEPS:  # next batch's dedup overlaps this backward
+                m.prefetch(batches[step + 1][0], offs, B, P)
             m.backward(grad, LR)
         torch.cuda.synchronize()
         dist.barrier()
@@ -95,8 +98,8 @@ def _worker(rank, port, q, storage):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("storage", ["hbm", "host"])
-def test_p2p_ipc_two_processes_match_loopback(ec, storage):
+@pytest.mark.parametrize("storage,prefetch", [("hbm", False), ("host", False), ("hbm", True), ("host", True)])
+def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch):
     import torch
     import torch.multiprocessing as mp
     # expected: the loopback group (staged copies) in this process
@@ -121,7 +124,7 @@ def test_p2p_ipc_two_processes_match_loopback(ec, storage):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q, storage)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, storage, prefetch)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = {}
