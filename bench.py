@@ -369,7 +369,11 @@ def run_ours(args, wl):
 
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
-    NS = depth + 2  # device id slots: step k+depth+1's copy runs during step k
+    # input pipeline: step k+LA's ids are copied during step k (two steps of
+    # slack: ec_copy_async pulls pinned host ids with a few CTAs, ~1 step long)
+    LA = depth + 2
+    NS = 6  # device id slots (> LA; a multiple of the engine's 3 buffer sets, so the
+    #         graphs of every (set, slot) pair are captured by the untimed warm-up)
     dev_ids = [torch.empty_like(ids[0]) for _ in range(NS)]
     counters = None
     e2e_start = torch.cuda.Event(enable_timing=True)
@@ -387,11 +391,11 @@ def run_ours(args, wl):
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
 
     def e2e_steps(nsteps, marks=None):
-        # input pipelining: step k+depth+1's H2D runs during step k, so a
-        # prefetch never waits on the link; every step still moves its own ids
+        # input pipelining: step k+LA's H2D runs during step k, so a prefetch
+        # never waits on the link; every step still moves its own ids
         # host->device and reads its result back
         tab.prefetch_drop()  # this loop primes its own pipeline
-        for k in range(min(nsteps, depth + 1)):
+        for k in range(min(nsteps, LA)):
             h2d(k)
         for k in range(min(nsteps, depth)):
             tab.prefetch(dev_ids[k % NS], offs, B, P, stream=copy_stream)
@@ -404,8 +408,8 @@ def run_ours(args, wl):
             consumed[k % NS].record(stream)
             if depth and k + depth < nsteps:
                 tab.prefetch(dev_ids[(k + depth) % NS], offs, B, P, stream=copy_stream)  # after its H2D copy
-            if k + depth + 1 < nsteps:
-                h2d(k + depth + 1)  # (after the prefetch above, which orders itself after the copy stream)
+            if k + LA < nsteps:
+                h2d(k + LA)  # (after the prefetch above, which orders itself after the copy stream)
             tab.backward(o, LR)
             # D2H of the step's result (per-table unique/miss counts) into a
             # pinned ring slot; decoded two steps later, like an async loss log

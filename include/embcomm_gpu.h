@@ -235,7 +235,10 @@ void ec_trace_destroy(ec_trace t);
 int ec_trace_info(ec_trace t, uint64_t* num_samples, int64_t* num_features, uint64_t* vocab);
 int ec_trace_ids(ec_trace t, const uint32_t** ids_host);  /* valid until ec_trace_destroy */
 /* stream-ordered copy between UVA addresses (pinned host <-> device), e.g. a
- * step's ids onto the GPU: cudaMemcpyAsync(cudaMemcpyDefault) in one call */
+ * step's ids onto the GPU.  Pinned (mapped) host -> device with 16-byte
+ * aligned ends is pulled by a few CTAs' loads (EC_H2D_CTAS, default 8; 0 =
+ * copy engine), which shares the host link with the cold tier's row reads far
+ * better than a copy-engine burst; other cases are cudaMemcpyAsync. */
 int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 /* samples [first, first+count) -> ids_dev (count*d ids) through pinned
  * double-buffered staging on `stream`; returns when the copies are done */

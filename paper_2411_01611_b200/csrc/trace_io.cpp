@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -107,15 +108,79 @@ struct ec_trace_s {
   TraceFile f;
 };
 
+namespace ec {
+namespace {
+
+// Pinned host -> device by SM loads of the mapped source, from a few CTAs.
+// The host link is shared with the cold tier's random 64 B row reads; a
+// copy-engine burst of the next batch's ids starves those (measured with
+// tools/hostlink_bench: 7187 rows 35 -> 63 us beside a 1.7 MB
+// cudaMemcpyAsync) while an 8-CTA pull leaves them at 46 us and lands in
+// ~66 us, within a step.  Kaggle e2e step (bench.py, interleaved runs on one
+// box): copy engine 0.132 ms, 4 CTAs 0.130-0.146, 8 CTAs 0.101-0.107,
+// 16 CTAs 0.125-0.133.
+__global__ void k_h2d_pull(const int4* __restrict__ src, int4* __restrict__ dst, uint64_t n16,
+                           const uint8_t* __restrict__ src_tail, uint8_t* __restrict__ dst_tail, int tail) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16; i += stride)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+
+int h2d_ctas() {
+  static const int n = [] {
+    const char* v = std::getenv("EC_H2D_CTAS");
+    return v ? std::max(0, std::atoi(v)) : 8;
+  }();
+  return n;
+}
+
+// Device address of a pinned, mapped host buffer, else nullptr.
+const void* mapped_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+bool is_device(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice;
+}
+
+}  // namespace
+}  // namespace ec
+
 extern "C" {
 
 // Stream-ordered copy between any two UVA addresses (pinned host <-> device):
 // the input-pipeline primitive of a training loop, with one call's host cost.
+// Pinned host -> device goes through k_h2d_pull (EC_H2D_CTAS CTAs, default 8;
+// 0 selects the copy engine), everything else through cudaMemcpyAsync.
 int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
   return guard([&] {
     if (!bytes) return;
     if (!dst || !src) invalid("null argument");
-    EC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int ctas = h2d_ctas();
+    const void* msrc = ctas ? mapped_host(src) : nullptr;
+    if (msrc && is_device(dst) && (reinterpret_cast<uintptr_t>(msrc) % 16) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst) % 16) == 0) {
+      const uint64_t n16 = bytes / 16;
+      const int tail = static_cast<int>(bytes % 16);
+      k_h2d_pull<<<ctas, 512, 0, st>>>(static_cast<const int4*>(msrc), static_cast<int4*>(dst), n16,
+                                       static_cast<const uint8_t*>(msrc) + n16 * 16,
+                                       static_cast<uint8_t*>(dst) + n16 * 16, tail);
+      EC_CUDA(cudaGetLastError());
+      return;
+    }
+    EC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
   });
 }
 

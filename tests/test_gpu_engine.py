@@ -403,3 +403,23 @@ def test_copy_async_and_prefetch_drop(ec, torch):
     u, _ = O.dedup(ids.cpu().numpy().view(np.uint32)[:B])
     assert (tab.export_unique(0) == u).all()
     tab.close()
+
+
+@pytest.mark.parametrize("nbytes,offset", [(1, 0), (15, 0), (16, 0), (17, 0), (1000, 4), (1703936, 0),
+                                           (1703939, 0), (4096, 8)])
+def test_copy_async_pull_and_fallback(ec, torch, nbytes, offset):
+    """Pinned host -> device runs as the SM pull kernel (16-byte aligned ends:
+    int4 body + byte tail), misaligned ones and device -> host through the
+    copy engine; every path is byte-exact."""
+    g = torch.Generator().manual_seed(nbytes)
+    src = torch.randint(0, 256, (nbytes + offset,), dtype=torch.uint8, generator=g).pin_memory()
+    dst = torch.zeros(nbytes + offset, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    ec.copy_async(dst[offset:], src[offset:], s)
+    s.synchronize()
+    assert torch.equal(dst[offset:].cpu(), src[offset:])
+    assert int(dst[:offset].sum()) == 0  # nothing written before the destination
+    back = torch.zeros(nbytes, dtype=torch.uint8).pin_memory()
+    ec.copy_async(back, dst[offset:], s)
+    s.synchronize()
+    assert torch.equal(back, src[offset:])

@@ -2,7 +2,7 @@
 // B200 and pinned host memory, the pattern of the cold tier (k_gather_host /
 // k_apply_host).  Built by tools/Makefile, run under gpurun.
 //
-//   ./hostlink_bench [numa_node|-1] [rows] [alloc: mmap|cuda|hugetlb]
+//   ./hostlink_bench [numa_node|-1] [rows] [alloc: mmap|cuda|hugetlb] [interference]
 //
 // Prints the GPU's NUMA node, sequential H2D/D2H copy bandwidth, and the time
 // of an LSU gather / scatter of `rows` random rows at several grid sizes.
@@ -43,6 +43,67 @@ __global__ void k_write(float4* __restrict__ host, const uint32_t* __restrict__ 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * VEC; i += lanes) {
     const int r = i / VEC, c = i % VEC;
     host[static_cast<size_t>(idx[r]) * VEC + c] = in[i];
+  }
+}
+
+// ids-style bulk stream (pinned host -> device) by SM loads, few CTAs
+__global__ void k_stream(const int4* __restrict__ src, int4* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Row reads (7187 x 64 B, grid 16, as k_gather_host) alone and beside a 1.7 MB
+// bulk H2D transfer: copy engine vs SM loads at several CTA counts.
+static void interference(float4* host, int rows_total, void* bulk_host) {
+  const int n = 7187;
+  const size_t bulk = 1703936;
+  std::mt19937 rng(11);
+  std::vector<uint32_t> idx(n);
+  for (auto& x : idx) x = rng() % rows_total;
+  uint32_t* didx;
+  float4* buf;
+  void* dbulk;
+  CK(cudaMalloc(&didx, n * 4));
+  CK(cudaMalloc(&buf, static_cast<size_t>(n) * 64));
+  CK(cudaMalloc(&dbulk, bulk));
+  CK(cudaMemcpy(didx, idx.data(), n * 4, cudaMemcpyHostToDevice));
+  int4* bulk_dev_view;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&bulk_dev_view), bulk_host, 0));
+  cudaStream_t s1, s2;
+  CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaEvent_t a, b, c, d;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventCreate(&c));
+  CK(cudaEventCreate(&d));
+  for (int mode = 0; mode < 6; ++mode) {  // 0 alone, 1 copy engine, 2.. SM stream with 1,2,4,8 CTAs
+    float best_r = 1e9f, best_t = 1e9f, best_b = 1e9f;
+    for (int it = 0; it < 10; ++it) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(a, s1));
+      CK(cudaStreamWaitEvent(s2, a, 0));
+      if (mode == 1) CK(cudaMemcpyAsync(dbulk, bulk_host, bulk, cudaMemcpyHostToDevice, s2));
+      if (mode >= 2)
+        k_stream<<<1 << (mode - 2), 512, 0, s2>>>(bulk_dev_view, static_cast<int4*>(dbulk), bulk / 16);
+      CK(cudaEventRecord(c, s2));
+      k_read<4><<<16, 256, 0, s1>>>(host, didx, n, buf);
+      CK(cudaEventRecord(b, s1));
+      CK(cudaStreamWaitEvent(s1, c, 0));
+      CK(cudaEventRecord(d, s1));
+      CK(cudaEventSynchronize(d));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best_r = std::min(best_r, ms);
+      CK(cudaEventElapsedTime(&ms, a, c));
+      best_b = std::min(best_b, ms);
+      CK(cudaEventElapsedTime(&ms, a, d));
+      best_t = std::min(best_t, ms);
+    }
+    const char* names[] = {"rows alone", "rows + copy engine 1.7MB", "rows + SM stream 1 CTA", "rows + SM stream 2 CTAs",
+                           "rows + SM stream 4 CTAs", "rows + SM stream 8 CTAs"};
+    std::printf("  %-28s rows %7.1f us  bulk %7.1f us  both %7.1f us\n", names[mode], best_r * 1e3,
+                mode ? best_b * 1e3 : 0.f, best_t * 1e3);
   }
 }
 
@@ -202,6 +263,13 @@ int main(int argc, char** argv) {
     std::printf("sequential 256 MiB: H2D %.1f GB/s  D2H %.1f GB/s\n", 0.256 * 1.048576 / (h2d * 1e-3),
                 0.256 * 1.048576 / (d2h * 1e-3));
     CK(cudaFree(d));
+  }
+  if (argc > 4 && std::string(argv[4]) == "interference") {
+    void* bulk_host;
+    CK(cudaHostAlloc(&bulk_host, 1703936, cudaHostAllocMapped));
+    std::memset(bulk_host, 1, 1703936);
+    interference(host, static_cast<int>(bytes / 64), bulk_host);
+    return 0;
   }
   run<4>(host, static_cast<int>(bytes / 64), n, 64);
   run<4>(host, static_cast<int>(bytes / 64), n * 8, 64);
