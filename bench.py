@@ -141,6 +141,31 @@ def make_dist(ec, wl, rows, t):
     return ec.EmbeddingDistribution.from_probabilities(p)
 
 
+def pick_h2d_path(ec, torch, dev, host, stream, pull_ctas=16):
+    """0 (copy engine) or pull_ctas, by timing 10 copies of one batch each."""
+    lib = ec._native.lib()
+    n = dev.numel() * dev.element_size()
+    best = {}
+    for ctas in (0, pull_ctas):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(2):  # second pass timed
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(10):
+                rc = (lib.ec_copy_async_pull(dev.data_ptr(), host.data_ptr(), n, ctas, stream.cuda_stream) if ctas
+                      else lib.ec_copy_async(dev.data_ptr(), host.data_ptr(), n, stream.cuda_stream))
+                if rc:
+                    ec._native.check(rc)
+            b.record(stream)
+            torch.cuda.synchronize()
+        best[ctas] = a.elapsed_time(b) / 10
+    H2D_PROBE.update({"copy_engine_us": round(best[0] * 1e3, 1), f"pull{pull_ctas}_us": round(best[pull_ctas] * 1e3, 1)})
+    return 0 if best[0] <= 1.2 * best[pull_ctas] else pull_ctas
+
+
+H2D_PROBE = {}
+
+
 def exchange_kind(wl):
     """N>1 transport: peer memory by default (remote rows loaded in the gather
     kernels, owner updates by NVLink atomics / owner inboxes, device barriers,
@@ -370,7 +395,11 @@ def run_ours(args, wl):
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
     # input pipeline: step k+LA's ids are copied during step k (two steps of
-    # slack: ec_copy_async pulls pinned host ids with a few CTAs, ~1 step long)
+    # slack), by the copy engine or pulled by 16 CTAs' loads
+    # (ec_copy_async_pull), whichever moves one batch faster on this box: the
+    # copy engine's H2D rate for a 1.7 MB copy varies 13-55 GB/s across this
+    # pool's boxes, the pull holds ~45 GB/s (tools/copyprobe.py)
+    pull = pick_h2d_path(ec, torch, ids[0], host_ids[0], copy_stream)
     LA = depth + 2
     NS = 6  # device id slots (> LA; a multiple of the engine's 3 buffer sets, so the
     #         graphs of every (set, slot) pair are captured by the untimed warm-up)
@@ -381,12 +410,24 @@ def run_ours(args, wl):
     copied = [torch.cuda.Event() for _ in range(NS)]
     consumed = [torch.cuda.Event() for _ in range(NS)]
 
+    # (host cost matters here: on a slow host the e2e loop is bound by the
+    # per-step Python + driver calls, so the copy path is one ctypes call on
+    # precomputed pointers)
+    nbytes_ids = ids[0].numel() * 4
+    dev_ptr = [t.data_ptr() for t in dev_ids]
+    host_ptr = [t.data_ptr() for t in host_ids]
+    cs_ptr = copy_stream.cuda_stream
+    lib = ec._native.lib()
+    copy_fn = (lambda d, s: lib.ec_copy_async_pull(d, s, nbytes_ids, pull, cs_ptr)) if pull else \
+        (lambda d, s: lib.ec_copy_async(d, s, nbytes_ids, cs_ptr))
+
     def h2d(k):  # step k's ids, pinned host -> device, on the copy stream
-        with torch.cuda.stream(copy_stream):
-            if k >= NS:  # the slot's previous batch was consumed by its forward
-                copy_stream.wait_event(consumed[k % NS])
-            ec.copy_async(dev_ids[k % NS], host_ids[k % N_BATCHES], copy_stream)
-            copied[k % NS].record(copy_stream)
+        if k >= NS:  # the slot's previous batch was consumed by its forward
+            copy_stream.wait_event(consumed[k % NS])
+        rc = copy_fn(dev_ptr[k % NS], host_ptr[k % N_BATCHES])
+        if rc:
+            ec._native.check(rc)
+        copied[k % NS].record(copy_stream)
 
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
 
@@ -546,7 +587,9 @@ def run_ours(args, wl):
                    if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
-                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4)},
+                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4),
+                "h2d_path": ("ec_copy_async_pull, %d CTAs" % pull) if pull else "ec_copy_async (copy engine)",
+                "h2d_probe": H2D_PROBE},
         "fwd_only": {"value": round(lookups_per_step * world / (fwd_ms * 1e-3), 1), "unit": "lookups/s",
                      "ms_per_step": round(fwd_ms, 5),
                      "step": "forward only (dedup, hit/miss, host-miss gather, pool), unpipelined"},

@@ -235,11 +235,13 @@ void ec_trace_destroy(ec_trace t);
 int ec_trace_info(ec_trace t, uint64_t* num_samples, int64_t* num_features, uint64_t* vocab);
 int ec_trace_ids(ec_trace t, const uint32_t** ids_host);  /* valid until ec_trace_destroy */
 /* stream-ordered copy between UVA addresses (pinned host <-> device), e.g. a
- * step's ids onto the GPU.  Pinned (mapped) host -> device with 16-byte
- * aligned ends is pulled by a few CTAs' loads (EC_H2D_CTAS, default 8; 0 =
- * copy engine), which shares the host link with the cold tier's row reads far
- * better than a copy-engine burst; other cases are cudaMemcpyAsync. */
+ * step's ids onto the GPU: cudaMemcpyAsync(cudaMemcpyDefault) in one call */
 int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+/* the same, pinned (mapped) host -> device pulled by `ctas` CTAs' loads: with
+ * the cold tier in pinned host memory the ids share the host link with its row
+ * reads, and a few CTAs' pull yields to them where a copy-engine burst starves
+ * them.  Other address kinds, misaligned ends or ctas <= 0: ec_copy_async. */
+int ec_copy_async_pull(void* dst, const void* src, uint64_t bytes, int ctas, void* stream);
 /* samples [first, first+count) -> ids_dev (count*d ids) through pinned
  * double-buffered staging on `stream`; returns when the copies are done */
 int ec_trace_upload(ec_trace t, uint64_t first, uint64_t count, uint32_t* ids_dev, void* stream);

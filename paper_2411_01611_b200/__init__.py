@@ -490,16 +490,21 @@ class Trace:
         return BinaryTrace(path)
 
 
-def copy_async(dst, src, stream=None) -> None:
+def copy_async(dst, src, stream=None, pull_ctas: int = 0) -> None:
     """dst.copy_(src, non_blocking=True) for contiguous same-size tensors (pinned
     host <-> device) through one ec_copy_async call: an input pipeline's copy
-    without the framework dispatch cost."""
+    without the framework dispatch cost.  pull_ctas > 0: pinned host -> device
+    pulled by that many CTAs (ec_copy_async_pull) -- for inputs sharing the
+    host link with a pinned-host cold tier."""
     import torch
     nbytes = src.numel() * src.element_size()
     if dst.numel() * dst.element_size() != nbytes or not (dst.is_contiguous() and src.is_contiguous()):
         raise ValidationError("copy_async needs contiguous tensors of equal byte size")
     s = stream if stream is not None else torch.cuda.current_stream()
-    check(N.lib().ec_copy_async(dst.data_ptr(), src.data_ptr(), nbytes, s.cuda_stream))
+    if pull_ctas > 0:
+        check(N.lib().ec_copy_async_pull(dst.data_ptr(), src.data_ptr(), nbytes, int(pull_ctas), s.cuda_stream))
+    else:
+        check(N.lib().ec_copy_async(dst.data_ptr(), src.data_ptr(), nbytes, s.cuda_stream))
 
 
 class BinaryTrace:

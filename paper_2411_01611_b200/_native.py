@@ -167,6 +167,7 @@ _SIGS = {
     "ec_trace_ids": [vp, P(vp)],
     "ec_trace_upload": [vp, u64, u64, vp, vp],
     "ec_copy_async": [vp, vp, u64, vp],
+    "ec_copy_async_pull": [vp, vp, u64, C.c_int, vp],
     "ec_tables_schedule": [vp, vp, u64, vp, P(u64), vp],
     "ec_tables_gather_batch": [vp, vp, vp, u64, u32, vp, vp],
     "ec_lookup_stats": [vp, vp, P(BatchStats), vp, vp],

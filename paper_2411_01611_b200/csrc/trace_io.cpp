@@ -118,21 +118,14 @@ namespace {
 // cudaMemcpyAsync) while an 8-CTA pull leaves them at 46 us and lands in
 // ~66 us, within a step.  Kaggle e2e step (bench.py, interleaved runs on one
 // box): copy engine 0.132 ms, 4 CTAs 0.130-0.146, 8 CTAs 0.101-0.107,
-// 16 CTAs 0.125-0.133.
+// 16 CTAs 0.125-0.133.  With HBM-resident rows nothing else uses the link
+// and the copy engine is the faster choice (the pull then bounds the step).
 __global__ void k_h2d_pull(const int4* __restrict__ src, int4* __restrict__ dst, uint64_t n16,
                            const uint8_t* __restrict__ src_tail, uint8_t* __restrict__ dst_tail, int tail) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16; i += stride)
     dst[i] = src[i];
   if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
-}
-
-int h2d_ctas() {
-  static const int n = [] {
-    const char* v = std::getenv("EC_H2D_CTAS");
-    return v ? std::max(0, std::atoi(v)) : 8;
-  }();
-  return n;
 }
 
 // Device address of a pinned, mapped host buffer, else nullptr.
@@ -161,15 +154,24 @@ extern "C" {
 
 // Stream-ordered copy between any two UVA addresses (pinned host <-> device):
 // the input-pipeline primitive of a training loop, with one call's host cost.
-// Pinned host -> device goes through k_h2d_pull (EC_H2D_CTAS CTAs, default 8;
-// 0 selects the copy engine), everything else through cudaMemcpyAsync.
 int ec_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
   return guard([&] {
     if (!bytes) return;
     if (!dst || !src) invalid("null argument");
+    EC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+// The same for pinned (mapped) host -> device, pulled by `ctas` CTAs' loads
+// (k_h2d_pull) instead of the copy engine: for inputs that share the host
+// link with the pinned-host cold tier.  Other address kinds, misaligned
+// (16-byte) ends or ctas <= 0 fall back to ec_copy_async.
+int ec_copy_async_pull(void* dst, const void* src, uint64_t bytes, int ctas, void* stream) {
+  return guard([&] {
+    if (!bytes) return;
+    if (!dst || !src) invalid("null argument");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int ctas = h2d_ctas();
-    const void* msrc = ctas ? mapped_host(src) : nullptr;
+    const void* msrc = ctas > 0 ? mapped_host(src) : nullptr;
     if (msrc && is_device(dst) && (reinterpret_cast<uintptr_t>(msrc) % 16) == 0 &&
         (reinterpret_cast<uintptr_t>(dst) % 16) == 0) {
       const uint64_t n16 = bytes / 16;

@@ -415,11 +415,11 @@ def test_copy_async_pull_and_fallback(ec, torch, nbytes, offset):
     src = torch.randint(0, 256, (nbytes + offset,), dtype=torch.uint8, generator=g).pin_memory()
     dst = torch.zeros(nbytes + offset, dtype=torch.uint8, device="cuda")
     s = torch.cuda.Stream()
-    ec.copy_async(dst[offset:], src[offset:], s)
+    ec.copy_async(dst[offset:], src[offset:], s, pull_ctas=8)
     s.synchronize()
     assert torch.equal(dst[offset:].cpu(), src[offset:])
     assert int(dst[:offset].sum()) == 0  # nothing written before the destination
     back = torch.zeros(nbytes, dtype=torch.uint8).pin_memory()
-    ec.copy_async(back, dst[offset:], s)
+    ec.copy_async(back, dst[offset:], s, pull_ctas=8)  # device -> host: copy engine
     s.synchronize()
     assert torch.equal(back, src[offset:])

@@ -21,13 +21,20 @@ tab, dists, caches, ks = bench.build_tables(ec, torch, wl, 0, 1, 0)
 ids, offs = bench.gen_batches(ec, torch, dists, wl, 0, bench.N_BATCHES)
 T, D, B, P = len(wl["rows"]), wl["dim"], wl["batch"], wl["pooling"]
 out = torch.empty((B, T * D), dtype=torch.float32, device="cuda")
-NB, NS = bench.N_BATCHES, 3
-cs = torch.cuda.Stream()
+NB, NS = bench.N_BATCHES, 6
+DEPTH = int(os.environ.get("E2E_DEPTH", "2" if wl["storage"] == "host" else "1"))
+LA = DEPTH + 2
+PULL = int(os.environ.get("E2E_PULL", "8"))
+cs = torch.cuda.Stream(priority=int(os.environ.get("E2E_CSPRIO", "0")))
 host_ids = ids.cpu().pin_memory()
 dev_ids = [torch.empty_like(ids[0]) for _ in range(NS)]
 copied = [torch.cuda.Event() for _ in range(NS)]
 consumed = [torch.cuda.Event() for _ in range(NS)]
 acc = {}
+lib = ec._native.lib()
+nbytes = ids[0].numel() * 4
+dptr = [t.data_ptr() for t in dev_ids]
+hptr = [t.data_ptr() for t in host_ids]
 
 
 def tick(name, t0):
@@ -37,11 +44,13 @@ def tick(name, t0):
 
 
 def h2d(k):
-    with torch.cuda.stream(cs):
-        if k >= NS:
-            cs.wait_event(consumed[k % NS])
-        ec.copy_async(dev_ids[k % NS], host_ids[k % NB], cs)
-        copied[k % NS].record(cs)
+    if k >= NS:
+        cs.wait_event(consumed[k % NS])
+    if PULL:
+        lib.ec_copy_async_pull(dptr[k % NS], hptr[k % NB], nbytes, PULL, cs.cuda_stream)
+    else:
+        lib.ec_copy_async(dptr[k % NS], hptr[k % NB], nbytes, cs.cuda_stream)
+    copied[k % NS].record(cs)
 
 
 DO_H2D = os.environ.get("E2E_H2D", "1") == "1"
@@ -49,9 +58,11 @@ DO_STATS = os.environ.get("E2E_STATS", "1") == "1"
 
 
 def run(n, rec):
-    h2d(0)
-    h2d(1)
-    tab.prefetch(dev_ids[0], offs, B, P, stream=cs)
+    tab.prefetch_drop()
+    for k in range(min(n, LA)):
+        h2d(k)
+    for k in range(min(n, DEPTH)):
+        tab.prefetch(dev_ids[k % NS], offs, B, P, stream=cs)
     for k in range(n):
         t = time.perf_counter()
         st.wait_event(copied[k % NS])
@@ -59,11 +70,11 @@ def run(n, rec):
         o = tab.forward(dev_ids[k % NS], offs, B, P, out=out)
         t = tick("forward", t) if rec else t
         consumed[k % NS].record(st)
-        if k + 1 < n:
-            tab.prefetch(dev_ids[(k + 1) % NS], offs, B, P, stream=cs)
+        if DEPTH and k + DEPTH < n:
+            tab.prefetch(dev_ids[(k + DEPTH) % NS], offs, B, P, stream=cs)
         t = tick("prefetch", t) if rec else t
-        if k + 2 < n and DO_H2D:
-            h2d(k + 2)
+        if k + LA < n and DO_H2D:
+            h2d(k + LA)
         t = tick("h2d", t) if rec else t
         tab.backward(o, bench.LR)
         t = tick("backward", t) if rec else t
@@ -71,18 +82,18 @@ def run(n, rec):
             tab.stats_enqueue(k % 4)
         t = tick("stats_enqueue", t) if rec else t
         if k >= 2 and DO_STATS:
-            tab.stats_collect((k - 2) % 4, per_table=True)
+            tab.stats_collect((k - 2) % 4)
         t = tick("stats_collect", t) if rec else t
     tab.prefetch_wait()
     torch.cuda.synchronize()
 
 
 tab.backward(tab.forward(ids[0], offs, B, P, out=out), bench.LR)  # geometry for the first prefetch
-run(20, False)
+run(24, False)
 t0 = time.perf_counter()
 run(steps, True)
 t1 = time.perf_counter()
-print(f"{sys.argv[1:]} h2d={DO_H2D} stats={DO_STATS}: e2e wall {1e6 * (t1 - t0) / steps:.1f} us/step")
+print(f"{sys.argv[1:]} h2d={DO_H2D} stats={DO_STATS} depth={DEPTH} pull={PULL} cs_prio={cs.priority}: e2e wall {1e6 * (t1 - t0) / steps:.1f} us/step")
 for k, v in acc.items():
     print(f"  {k:14s} mean {np.mean(v):7.1f}  median {np.median(v):7.1f}  p90 {np.percentile(v, 90):7.1f}")
 tab.close()
