@@ -953,6 +953,11 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
     use_device(e.device);
     e.p2p_alloc();
     Exchange& x = *e.ex;
+    for (int p = 0; p < e.world; ++p) {  // validate every blob before opening any handle
+      HostSeg hs;
+      std::memcpy(&hs, blobs + p * blob_len + kP2PHandles * sizeof(cudaIpcMemHandle_t), sizeof(hs));
+      if (hs.present != (e.storage == EC_STORAGE_HOST ? 1 : 0)) invalid("ranks disagree on the storage tier");
+    }
     std::vector<PeerView> views(e.world);
     for (int p = 0; p < e.world; ++p) {
       if (p == e.rank) {
@@ -971,7 +976,6 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
       }
       HostSeg hs;
       std::memcpy(&hs, b + kP2PHandles * sizeof(cudaIpcMemHandle_t), sizeof(hs));
-      if (hs.present != (e.storage == EC_STORAGE_HOST ? 1 : 0)) invalid("ranks disagree on the storage tier");
       if (hs.present) {  // the peer's shard, mapped here and read over this GPU's own link
         const std::string path = "/proc/" + std::to_string(hs.pid) + "/fd/" + std::to_string(hs.fd);
         const int fd = open(path.c_str(), O_RDWR);

@@ -174,3 +174,30 @@ def test_group_p2p_forward_only_steps(ec, torch):
     g.close()
     for m in ms:
         m.close()
+
+
+def test_p2p_import_validation(ec, torch):
+    """ec_tables_p2p_import refuses a single rank, wrong blob sizes, a blob
+    count that is not the world size and ranks on different tiers; p2p_disable
+    returns a rank to 'no transport'."""
+    one = ec.EmbeddingTables([100], 4, max_lookups_per_table=8, max_batch_size=8)
+    with pytest.raises(ec.ValidationError):
+        one.p2p_import([one.p2p_export()])
+    one.close()
+    hb = [ec.EmbeddingTables([100], 4, storage="hbm", rank=r, world=2, max_lookups_per_table=8, max_batch_size=8)
+          for r in range(2)]
+    ho = ec.EmbeddingTables([100], 4, storage="host", rank=1, world=2, max_lookups_per_table=8, max_batch_size=8)
+    blobs = [m.p2p_export() for m in hb]
+    assert len(blobs[0]) == 544
+    with pytest.raises(ValueError):
+        hb[0].p2p_import(blobs[:1])
+    with pytest.raises(ValueError):
+        hb[0].p2p_import([blobs[0], blobs[1][:-1]])
+    with pytest.raises(ec.ValidationError):  # rank 1 exports a host shard, rank 0 holds HBM
+        hb[0].p2p_import([blobs[0], ho.p2p_export()])
+    hb[0].p2p_disable()
+    ids = torch.zeros(8, dtype=torch.int32, device="cuda")
+    with pytest.raises(ec.ValidationError):  # world 2 without a transport
+        hb[0].forward(ids, [0, 8], 8, 1)
+    for m in hb + [ho]:
+        m.close()
