@@ -569,7 +569,7 @@ def run_ours(args, wl):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp32 rows, uint32 ids",
+        "dtype": "f32", "index_dtype": "u32",
         "data": "synthetic: Zipf(1.05) ids from the reference sampler stream (GPU K0, bit-exact), synthetic rows",
         "config": {"workload": wl["name"], "distribution": list(wl.get("dist", ("zipf", wl.get("alpha")))),
                    "tables": T, "dim": D, "batch_per_gpu": B, "pooling": P,
@@ -711,7 +711,7 @@ def run_reference(args, wl):
     res = {"impl": "reference", "metric": "embedding lookups/sec (fwd+bwd step)", "value": round(value, 1),
            "unit": "lookups/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "uint32 ids", "data": "synthetic: Zipf(1.05) ids from the reference's sample_batch",
+           "dtype": "u32", "data": "synthetic: Zipf(1.05) ids from the reference's sample_batch",
            "config": {"workload": wl["name"], "tables": T, "batch_per_gpu": B, "pooling": P,
                       "cache_rows": int(sum(c.size for c in caches))},
            "cpu_baseline": {"value": round(value, 1), "unit": "lookups/s", "cores": threads, "kind": "reference",
