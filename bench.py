@@ -164,6 +164,7 @@ def pick_h2d_path(ec, torch, dev, host, stream, pull_ctas=16):
 
 
 H2D_PROBE = {}
+HOST = {"blocked": 0.0}
 
 
 def exchange_kind(wl):
@@ -456,7 +457,9 @@ def run_ours(args, wl):
             # pinned ring slot; decoded two steps later, like an async loss log
             tab.stats_enqueue(k % 4)
             if k >= 2:
+                t_blk = time.perf_counter()
                 res = tab.stats_collect((k - 2) % 4, per_table=True)
+                HOST["blocked"] += time.perf_counter() - t_blk
         tab.prefetch_wait()  # joins the last step's deferred host-tier write-back into `stream`
         for k in range(max(0, nsteps - 2), nsteps):
             res = tab.stats_collect(k % 4, per_table=True)
@@ -467,9 +470,12 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     torch.cuda._sleep(HEAD_START_CYCLES)
     gc.disable()  # no collector pauses inside the timed host loop
+    HOST["blocked"] = 0.0
+    t_host = time.perf_counter()
     e2e_start.record(stream)
     counters = e2e_steps(args.steps, e2e_marks)
     e2e_end.record(stream)
+    t_host = time.perf_counter() - t_host
     torch.cuda.synchronize()
     gc.enable()
     barrier()
@@ -589,7 +595,10 @@ def run_ours(args, wl):
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
                 "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4),
                 "h2d_path": ("ec_copy_async_pull, %d CTAs" % pull) if pull else "ec_copy_async (copy engine)",
-                "h2d_probe": H2D_PROBE},
+                "h2d_probe": H2D_PROBE,
+                # host time per step outside the blocking result reads: when it
+                # approaches ms_per_step the loop is host-bound, not GPU-bound
+                "host_busy_ms_per_step": round((t_host - HOST["blocked"]) * 1e3 / args.steps, 5)},
         "fwd_only": {"value": round(lookups_per_step * world / (fwd_ms * 1e-3), 1), "unit": "lookups/s",
                      "ms_per_step": round(fwd_ms, 5),
                      "step": "forward only (dedup, hit/miss, host-miss gather, pool), unpipelined"},
