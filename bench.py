@@ -431,6 +431,7 @@ def run_ours(args, wl):
         copied[k % NS].record(copy_stream)
 
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ready_stream = torch.cuda.Stream()  # a prefetch's input: ordered after its batch's copy only
 
     def e2e_steps(nsteps, marks=None):
         # input pipelining: step k+LA's H2D runs during step k, so a prefetch
@@ -440,7 +441,8 @@ def run_ours(args, wl):
         for k in range(min(nsteps, LA)):
             h2d(k)
         for k in range(min(nsteps, depth)):
-            tab.prefetch(dev_ids[k % NS], offs, B, P, stream=copy_stream)
+            ready_stream.wait_event(copied[k % NS])
+            tab.prefetch(dev_ids[k % NS], offs, B, P, stream=ready_stream)
         res = None
         for k in range(nsteps):
             if marks is not None:
@@ -449,9 +451,12 @@ def run_ours(args, wl):
             o = tab.forward(dev_ids[k % NS], offs, B, P, out=out)
             consumed[k % NS].record(stream)
             if depth and k + depth < nsteps:
-                tab.prefetch(dev_ids[(k + depth) % NS], offs, B, P, stream=copy_stream)  # after its H2D copy
+                # after exactly its own H2D copy (not the copy stream's tail,
+                # which already holds the next batch's copy)
+                ready_stream.wait_event(copied[(k + depth) % NS])
+                tab.prefetch(dev_ids[(k + depth) % NS], offs, B, P, stream=ready_stream)
             if k + LA < nsteps:
-                h2d(k + LA)  # (after the prefetch above, which orders itself after the copy stream)
+                h2d(k + LA)
             tab.backward(o, LR)
             # D2H of the step's result (per-table unique/miss counts) into a
             # pinned ring slot; decoded two steps later, like an async loss log

@@ -54,6 +54,16 @@ def h2d(k):
 
 
 DO_H2D = os.environ.get("E2E_H2D", "1") == "1"
+READY = os.environ.get("E2E_READY", "1") == "1"
+ready = torch.cuda.Stream()
+
+
+def pf(k):
+    if READY:
+        ready.wait_event(copied[k % NS])
+        tab.prefetch(dev_ids[k % NS], offs, B, P, stream=ready)
+    else:
+        tab.prefetch(dev_ids[k % NS], offs, B, P, stream=cs)
 DO_STATS = os.environ.get("E2E_STATS", "1") == "1"
 
 
@@ -62,7 +72,7 @@ def run(n, rec):
     for k in range(min(n, LA)):
         h2d(k)
     for k in range(min(n, DEPTH)):
-        tab.prefetch(dev_ids[k % NS], offs, B, P, stream=cs)
+        pf(k)
     for k in range(n):
         t = time.perf_counter()
         st.wait_event(copied[k % NS])
@@ -71,7 +81,7 @@ def run(n, rec):
         t = tick("forward", t) if rec else t
         consumed[k % NS].record(st)
         if DEPTH and k + DEPTH < n:
-            tab.prefetch(dev_ids[(k + DEPTH) % NS], offs, B, P, stream=cs)
+            pf(k + DEPTH)
         t = tick("prefetch", t) if rec else t
         if k + LA < n and DO_H2D:
             h2d(k + LA)
@@ -88,12 +98,35 @@ def run(n, rec):
     torch.cuda.synchronize()
 
 
+BG = os.environ.get("E2E_BG", "")  # background H2D copies beside the steps: "ce" or "pull"
+bgs = torch.cuda.Stream()
+bg_dev = torch.empty_like(ids[0])
+
+
+def background(n):
+    for k in range(n):
+        if BG == "ce":
+            lib.ec_copy_async(bg_dev.data_ptr(), hptr[k % NB], nbytes, bgs.cuda_stream)
+        elif BG == "pull":
+            lib.ec_copy_async_pull(bg_dev.data_ptr(), hptr[k % NB], nbytes, 16, bgs.cuda_stream)
+
+
 tab.backward(tab.forward(ids[0], offs, B, P, out=out), bench.LR)  # geometry for the first prefetch
 run(24, False)
+if BG:
+    torch.cuda.synchronize()
+    bg0 = torch.cuda.Event(enable_timing=True)
+    bg1 = torch.cuda.Event(enable_timing=True)
+    bg0.record(bgs)
+    background(steps)
+    bg1.record(bgs)
 t0 = time.perf_counter()
 run(steps, True)
 t1 = time.perf_counter()
-print(f"{sys.argv[1:]} h2d={DO_H2D} stats={DO_STATS} depth={DEPTH} pull={PULL} cs_prio={cs.priority}: e2e wall {1e6 * (t1 - t0) / steps:.1f} us/step")
+if BG:
+    torch.cuda.synchronize()
+    print(f"background {BG}: {steps} copies in {bg0.elapsed_time(bg1) * 1e3 / steps:.1f} us each")
+print(f"{sys.argv[1:]} bg={BG} h2d={DO_H2D} stats={DO_STATS} depth={DEPTH} pull={PULL} cs_prio={cs.priority} ready={READY}: e2e wall {1e6 * (t1 - t0) / steps:.1f} us/step")
 for k, v in acc.items():
     print(f"  {k:14s} mean {np.mean(v):7.1f}  median {np.median(v):7.1f}  p90 {np.percentile(v, 90):7.1f}")
 tab.close()
