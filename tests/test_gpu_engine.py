@@ -226,6 +226,33 @@ def test_config2_kaggle_shape_host_tier(ec, torch, ref, mode):
     tab.close()
 
 
+TB_ROWS = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546, 403346, 10, 2208, 11938,
+           155, 4, 976, 14, 39979771, 25641295, 39664984, 585935, 12972, 108, 36]
+
+
+@pytest.mark.parametrize("mode", ["auto", "cluster"])
+def test_config3_terabyte_shape_one_rank(ec, torch, ref, mode):
+    """Config 3's per-rank shape (BASELINE.json configs[2] at G=1): 26
+    Criteo-Terabyte-cardinality tables (188M rows, 48 GB at D=64) in HBM,
+    b=65536, P=1, 1 GB hot cache by global top-k.  Counts bit-exact vs the
+    reference, sets / rows / pooled vs the oracle, on the tile path (auto at
+    this size) and the cluster kernel at its widest (16 items per thread)."""
+    D, B = 64, 65536
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in TB_ROWS]
+    ks = ec.place_topk_global(dists, (1 << 30) // (D * 4))
+    caches = [d.top_ids(k) for d, k in zip(dists, ks)]
+    tab = ec.EmbeddingTables(TB_ROWS, D, storage="hbm", max_lookups_per_table=B, max_batch_size=B)
+    tab.dedup_mode(mode)
+    tab.init_synthetic(5, 0.02)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B] * 26, 7331)
+    out = tab.forward(ids, offs, B, 1)
+    st = check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, TB_ROWS, D, 5, 0.02, P=1, B=B,
+                     out=out, ref=ref)
+    assert st["miss_rows"] > 0 and st["hit_rows"] > 0
+    tab.close()
+
+
 def test_async_stats_ring_matches_sync_stats(ec, torch):
     """ec_lookup_stats_enqueue/collect (pinned ring, no sync at enqueue)
     decode each batch's counters exactly like the synchronous ec_lookup_stats,
