@@ -226,6 +226,49 @@ def test_config2_kaggle_shape_host_tier(ec, torch, ref, mode):
     tab.close()
 
 
+@pytest.mark.parametrize("storage", ["host", "hbm"])
+def test_config2_kaggle_shape_training_step(ec, torch, storage):
+    """One bench-style training step at the Kaggle shape (configs[1]) on the
+    fused single-rank path: forward, backward with grad = pooled output,
+    lr 0.01.  Every touched row (cache, HBM or pinned-host) equals the fp64
+    oracle's w - lr * sum(grads).  The update is fp32 reductions straight
+    into the row (one rounding of at most half an ulp of the running value per
+    add, in a varying order), so the bound is count * 2^-24 * |row|."""
+    D, B, lr = 16, 16384, 0.01
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in KAGGLE]
+    ks = ec.place_topk_global(dists, (256 << 20) // (D * 4))
+    caches = [d.top_ids(k) for d, k in zip(dists, ks)]
+    tab = ec.EmbeddingTables(KAGGLE, D, storage=storage, max_lookups_per_table=B, max_batch_size=B)
+    tab.init_synthetic(4, 0.05)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B] * 26, 909)
+    out = tab.forward(ids, offs, B, 1)
+    grad = out.clone()
+    tab.backward(grad, lr)
+    torch.cuda.synchronize()
+    ids_h = ids.cpu().numpy().view(np.uint32)
+    g = grad.cpu().numpy()
+    bag = np.arange(B + 1, dtype=np.int64)
+    for t in range(26):
+        seg = ids_h[offs[t]:offs[t + 1]]
+        u, inv = O.dedup(seg)
+        w0 = O.synthetic_rows(4, 0.05, t, u, D)
+        ug, want = O.backward_sgd(np.ascontiguousarray(g[:, t * D:(t + 1) * D]), inv[:seg.size], bag, w0, lr)
+        got = tab.read_rows(t, u)
+        cnt = np.bincount(inv[:seg.size], minlength=u.size)[:, None]
+        want = w0 - lr * ug
+        mag = np.maximum(np.abs(want), np.abs(w0)).max(axis=1, keepdims=True)
+        tol = cnt * 2.0 ** -24 * mag + 1e-7
+        err = np.abs(got - want)
+        bad = err > tol
+        if bad.any():
+            k = np.argwhere(bad)[0]
+            raise AssertionError(f"table {t}: {bad.sum()} bad of {bad.size}; first row {k[0]} id {u[k[0]]} "
+                                 f"count {cnt[k[0], 0]} got {got[k[0], k[1]]} want {want[k[0], k[1]]} "
+                                 f"w0 {w0[k[0], k[1]]} tol {tol[k[0], 0]}")
+    tab.close()
+
+
 TB_ROWS = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546, 403346, 10, 2208, 11938,
            155, 4, 976, 14, 39979771, 25641295, 39664984, 585935, 12972, 108, 36]
 
