@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import gc
+import glob
 import json
 import os
 import statistics
@@ -561,8 +562,10 @@ def run_ours(args, wl):
     dom_gbs = hbm_phases[dom]["gbs"]
     # dram bytes per launch of that kernel from the committed ncu --set full capture
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"{args.workload}_traffic.json")
-    if os.path.exists(tfile):
+    # (the newest round's capture: profiles/rNN/<workload>_traffic.json)
+    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9]*", f"{args.workload}_traffic.json")))
+    tfile = tfiles[-1] if tfiles else None
+    if tfile:
         traffic = json.load(open(tfile)).get(dom)
     step_alg = sum(mean_bytes.values())
     link_ms = sum(phases[k]["ms_per_call"] for k in ("k_gather_host", "k_apply_host") if k in phases)
@@ -611,11 +614,11 @@ def run_ours(args, wl):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": round(dom_gbs / peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": hbm_phases[dom]["alg_bytes"],
-                     "traffic_source": (f"profiles/{args.workload}_traffic.json (ncu --set full, dram read+write "
+                     "traffic_source": (f"{os.path.relpath(tfile, ROOT)} (ncu --set full, dram read+write "
                                         "bytes per launch)") if traffic else None,
                      "peak_source": peak_src},
         # the pinned-host tier's bound: the host link serves ~215 M row requests/s
-        # (reads and writes share it; tools/hostlink_bench.cu, profiles/hostlink_probe.txt)
+        # (reads and writes share it; tools/hostlink_bench.cu, profiles/r01/hostlink_probe.txt)
         "host_link": ({"bound": "host-link request rate", "rows_per_step": int(2 * s0["miss_rows"]),
                        "achieved_rows_per_s": round(2 * s0["miss_rows"] / (link_ms * 1e-3), 1),
                        "peak_rows_per_s": HOST_LINK_ROWS_PER_S,

@@ -166,7 +166,7 @@ int Engine::host_grid() const {
   // TMA path: the copy engine holds the row reads, so CTAs are cheap -- 2 per
   // SM keep 16 KiB each in flight.
   // LSU path (default): 16 CTAs x 256 threads keep ~4k row reads in flight --
-  // the host link is request-rate bound (~215 M rows/s, profiles/hostlink_probe.txt)
+  // the host link is request-rate bound (~215 M rows/s, profiles/r01/hostlink_probe.txt)
   // and deeper queues only stall the concurrent pool/dedup/scatter.  Measured
   // on the pipelined Kaggle step: 12/16/24/32 CTAs 0.099-0.103/0.100-0.104/
   // 0.103-0.110/0.107-0.113 ms; 8 CTAs starve the link (0.109), TMA at 296
