@@ -1216,6 +1216,7 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
     // joined by whatever next reuses this set or the host tier
     if (storage == EC_STORAGE_HOST) EC_DISPATCH_VEC(enqueue_host_writeback, lr);
   } else if (p2p_on()) {
+    if (!p2p_step_open()) invalid("the peer-memory exchange takes one backward per forward");
     EC_DISPATCH_VEC(bwd_scatter, grad, st);
     p2p_bwd_publish(lr, st);  // hits -> own list, misses -> owners' rows (NVLink atomics)
     p2p_signal(0, st);

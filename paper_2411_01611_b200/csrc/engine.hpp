@@ -334,6 +334,7 @@ struct Engine {
   PeerView p2p_self() const;
   void p2p_fwd_begin(cudaStream_t st);
   void p2p_close_open(cudaStream_t st);
+  bool p2p_step_open() const;
   void p2p_bwd_publish(float lr, cudaStream_t st);
   template <int VEC> void p2p_publish(float lr, cudaStream_t st);
   void p2p_signal(int b, cudaStream_t st);

@@ -498,6 +498,7 @@ void Engine::ex_apply_bwd(float lr, cudaStream_t st) {
 // applies every rank's list in rank order, signals barrier 1.
 // No host synchronisation, no NCCL call.
 bool Engine::p2p_on() const { return ex != nullptr && ex->p2p; }
+bool Engine::p2p_step_open() const { return p2p_on() && ex->step_open; }
 const PeerView* Engine::p2p_peers() const { return p2p_on() ? ex->peers.p : nullptr; }
 const int64_t* Engine::p2p_shard_off() const { return p2p_on() ? ex->shard_off.p : nullptr; }
 
@@ -837,11 +838,15 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
     const int W = static_cast<int>(g->members.size());
     const size_t D = g->members[0]->e.D;
     if (g->members[0]->e.p2p_on()) {
+      for (int r = 0; r < W; ++r) {  // validate before enqueuing anything
+        Engine& e = g->members[r]->e;
+        if (!e.have_fwd) invalid("ec_group_lookup_bwd needs a preceding forward");
+        if (!e.p2p_step_open()) invalid("the peer-memory exchange takes one backward per forward");
+        if (!grads[r]) invalid("null gradient");
+      }
       // every rank's signal of barrier 0 precedes every rank's wait on one stream
       for (int r = 0; r < W; ++r) {
         Engine& e = g->members[r]->e;
-        if (!e.have_fwd) invalid("ec_group_lookup_bwd needs a preceding forward");
-        if (!grads[r]) invalid("null gradient");
         e.scatter_grads(grads[r], st);
         e.p2p_bwd_publish(lr, st);
         e.p2p_signal(0, st);
