@@ -895,7 +895,6 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
       p2p_fwd_begin(st);
       gather_local(st);
       pool(st);
-      p2p_signal(2, st);
       have_fwd = true;
       return;
     }
@@ -940,7 +939,6 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
     enqueue_dedup_partition(b.indices_dev, st);
     gather_local(st);  // K4 fused: remote misses are loads from their owners' shards
     pool(st);          // (joins the host-row gather of the side stream)
-    p2p_signal(2, st);
   } else {
     enqueue_dedup_partition(b.indices_dev, st);
     gather_local(st);

@@ -46,7 +46,7 @@ inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 5; }
 // What a rank sees of a peer for the peer-memory exchange (K4 over NVLink
 // loads/stores/atomics): the peer's HBM shard and its published hot-row
 // gradient list, and the flag words the peer waits on.
-constexpr int kP2PBarriers = 3;  // device barriers per step of the peer-memory exchange
+constexpr int kP2PBarriers = 2;  // device barriers per step of the peer-memory exchange
 
 struct PeerView {
   float* store;             // the peer's whole shard (row = shard_off[peer][t] + id / world)
@@ -336,7 +336,7 @@ struct Engine {
   void p2p_close_open(cudaStream_t st);
   bool p2p_step_open() const;
   void p2p_bwd_publish(float lr, cudaStream_t st);
-  template <int VEC> void p2p_publish(float lr, cudaStream_t st);
+  template <int VEC> void p2p_publish(float lr, cudaStream_t st, int part);
   void p2p_signal(int b, cudaStream_t st);
   void p2p_wait(int b, unsigned epoch, cudaStream_t st);
   void p2p_bwd_finish(float lr, cudaStream_t st);

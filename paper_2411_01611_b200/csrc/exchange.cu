@@ -207,7 +207,7 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
                             const int32_t* __restrict__ usrc, const float* __restrict__ ugrad, float lr,
                             const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, int rank,
                             int world, uint32_t* __restrict__ pub_slot, float* __restrict__ pub_grad,
-                            int* __restrict__ pub_cnt, int64_t inbox_cap) {
+                            int* __restrict__ pub_cnt, int64_t inbox_cap, int part) {
   constexpr int D = VEC * 4;
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   const int sub = lane_id() / VEC, c = lane_id() % VEC;
@@ -218,8 +218,8 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
     const bool live = g < U;
     const int32_t s = live ? usrc[g] : -1;
     const float4 gv = live ? ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    // hits: one list slot per row (lane c == 0 of the row's group claims it)
-    const bool hit = live && s >= 0;
+    // part & 1 -- hits: one list slot per row (lane c == 0 of the row's group claims it)
+    const bool hit = (part & 1) && live && s >= 0;
     const unsigned hb = __ballot_sync(kFull, hit && c == 0);
     int b0 = 0;
     if (hb && lane_id() == __ffs(hb) - 1) b0 = atomicAdd(pub_cnt, __popc(hb));
@@ -229,8 +229,8 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
       if (c == 0) pub_slot[pos] = static_cast<uint32_t>(s);
       st4(pub_grad + static_cast<int64_t>(pos) * D + c * 4, gv);
     }
-    // misses: the owner's row (index in its shard)
-    const bool miss = live && s < 0;
+    // part & 2 -- misses: the owner's row (index in its shard)
+    const bool miss = (part & 2) && live && s < 0;
     const uint32_t id = miss ? uniq[g] : 0;
     const int o = static_cast<int>(id % world);
     const int64_t row = miss ? shard_off[static_cast<int64_t>(o) * (T + 1) + utab[g]] + id / world : 0;
@@ -296,8 +296,8 @@ __global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float
 
 // Device barrier over peer memory, split in two so a loopback group can
 // enqueue every rank's signal before any rank's wait on one stream.
-// Barrier b (0: hot lists published, 1: step applied, 2: forward reads done)
-// of generation `epoch`.
+// Barrier b (0: hot lists published -- every rank is past its forward reads;
+// 1: step applied) of generation `epoch`.
 __global__ void k_p2p_signal(const PeerView* __restrict__ peers, int world, int rank, int b, unsigned epoch) {
   if (threadIdx.x >= world) return;
   __threadfence_system();  // this rank's writes of the step before the word
@@ -491,12 +491,13 @@ void Engine::ex_apply_bwd(float lr, cudaStream_t st) {
 
 // ------------------------------------------------------------ P2P driver
 // Per step (generation e = ++epoch): forward waits barrier 1 of e-1 (every
-// rank applied the previous step), pulls remote rows in k_gather and signals
-// barrier 2 (its reads of peers' shards are done); backward waits barrier 2
-// (nobody still reads the rows it is about to update), publishes its hot list
-// and updates owners' rows by atomics, signals barrier 0, waits for it,
-// applies every rank's list in rank order, signals barrier 1.
-// No host synchronisation, no NCCL call.
+// rank applied the previous step) and pulls remote rows in k_gather; backward
+// publishes its hot list (and, for pinned-host shards, its miss gradients into
+// the owners' inboxes), signals barrier 0 and waits for it -- every rank is
+// then past its forward, so no one still reads the rows about to change --
+// updates owners' rows (HBM: atomics over NVLink; host: each owner applies
+// its inbox), applies every rank's hot list in rank order, signals barrier 1.
+// Two device barriers, no host synchronisation, no NCCL call.
 bool Engine::p2p_on() const { return ex != nullptr && ex->p2p; }
 bool Engine::p2p_step_open() const { return p2p_on() && ex->step_open; }
 const PeerView* Engine::p2p_peers() const { return p2p_on() ? ex->peers.p : nullptr; }
@@ -571,25 +572,26 @@ void Engine::p2p_fwd_begin(cudaStream_t st) {
 }
 
 template <int VEC>
-void Engine::p2p_publish(float lr, cudaStream_t st) {
+void Engine::p2p_publish(float lr, cudaStream_t st, int part) {
   Exchange& x = *ex;
-  p2p_wait(2, x.epoch, st);  // every rank's forward reads of step e are done
-  EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
+  if (part & 1) EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
   k_p2p_apply<VEC><<<row_grid(), 256, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, usrc.p,
                                                    ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.pub_slot.p,
                                                    x.pub_grad.p, x.pub_cnt.p,
-                                                   storage == EC_STORAGE_HOST ? x.inbox_cap : 0);
+                                                   storage == EC_STORAGE_HOST ? x.inbox_cap : 0, part);
   launched();
 }
 void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
   if (!ex->step_open) invalid("the peer-memory exchange takes one backward per forward");
   PhaseScope ph(prof, kPhaseExchange, st);
-  EC_DISPATCH_VEC(p2p_publish, lr, st);
+  // hits; pinned-host shards also their misses (inbox appends change no row)
+  EC_DISPATCH_VEC(p2p_publish, lr, st, storage == EC_STORAGE_HOST ? 3 : 1);
 }
 
 template <int VEC>
 void Engine::p2p_hot(float lr, cudaStream_t st) {
   Exchange& x = *ex;
+  if (storage != EC_STORAGE_HOST) p2p_publish<VEC>(lr, st, 2);  // misses: atomics into the owners' rows
   if (x.inbox_cap && storage == EC_STORAGE_HOST) {  // owner: every source's miss gradients, rank order
     for (int p = 0; p < x.W; ++p) {
       k_p2p_inbox_apply<VEC><<<host_grid(), 256, 0, st>>>(x.inbox_idx.p + p * x.inbox_cap,
@@ -597,7 +599,7 @@ void Engine::p2p_hot(float lr, cudaStream_t st) {
                                                           store_base, lr);
       launched();
     }
-    EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append again after barrier 2
+    EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append after barrier 1
   }
   for (int p = 0; p < ex->W; ++p) {
     k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr);
@@ -780,7 +782,6 @@ int ec_group_lookup_fwd(ec_group g, const ec_batch* batches, float* const* outs,
         e.enqueue_dedup_partition(batches[r].indices_dev, st);
         e.gather_local(st);
         e.pool(st);
-        e.p2p_signal(2, st);  // after the pool: it joins the side stream's host-row reads
         e.have_fwd = true;
       }
       return;
