@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libembcomm_gpu.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("EC_LIB_NAME", "libembcomm_gpu.so"))  # (A/B builds)
 
 EC_OK, EC_EINVAL, EC_EINVARIANT, EC_ECUDA, EC_ENCCL, EC_ENOMEM = 0, 2, 3, 4, 5, 6
 

@@ -912,7 +912,10 @@ namespace cg = cooperative_groups;
 #define EC_CLUSTER_CTAS 8
 #endif
 constexpr int kClusterCtas = EC_CLUSTER_CTAS;
-constexpr int kClusterThreads = 512;
+#ifndef EC_CLUSTER_THREADS
+#define EC_CLUSTER_THREADS 512
+#endif
+constexpr int kClusterThreads = EC_CLUSTER_THREADS;
 constexpr int kClusterMaxItems = 16;     // per thread -> n_t <= 8 * 512 * 16 = 65536
 constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared memory
 // per-table look-back word: count [0,32), CTA arrivals [32,40), inclusive flag
@@ -921,7 +924,8 @@ __host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLo
 
 
 template <int ITEMS>
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, ITEMS <= 4 ? 2 : 1)
+__global__ void __cluster_dims__(kClusterCtas, 1, 1)
+__launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1) : (ITEMS <= 8 ? 3 : 2))
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
                     unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
