@@ -142,7 +142,7 @@ def make_dist(ec, wl, rows, t):
     return ec.EmbeddingDistribution.from_probabilities(p)
 
 
-def pick_h2d_path(ec, torch, dev, host, stream, pull_ctas=16):
+def pick_h2d_path(ec, torch, dev, host, stream, pull_ctas=8):
     """0 (copy engine) or pull_ctas, by timing 10 copies of one batch each."""
     lib = ec._native.lib()
     n = dev.numel() * dev.element_size()
@@ -400,7 +400,7 @@ def run_ours(args, wl):
     # ---- e2e through the public API with host buffers (pinned), K steps
     host_ids = ids.cpu().pin_memory()
     # input pipeline: step k+LA's ids are copied during step k (two steps of
-    # slack), pulled by 16 CTAs' loads (ec_copy_async_pull) unless the copy
+    # slack), pulled by 8 CTAs' loads (ec_copy_async_pull) unless the copy
     # engine is far faster on this box: the copy engine's H2D rate for a 1.7 MB
     # copy varies 13-55 GB/s across this pool's boxes and over time, the pull
     # holds ~45 GB/s (tools/copyprobe.py)
