@@ -297,6 +297,7 @@ Engine::~Engine() {
   if (ev_patch) cudaEventDestroy(ev_patch);
   if (ev_pfcall) cudaEventDestroy(ev_pfcall);
   if (ev_gate) cudaEventDestroy(ev_gate);
+  if (ev_b1) cudaEventDestroy(ev_b1);
   destroy_comm();  // (unmaps the peers' shards first)
   if (store_host) free_host_tier(store_host, store_host_bytes, store_host_mmapped);
   if (store_host_fd >= 0) close(store_host_fd);
@@ -419,6 +420,7 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaEventCreateWithFlags(&ev_patch, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_pfcall, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_gate, cudaEventDisableTiming));
+  EC_CUDA(cudaEventCreateWithFlags(&ev_b1, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
@@ -891,10 +893,18 @@ void Engine::forward(const ec_batch& b, float* out, cudaStream_t st) {
       nx.pending = false;
       EC_CUDA(cudaEventRecord(bb[cur].ev_free, st));
       select(h);
-      EC_CUDA(cudaStreamWaitEvent(st, nx.ev_ded, 0));
+      EC_CUDA(cudaStreamWaitEvent(st, nx.rows_early ? nx.ev_pf : nx.ev_ded, 0));
       p2p_fwd_begin(st);
-      gather_local(st);
-      pool(st);
+      if (nx.rows_early) p2p_patch_prefetched(st);  // rows the last step updated after the early read
+      consuming_prefetch = nx.rows_early;
+      try {
+        gather_local(st);
+        pool(st);
+      } catch (...) {
+        consuming_prefetch = false;
+        throw;
+      }
+      consuming_prefetch = false;
       have_fwd = true;
       return;
     }
@@ -976,8 +986,11 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // this prefetch (e.g. the copy that produced these indices) comes first
   EC_CUDA(cudaEventRecord(ev_pfcall, st));
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_pfcall, 0));
-  // (peer exchange: rows are read after the step's barrier, in the forward)
-  const bool gather_now = storage == EC_STORAGE_HOST && next_in_line && world == 1;
+  // peer exchange: rows are read once the forward in flight passed its step
+  // barrier (every update of the step before is in), and the ones this step
+  // updates are patched after the next barrier (p2p_patch_prefetched)
+  const bool gather_now = storage == EC_STORAGE_HOST && next_in_line;
+  if (gather_now && world > 1) EC_CUDA(cudaStreamWaitEvent(pstream, ev_b1, 0));
   const int saved = cur;
   select(s);
   try {
@@ -997,6 +1010,7 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   BatchBufs& nb = bb[s];
   nb.pending = true;
   nb.gathered = storage != EC_STORAGE_HOST || gather_now || world > 1;
+  nb.rows_early = world > 1 && gather_now;
   nb.seq = ++pf_seq;
   nb.indices = b.indices_dev;
   nb.geom_version = geom_version;

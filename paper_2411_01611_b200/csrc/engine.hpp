@@ -59,6 +59,7 @@ struct PeerView {
   uint32_t* inbox_idx;
   float* inbox_grad;
   int* inbox_cnt;
+  uint32_t* ver;  // pinned-host shards: step generation of each row's last update (prefetch patch)
 };
 
 struct Exchange;  // exchange.cu
@@ -87,6 +88,7 @@ struct BatchBufs {
   uint64_t geom_version = 0;
   bool pending = false;               // prefetched, not yet consumed by forward
   bool gathered = false;              // its pinned-host miss gather was launched (ev_pf)
+  bool rows_early = false;            // (peer exchange) host rows read before the step barrier: patch them
   uint64_t seq = 0;                   // prefetch order (the smallest pending seq is consumed next)
   cudaEvent_t ev_free = nullptr;      // main-stream work of its last batch done (set reusable)
   cudaEvent_t ev_ded = nullptr;       // its prefetch's dedup done
@@ -250,6 +252,7 @@ struct Engine {
   cudaStream_t side = nullptr, side2 = nullptr, pstream = nullptr;
   cudaEvent_t ev_pfcall = nullptr;   // caller's stream at the prefetch call
   cudaEvent_t ev_gate = nullptr;     // caller's stream at the forward that starts a pending gather
+  cudaEvent_t ev_b1 = nullptr;       // (peer exchange) the last forward passed its step barrier
 
   cudaEvent_t ev_part = nullptr, ev_side = nullptr, ev_side2 = nullptr,
               ev_grad = nullptr, ev_patch = nullptr;
@@ -335,6 +338,8 @@ struct Engine {
   void p2p_fwd_begin(cudaStream_t st);
   void p2p_close_open(cudaStream_t st);
   bool p2p_step_open() const;
+  void p2p_patch_prefetched(cudaStream_t st);
+  template <int VEC> void p2p_patch(cudaStream_t st);
   void p2p_bwd_publish(float lr, cudaStream_t st);
   template <int VEC> void p2p_publish(float lr, cudaStream_t st, int part);
   void p2p_signal(int b, cudaStream_t st);

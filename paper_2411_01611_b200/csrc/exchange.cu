@@ -77,6 +77,7 @@ struct Exchange {
   DevBuf<uint32_t> inbox_idx;       // [W * cap]
   DevBuf<float> inbox_grad;         // [W * cap * D]
   DevBuf<int> inbox_cnt;            // [W]
+  DevBuf<uint32_t> ver;             // [shard rows]: step generation of each row's last inbox update
   int64_t inbox_cap = 0;
   std::vector<std::pair<void*, size_t>> host_maps;  // peers' host shards mapped here
 
@@ -261,7 +262,8 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
 // source's segment, so each launch is a plain read-modify-write).
 template <int VEC>
 __global__ void k_p2p_inbox_apply(const uint32_t* __restrict__ idx, const float* __restrict__ grad,
-                                  const int* __restrict__ cnt, float* __restrict__ store, float lr) {
+                                  const int* __restrict__ cnt, float* __restrict__ store, float lr,
+                                  uint32_t* __restrict__ ver, unsigned epoch) {
   constexpr int D = VEC * 4;
   const int64_t total = static_cast<int64_t>(*cnt) * VEC;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -272,8 +274,34 @@ __global__ void k_p2p_inbox_apply(const uint32_t* __restrict__ idx, const float*
     float4 v = *reinterpret_cast<const float4*>(w);
     v = make_float4(v.x - lr * gv.x, v.y - lr * gv.y, v.z - lr * gv.z, v.w - lr * gv.w);
     st4(w, v);
+    if (c == 0) ver[idx[k]] = epoch;  // read by peers' prefetch patch after barrier 1
   }
 }
+
+// A prefetched batch's host rows were read while the step before ran; rows
+// that step updated (stamped with its generation by their owner) are read
+// again once every rank passed barrier 1.
+template <int VEC>
+__global__ void k_p2p_patch(const int* __restrict__ ctr, int T, const uint32_t* __restrict__ missq,
+                            const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                            float* __restrict__ urows, const PeerView* __restrict__ peers,
+                            const int64_t* __restrict__ shard_off, int world, unsigned epoch) {
+  constexpr int D = VEC * 4;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int64_t total = static_cast<int64_t>(nm) * VEC;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = static_cast<int>(i / VEC);
+    const int c = static_cast<int>(i - static_cast<int64_t>(q) * VEC);
+    const uint32_t g = missq[q];
+    const uint32_t id = uniq[g];
+    const int o = static_cast<int>(id % world);
+    const int64_t row = shard_off[static_cast<int64_t>(o) * (T + 1) + utab[g]] + id / world;
+    const PeerView pv = peers[o];
+    if (*reinterpret_cast<const volatile uint32_t*>(pv.ver + row) != epoch) continue;
+    st4(urows + static_cast<int64_t>(g) * D + c * 4, *reinterpret_cast<const float4*>(pv.store + row * D + c * 4));
+  }
+}
+
 
 // One source rank's published hot gradients into this rank's cache replica
 // (launched for p = 0..world-1: every replica sees the same order).
@@ -514,6 +542,8 @@ void Engine::p2p_alloc() {
     x.inbox_grad.alloc(x.W * N * D);
     x.inbox_cnt.alloc(x.W);
     EC_CUDA(cudaMemset(x.inbox_cnt.p, 0, x.inbox_cnt.bytes()));
+    x.ver.alloc(std::max<uint64_t>(store_off[T], 1));
+    EC_CUDA(cudaMemset(x.ver.p, 0, x.ver.bytes()));  // generation 0 is never a step
   }
   if (x.pub_slot.n < N) x.pub_slot.alloc(N);
   if (x.pub_grad.n < N * D) x.pub_grad.alloc(N * D);
@@ -528,8 +558,8 @@ void Engine::p2p_alloc() {
 }
 
 PeerView Engine::p2p_self() const {
-  return PeerView{store_base, ex->pub_slot.p, ex->pub_grad.p, ex->pub_cnt.p, ex->flags.p,
-                  ex->inbox_idx.p, ex->inbox_grad.p, ex->inbox_cnt.p};
+  return PeerView{store_base,      ex->pub_slot.p,   ex->pub_grad.p,  ex->pub_cnt.p, ex->flags.p,
+                  ex->inbox_idx.p, ex->inbox_grad.p, ex->inbox_cnt.p, ex->ver.p};
 }
 
 void Engine::p2p_set_peers(const std::vector<PeerView>& v) {
@@ -567,6 +597,7 @@ void Engine::p2p_fwd_begin(cudaStream_t st) {
   ++x.epoch;
   x.step_open = true;
   p2p_wait(1, x.epoch - 1, st);
+  EC_CUDA(cudaEventRecord(ev_b1, st));  // a host-row prefetch may start reading from here
   last_wire_rows = 0;  // (counted on the device: Counters::wire)
   last_wire_bytes = 0;
 }
@@ -596,7 +627,7 @@ void Engine::p2p_hot(float lr, cudaStream_t st) {
     for (int p = 0; p < x.W; ++p) {
       k_p2p_inbox_apply<VEC><<<host_grid(), 256, 0, st>>>(x.inbox_idx.p + p * x.inbox_cap,
                                                           x.inbox_grad.p + p * x.inbox_cap * D, x.inbox_cnt.p + p,
-                                                          store_base, lr);
+                                                          store_base, lr, x.ver.p, x.epoch);
       launched();
     }
     EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append after barrier 1
@@ -606,6 +637,14 @@ void Engine::p2p_hot(float lr, cudaStream_t st) {
     launched();
   }
 }
+template <int VEC>
+void Engine::p2p_patch(cudaStream_t st) {
+  k_p2p_patch<VEC><<<host_grid(), 256, 0, st>>>(ctr.p, static_cast<int>(T), missq.p, uniq.p, utab.p, urows.p,
+                                                ex->peers.p, ex->shard_off.p, world, ex->epoch - 1);
+  launched();
+}
+void Engine::p2p_patch_prefetched(cudaStream_t st) { EC_DISPATCH_VEC(p2p_patch, st); }
+
 void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseExchange, st);
   p2p_wait(0, ex->epoch, st);
@@ -905,10 +944,11 @@ int ec_group_set_p2p(ec_group g, int enable) {
 // Multi-process: this rank's peer-visible allocations, to be all-gathered
 // and passed to every rank's ec_tables_p2p_import.  Blob: CUDA IPC handles of
 // {shard (HBM), hot list, its gradients, its length, barrier words, inbox
-// indices, inbox gradients, inbox counts} (unused ones zero), then the host
+// indices, inbox gradients, inbox counts, row generations} (unused ones
+// zero), then the host
 // shard's memfd as {pid, fd, bytes} (pinned-host tier; zeros for HBM).
 namespace {
-constexpr int kP2PHandles = 8;
+constexpr int kP2PHandles = 9;
 struct HostSeg {
   int64_t pid, fd;
   uint64_t bytes;
@@ -928,8 +968,8 @@ int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len
     if (cap < kP2PBlob) invalid("p2p export blob needs " + std::to_string(kP2PBlob) + " bytes");
     std::memset(blob, 0, kP2PBlob);
     const Exchange& x = *e.ex;
-    void* ptrs[kP2PHandles] = {e.store_dev.p, x.pub_slot.p,  x.pub_grad.p,   x.pub_cnt.p,
-                               x.flags.p,     x.inbox_idx.p, x.inbox_grad.p, x.inbox_cnt.p};
+    void* ptrs[kP2PHandles] = {e.store_dev.p, x.pub_slot.p,   x.pub_grad.p,  x.pub_cnt.p, x.flags.p,
+                               x.inbox_idx.p, x.inbox_grad.p, x.inbox_cnt.p, x.ver.p};
     for (int k = 0; k < kP2PHandles; ++k) {
       if (!ptrs[k]) continue;
       cudaIpcMemHandle_t h;
@@ -999,10 +1039,11 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
         x.host_maps.emplace_back(m, maplen);
         EC_CUDA(cudaHostGetDevicePointer(&ptrs[0], m, 0));
       }
-      views[p] = PeerView{static_cast<float*>(ptrs[0]),        static_cast<const uint32_t*>(ptrs[1]),
-                          static_cast<const float*>(ptrs[2]),  static_cast<const int*>(ptrs[3]),
-                          static_cast<unsigned*>(ptrs[4]),     static_cast<uint32_t*>(ptrs[5]),
-                          static_cast<float*>(ptrs[6]),        static_cast<int*>(ptrs[7])};
+      views[p] = PeerView{static_cast<float*>(ptrs[0]),       static_cast<const uint32_t*>(ptrs[1]),
+                          static_cast<const float*>(ptrs[2]), static_cast<const int*>(ptrs[3]),
+                          static_cast<unsigned*>(ptrs[4]),    static_cast<uint32_t*>(ptrs[5]),
+                          static_cast<float*>(ptrs[6]),       static_cast<int*>(ptrs[7]),
+                          static_cast<uint32_t*>(ptrs[8])};
     }
     e.p2p_set_peers(views);
   });

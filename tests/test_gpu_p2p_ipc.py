@@ -40,12 +40,15 @@ def _setup(ec, rank, world, storage):
     return m, dists, caches
 
 
-def _batch(ec, torch, dists, rank, step):
+def _batch(ec, torch, dists, rank, step, repeat=False):
+    """repeat: the same ids every step (every cold row a step reads was updated
+    by the step before: a prefetch read before the barrier is always stale)."""
     n = B * P
     ids = torch.empty(len(dists) * n, dtype=torch.int32, device="cuda")
     for t, d in enumerate(dists):
         ec.DiscreteSampler(d).sample_into(ids.data_ptr() + 4 * n * t,
-                                          ec.substream_seed(ec.substream_seed(100 + step, rank), t), 0, n)
+                                          ec.substream_seed(ec.substream_seed(100 + (0 if repeat else step), rank), t),
+                                          0, n)
     g = torch.Generator(device="cuda").manual_seed(1000 * step + rank)
     grad = torch.randn(B, len(dists) * D, device="cuda", generator=g)
     return ids, grad
@@ -62,7 +65,7 @@ def _probe(m, rank, world, caches):
     return out
 
 
-def _worker(rank, port, q, storage, prefetch):
+def _worker(rank, port, q, storage, prefetch, repeat):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -79,7 +82,7 @@ def _worker(rank, port, q, storage, prefetch):
         dist.barrier()
         offs = np.arange(len(ROWS) + 1, dtype=np.int64) * (B * P)
         outs = []
-        batches = [_batch(ec, torch, dists, rank, step) for step in range(STEPS)]
+        batches = [_batch(ec, torch, dists, rank, step, repeat) for step in range(STEPS)]
         for step in range(STEPS):
             ids, grad = batches[step]
             outs.append(m.forward(ids, offs, B, P).cpu().numpy())
@@ -98,8 +101,10 @@ def _worker(rank, port, q, storage, prefetch):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("storage,prefetch", [("hbm", False), ("host", False), ("hbm", True), ("host", True)])
-def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch):
+@pytest.mark.parametrize("storage,prefetch,repeat", [("hbm", False, False), ("host", False, False),
+                                                     ("hbm", True, False), ("host", True, False),
+                                                     ("host", True, True)])
+def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch, repeat):
     import torch
     import torch.multiprocessing as mp
     # expected: the loopback group (staged copies) in this process
@@ -110,7 +115,7 @@ def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch):
     offs = np.arange(len(ROWS) + 1, dtype=np.int64) * (B * P)
     want = [[] for _ in range(WORLD)]
     for step in range(STEPS):
-        batch = [_batch(ec, torch, dists[0], r, step) for r in range(WORLD)]
+        batch = [_batch(ec, torch, dists[0], r, step, repeat) for r in range(WORLD)]
         outs = group.forward([b[0] for b in batch], offs, B, P)
         for r in range(WORLD):
             want[r].append(outs[r].cpu().numpy())
@@ -124,7 +129,7 @@ def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q, storage, prefetch)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, storage, prefetch, repeat)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = {}
