@@ -597,8 +597,9 @@ def run_ours(args, wl):
                             "host-miss gather overlap this step and are inside its window, as is this step's "
                             "host write-back") if depth and world == 1 else
                            ("fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD) + peer exchange; "
-                            "pipelined (ec_lookup_prefetch depth 1): batch j+1's dedup/hit-miss overlaps this step "
-                            "and is inside its window") if depth else
+                            "pipelined (ec_lookup_prefetch depth 1): batch j+1's dedup/hit-miss (and, pinned-host "
+                            "tier, its host-row gather, patched after the step barrier) overlaps this step and is "
+                            "inside its window") if depth else
                            "fwd (dedup, hit/miss, gather, pool) + bwd (grad scatter + SGD), unpipelined",
                    "parallelism": f"row-sharded x{world}, owner = id % {world}, {MODES.get('exchange_used')} exchange"
                    if world > 1 else "single GPU"},
