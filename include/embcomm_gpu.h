@@ -366,7 +366,10 @@ int ec_tables_schedule(ec_tables t, const uint32_t* ids_dev, uint64_t num_sample
                        uint64_t* num_hot, void* stream);
 int ec_tables_gather_batch(ec_tables t, const uint32_t* ids_dev, const uint32_t* order_dev, uint64_t first,
                            uint32_t count, uint32_t* indices_dev, void* stream);
-/* Start the next batch while the current one finishes (single rank): its
+/* Start the next batch while the current one finishes (single rank, or a
+ * rank on the peer-memory exchange, where the next batch's pinned-host rows
+ * are read once the current forward passed its step barrier and the ones the
+ * current step updates are re-read after the next barrier): its
  * dedup, hit/miss partition and pinned-host miss gather run on internal
  * streams into a second buffer set, overlapping the current backward; the
  * next ec_lookup_fwd with the same indices_dev consumes them (up to 2 batches
