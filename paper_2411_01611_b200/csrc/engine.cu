@@ -1230,9 +1230,8 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   } else if (p2p_on()) {
     if (!p2p_step_open()) invalid("the peer-memory exchange takes one backward per forward");
     EC_DISPATCH_VEC(bwd_scatter, grad, st);
-    p2p_bwd_publish(lr, st);  // hits -> own list, misses -> owners' rows (NVLink atomics)
-    p2p_signal(0, st);
-    p2p_bwd_finish(lr, st);   // every rank's list, in rank order, into the cache replica
+    p2p_bwd_publish(lr, st);  // hits -> own list (host tier: misses -> owners' inboxes); signals barrier 0
+    p2p_bwd_finish(lr, st);   // owners' rows, then every rank's list in rank order into the cache replica
   } else {
     scatter_and_apply_local(grad, lr, st);
     exchange_bwd(lr, st);  // remote misses -> owners, replicated hot rows in rank order

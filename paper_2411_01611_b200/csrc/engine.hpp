@@ -341,7 +341,7 @@ struct Engine {
   void p2p_patch_prefetched(cudaStream_t st);
   template <int VEC> void p2p_patch(cudaStream_t st);
   void p2p_bwd_publish(float lr, cudaStream_t st);
-  template <int VEC> void p2p_publish(float lr, cudaStream_t st, int part);
+  template <int VEC> void p2p_publish(float lr, cudaStream_t st, int part, int wait_b, int sig_b);
   void p2p_signal(int b, cudaStream_t st);
   void p2p_wait(int b, unsigned epoch, cudaStream_t st);
   void p2p_bwd_finish(float lr, cudaStream_t st);

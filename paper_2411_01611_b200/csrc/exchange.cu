@@ -72,6 +72,7 @@ struct Exchange {
   DevBuf<float> pub_grad;
   DevBuf<int> pub_cnt;
   DevBuf<unsigned> flags;           // [2W] barrier words peers write into
+  DevBuf<unsigned> done;            // arrival counter of a kernel that signals a barrier
   std::vector<void*> ipc_opened;    // peer allocations mapped by cudaIpcOpenMemHandle
   // pinned-host shards: miss gradients sent to this rank as owner
   DevBuf<uint32_t> inbox_idx;       // [W * cap]
@@ -202,14 +203,76 @@ __global__ void k_rows_sgd(float* __restrict__ rows, const uint32_t* __restrict_
 // published hot list (applied by every rank in rank order); misses update
 // their owner's shard row in place with -lr*g (float atomics: the owner's row
 // may receive several ranks' updates in one step; it is not replicated).
+// Device barrier pieces folded into the exchange kernels: a kernel may wait
+// for barrier `wait_b` in its prologue (every block, threads < world spin on
+// this rank's flag words) and signal barrier `sig_b` from its last block to
+// finish (a grid-wide arrival counter), saving the separate barrier launches.
+// The driver folds the signals only: a spinning prologue in every block would
+// hold the SMs a prefetch on another stream could use while a peer is late.
+constexpr uint64_t kP2PTimeoutNs = 60ull * 1000 * 1000 * 1000;
+struct P2PSync {
+  const unsigned* flags = nullptr;  // this rank's words (waits)
+  const PeerView* peers = nullptr;  // every rank's words (signals)
+  unsigned* done = nullptr;         // arrival counter of the signalling kernel (0 between launches)
+  int world = 0, rank = 0;
+  int wait_b = -1, sig_b = -1;
+  unsigned epoch = 0;
+};
+
+__device__ void p2p_spin(const unsigned* flags, int world, int b, unsigned epoch) {
+  const unsigned* f = flags + b * world + threadIdx.x;
+  unsigned v;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (unsigned k = 1;; ++k) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (static_cast<int>(v - epoch) >= 0) break;
+    if ((k & 1023) == 0) {  // a peer that never arrives (died, or called fwd/bwd fewer times)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > kP2PTimeoutNs) {
+        printf("embcomm p2p: barrier %d generation %u: rank %d never arrived\n", b, epoch, threadIdx.x);
+        __trap();  // fail the step loudly instead of hanging the GPU
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+__device__ __forceinline__ void p2p_post(const PeerView* peers, int world, int rank, int b, unsigned epoch) {
+  unsigned* f = peers[threadIdx.x].flags + b * world + rank;
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+}
+
+__device__ __forceinline__ void p2p_prologue(const P2PSync& s) {
+  if (s.wait_b < 0) return;
+  if (static_cast<int>(threadIdx.x) < s.world) p2p_spin(s.flags, s.world, s.wait_b, s.epoch);
+  __syncthreads();
+}
+
+__device__ __forceinline__ void p2p_epilogue(const P2PSync& s) {
+  if (s.sig_b < 0) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // this block's writes (local and over NVLink) before its arrival
+    s_last = atomicAdd(s.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) *s.done = 0;
+  __threadfence_system();
+  if (static_cast<int>(threadIdx.x) < s.world) p2p_post(s.peers, s.world, s.rank, s.sig_b, s.epoch);
+}
+
 template <int VEC>
 __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                             const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                             const int32_t* __restrict__ usrc, const float* __restrict__ ugrad, float lr,
                             const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, int rank,
                             int world, uint32_t* __restrict__ pub_slot, float* __restrict__ pub_grad,
-                            int* __restrict__ pub_cnt, int64_t inbox_cap, int part) {
+                            int* __restrict__ pub_cnt, int64_t inbox_cap, int part, P2PSync sync) {
   constexpr int D = VEC * 4;
+  p2p_prologue(sync);
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   const int sub = lane_id() / VEC, c = lane_id() % VEC;
   constexpr int RPW = 32 / VEC;
@@ -255,6 +318,7 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
       atomicAdd(w + 3, -lr * gv.w);
     }
   }
+  p2p_epilogue(sync);
 }
 
 // Owner side, pinned-host shards: source rank p's miss gradients into this
@@ -263,8 +327,9 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
 template <int VEC>
 __global__ void k_p2p_inbox_apply(const uint32_t* __restrict__ idx, const float* __restrict__ grad,
                                   const int* __restrict__ cnt, float* __restrict__ store, float lr,
-                                  uint32_t* __restrict__ ver, unsigned epoch) {
+                                  uint32_t* __restrict__ ver, unsigned epoch, P2PSync sync) {
   constexpr int D = VEC * 4;
+  p2p_prologue(sync);
   const int64_t total = static_cast<int64_t>(*cnt) * VEC;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i / VEC;
@@ -276,6 +341,7 @@ __global__ void k_p2p_inbox_apply(const uint32_t* __restrict__ idx, const float*
     st4(w, v);
     if (c == 0) ver[idx[k]] = epoch;  // read by peers' prefetch patch after barrier 1
   }
+  p2p_epilogue(sync);
 }
 
 // A prefetched batch's host rows were read while the step before ran; rows
@@ -306,8 +372,10 @@ __global__ void k_p2p_patch(const int* __restrict__ ctr, int T, const uint32_t* 
 // One source rank's published hot gradients into this rank's cache replica
 // (launched for p = 0..world-1: every replica sees the same order).
 template <int VEC>
-__global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float* __restrict__ cache, float lr) {
+__global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float* __restrict__ cache, float lr,
+                                P2PSync sync) {
   constexpr int D = VEC * 4;
+  p2p_prologue(sync);
   const PeerView pv = peers[p];
   const int n = *reinterpret_cast<const volatile int*>(pv.pub_cnt);
   const int64_t total = static_cast<int64_t>(n) * VEC;
@@ -320,6 +388,7 @@ __global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float
     v = make_float4(v.x - lr * gv.x, v.y - lr * gv.y, v.z - lr * gv.z, v.w - lr * gv.w);
     st4(w, v);
   }
+  p2p_epilogue(sync);
 }
 
 // Device barrier over peer memory, split in two so a loopback group can
@@ -327,30 +396,25 @@ __global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float
 // Barrier b (0: hot lists published -- every rank is past its forward reads;
 // 1: step applied) of generation `epoch`.
 __global__ void k_p2p_signal(const PeerView* __restrict__ peers, int world, int rank, int b, unsigned epoch) {
-  if (threadIdx.x >= world) return;
+  if (static_cast<int>(threadIdx.x) >= world) return;
   __threadfence_system();  // this rank's writes of the step before the word
-  unsigned* f = peers[threadIdx.x].flags + b * world + rank;
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  p2p_post(peers, world, rank, b, epoch);
 }
-constexpr uint64_t kP2PTimeoutNs = 60ull * 1000 * 1000 * 1000;
 __global__ void k_p2p_wait(const unsigned* __restrict__ flags, int world, int b, unsigned epoch) {
-  if (threadIdx.x >= world) return;
-  const unsigned* f = flags + b * world + threadIdx.x;
-  unsigned v;
-  uint64_t t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (unsigned k = 1;; ++k) {
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (static_cast<int>(v - epoch) >= 0) break;
-    if ((k & 1023) == 0) {  // a peer that never arrives (died, or called fwd/bwd fewer times)
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > kP2PTimeoutNs) {
-        printf("embcomm p2p: barrier %d generation %u: rank %d never arrived\n", b, epoch, threadIdx.x);
-        __trap();  // fail the step loudly instead of hanging the GPU
-      }
-    }
-  }
-  __threadfence_system();
+  if (static_cast<int>(threadIdx.x) < world) p2p_spin(flags, world, b, epoch);
+}
+
+static P2PSync p2p_sync(const Exchange& x, int rank, int wait_b, int sig_b) {
+  P2PSync s;
+  s.flags = x.flags.p;
+  s.peers = x.peers.p;
+  s.done = x.done.p;
+  s.world = x.W;
+  s.rank = rank;
+  s.wait_b = wait_b;
+  s.sig_b = sig_b;
+  s.epoch = x.epoch;
+  return s;
 }
 
 static int grid_rows(int64_t n, int vec4, int device) {
@@ -551,6 +615,10 @@ void Engine::p2p_alloc() {
     x.pub_cnt.alloc(1);
     EC_CUDA(cudaMemset(x.pub_cnt.p, 0, sizeof(int)));
   }
+  if (!x.done.n) {
+    x.done.alloc(1);
+    EC_CUDA(cudaMemset(x.done.p, 0, sizeof(unsigned)));
+  }
   if (x.flags.n < static_cast<size_t>(kP2PBarriers * x.W)) {
     x.flags.alloc(kP2PBarriers * x.W);
     EC_CUDA(cudaMemset(x.flags.p, 0, x.flags.bytes()));
@@ -603,37 +671,44 @@ void Engine::p2p_fwd_begin(cudaStream_t st) {
 }
 
 template <int VEC>
-void Engine::p2p_publish(float lr, cudaStream_t st, int part) {
+void Engine::p2p_publish(float lr, cudaStream_t st, int part, int wait_b, int sig_b) {
   Exchange& x = *ex;
   if (part & 1) EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
   k_p2p_apply<VEC><<<row_grid(), 256, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, usrc.p,
                                                    ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.pub_slot.p,
                                                    x.pub_grad.p, x.pub_cnt.p,
-                                                   storage == EC_STORAGE_HOST ? x.inbox_cap : 0, part);
+                                                   storage == EC_STORAGE_HOST ? x.inbox_cap : 0, part,
+                                                   p2p_sync(x, rank, wait_b, sig_b));
   launched();
 }
 void Engine::p2p_bwd_publish(float lr, cudaStream_t st) {
   if (!ex->step_open) invalid("the peer-memory exchange takes one backward per forward");
   PhaseScope ph(prof, kPhaseExchange, st);
-  // hits; pinned-host shards also their misses (inbox appends change no row)
-  EC_DISPATCH_VEC(p2p_publish, lr, st, storage == EC_STORAGE_HOST ? 3 : 1);
+  // hits; pinned-host shards also their misses (inbox appends change no row);
+  // the last block signals barrier 0
+  EC_DISPATCH_VEC(p2p_publish, lr, st, storage == EC_STORAGE_HOST ? 3 : 1, -1, 0);
 }
 
 template <int VEC>
 void Engine::p2p_hot(float lr, cudaStream_t st) {
   Exchange& x = *ex;
-  if (storage != EC_STORAGE_HOST) p2p_publish<VEC>(lr, st, 2);  // misses: atomics into the owners' rows
-  if (x.inbox_cap && storage == EC_STORAGE_HOST) {  // owner: every source's miss gradients, rank order
+  // (after the barrier-0 wait kernel: a one-block spin leaves the SMs to a
+  // prefetch on another stream, a spinning prologue in every block would not);
+  // the last kernel signals barrier 1 from its last block
+  const bool host = storage == EC_STORAGE_HOST;
+  if (!host) p2p_publish<VEC>(lr, st, 2, -1, -1);  // misses: atomics into the owners' rows
+  if (host) {  // owner: every source's miss gradients, rank order (inbox allocated by p2p_alloc)
     for (int p = 0; p < x.W; ++p) {
       k_p2p_inbox_apply<VEC><<<host_grid(), 256, 0, st>>>(x.inbox_idx.p + p * x.inbox_cap,
                                                           x.inbox_grad.p + p * x.inbox_cap * D, x.inbox_cnt.p + p,
-                                                          store_base, lr, x.ver.p, x.epoch);
+                                                          store_base, lr, x.ver.p, x.epoch, p2p_sync(x, rank, -1, -1));
       launched();
     }
     EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append after barrier 1
   }
   for (int p = 0; p < ex->W; ++p) {
-    k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr);
+    k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr,
+                                                                p2p_sync(x, rank, -1, p == ex->W - 1 ? 1 : -1));
     launched();
   }
 }
@@ -648,8 +723,7 @@ void Engine::p2p_patch_prefetched(cudaStream_t st) { EC_DISPATCH_VEC(p2p_patch, 
 void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseExchange, st);
   p2p_wait(0, ex->epoch, st);
-  EC_DISPATCH_VEC(p2p_hot, lr, st);
-  p2p_signal(1, st);
+  EC_DISPATCH_VEC(p2p_hot, lr, st);  // its last kernel signals barrier 1
   ex->step_open = false;
 }
 
@@ -888,8 +962,7 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
       for (int r = 0; r < W; ++r) {
         Engine& e = g->members[r]->e;
         e.scatter_grads(grads[r], st);
-        e.p2p_bwd_publish(lr, st);
-        e.p2p_signal(0, st);
+        e.p2p_bwd_publish(lr, st);  // (its last block signals barrier 0)
       }
       for (int r = 0; r < W; ++r) g->members[r]->e.p2p_bwd_finish(lr, st);
       return;
