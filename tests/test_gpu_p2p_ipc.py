@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ROWS, D, B, P, SEED, LR = [5000, 37, 20000], 16, 64, 5, 7, 0.25
-WORLD, STEPS = 2, 3
+STEPS = 3
 PROBE = 400  # rows per table read back at the end
 
 
@@ -65,7 +65,7 @@ def _probe(m, rank, world, caches):
     return out
 
 
-def _worker(rank, port, q, storage, prefetch, repeat):
+def _worker(rank, port, q, storage, prefetch, repeat, WORLD):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -101,10 +101,11 @@ def _worker(rank, port, q, storage, prefetch, repeat):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("storage,prefetch,repeat", [("hbm", False, False), ("host", False, False),
-                                                     ("hbm", True, False), ("host", True, False),
-                                                     ("host", True, True)])
-def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch, repeat):
+@pytest.mark.parametrize("storage,prefetch,repeat,WORLD", [("hbm", False, False, 2), ("host", False, False, 2),
+                                                           ("hbm", True, False, 2), ("host", True, False, 2),
+                                                           ("host", True, True, 2), ("hbm", True, True, 3),
+                                                           ("host", True, True, 3)])
+def test_p2p_ipc_processes_match_loopback(ec, storage, prefetch, repeat, WORLD):
     import torch
     import torch.multiprocessing as mp
     # expected: the loopback group (staged copies) in this process
@@ -129,7 +130,7 @@ def test_p2p_ipc_two_processes_match_loopback(ec, storage, prefetch, repeat):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q, storage, prefetch, repeat)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, storage, prefetch, repeat, WORLD)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = {}
