@@ -107,6 +107,104 @@ static void interference(float4* host, int rows_total, void* bulk_host) {
   }
 }
 
+// HBM-bound neighbour: a grid-stride copy over all SMs (what the pool/scatter
+// do beside the host gather in a pipelined step)
+__global__ void k_hbm_copy(const float4* __restrict__ a, float4* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+// the engine's host gather chain: queue slot -> unique index -> id -> row
+template <int VEC>
+__global__ void k_read_chain(const float4* __restrict__ host, const uint32_t* __restrict__ missq,
+                             const uint32_t* __restrict__ uniq, int n, float4* __restrict__ out) {
+  const int lanes = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * VEC; i += lanes) {
+    const int q = i / VEC, c = i % VEC;
+    const uint32_t g = missq[q];
+    out[static_cast<size_t>(g) * VEC + c] = host[static_cast<size_t>(uniq[g]) * VEC + c];
+  }
+}
+
+static void chain_cost(float4* host, int rows_total) {
+  const int n = 7187, U = 75000;
+  std::mt19937 rng(17);
+  std::vector<uint32_t> uniq(U), missq(n);
+  for (auto& x : uniq) x = rng() % rows_total;
+  for (auto& x : missq) x = rng() % U;
+  uint32_t *du, *dq, *didx;
+  float4* buf;
+  CK(cudaMalloc(&du, U * 4));
+  CK(cudaMalloc(&dq, n * 4));
+  CK(cudaMalloc(&didx, n * 4));
+  CK(cudaMalloc(&buf, static_cast<size_t>(U) * 64));
+  CK(cudaMemcpy(du, uniq.data(), U * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dq, missq.data(), n * 4, cudaMemcpyHostToDevice));
+  std::vector<uint32_t> flat(n);
+  for (int i = 0; i < n; ++i) flat[i] = uniq[missq[i]];
+  CK(cudaMemcpy(didx, flat.data(), n * 4, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int mode = 0; mode < 2; ++mode) {
+    float best = 1e9f;
+    for (int it = 0; it < 10; ++it) {
+      CK(cudaEventRecord(a));
+      if (mode == 0) k_read<4><<<16, 256>>>(host, didx, n, buf);
+      else k_read_chain<4><<<16, 256>>>(host, dq, du, n, buf);
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    std::printf("  %s: %.1f us\n", mode == 0 ? "row index precomputed" : "queue -> unique -> id chain", best * 1e3);
+  }
+}
+
+static void hbm_interference(float4* host, int rows_total) {
+  const int n = 7187;
+  std::mt19937 rng(13);
+  std::vector<uint32_t> idx(n);
+  for (auto& x : idx) x = rng() % rows_total;
+  uint32_t* didx;
+  float4* buf;
+  CK(cudaMalloc(&didx, n * 4));
+  CK(cudaMalloc(&buf, static_cast<size_t>(n) * 64));
+  CK(cudaMemcpy(didx, idx.data(), n * 4, cudaMemcpyHostToDevice));
+  const size_t hb = 1ull << 30;
+  float4 *ha, *hbuf;
+  CK(cudaMalloc(&ha, hb));
+  CK(cudaMalloc(&hbuf, hb));
+  cudaStream_t s1, s2;
+  CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaEvent_t a, b, c;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(cudaEventCreate(&c));
+  for (int mode = 0; mode < 3; ++mode) {  // 0 rows alone, 1 beside an HBM copy (4 CTAs/SM), 2 beside 1 CTA/SM
+    float best = 1e9f, bestc = 1e9f;
+    for (int it = 0; it < 8; ++it) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(a, s1));
+      CK(cudaStreamWaitEvent(s2, a, 0));
+      if (mode) k_hbm_copy<<<148 * (mode == 1 ? 4 : 1), 256, 0, s2>>>(ha, hbuf, hb / 16 / 8);
+      CK(cudaEventRecord(c, s2));
+      k_read<4><<<16, 256, 0, s1>>>(host, didx, n, buf);
+      CK(cudaEventRecord(b, s1));
+      CK(cudaDeviceSynchronize());
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+      CK(cudaEventElapsedTime(&ms, a, c));
+      bestc = std::min(bestc, ms);
+    }
+    std::printf("  rows %s: %.1f us (copy %.1f us)\n", mode == 0 ? "alone" : mode == 1 ? "+HBM copy 4 CTAs/SM" : "+HBM copy 1 CTA/SM",
+                best * 1e3, mode ? bestc * 1e3 : 0.f);
+  }
+}
+
 static int gpu_numa_node() {
   char bus[64];
   CK(cudaDeviceGetPCIBusId(bus, sizeof(bus), 0));
@@ -263,6 +361,14 @@ int main(int argc, char** argv) {
     std::printf("sequential 256 MiB: H2D %.1f GB/s  D2H %.1f GB/s\n", 0.256 * 1.048576 / (h2d * 1e-3),
                 0.256 * 1.048576 / (d2h * 1e-3));
     CK(cudaFree(d));
+  }
+  if (argc > 4 && std::string(argv[4]) == "chain") {
+    chain_cost(host, static_cast<int>(bytes / 64));
+    return 0;
+  }
+  if (argc > 4 && std::string(argv[4]) == "hbm") {
+    hbm_interference(host, static_cast<int>(bytes / 64));
+    return 0;
   }
   if (argc > 4 && std::string(argv[4]) == "interference") {
     void* bulk_host;
