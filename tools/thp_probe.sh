@@ -1,3 +1,4 @@
+# Transparent-huge-page / hugetlb probe of the GPU box (backs the host-tier allocation choice in engine.cu alloc_host_tier).
 mkdir -p gpurun_out
 { cat /sys/kernel/mm/transparent_hugepage/enabled; cat /sys/kernel/mm/transparent_hugepage/defrag; 
 python - <<'PY'
