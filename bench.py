@@ -544,10 +544,14 @@ def run_ours(args, wl):
     pb = [phase_bytes(s, wl, T, fused) for s in stats]
     mean_bytes = {k: S.mean(p[k] for p in pb) for k in pb[0]}
     pfile = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peaks = json.load(open(pfile)) if os.path.exists(pfile) else {}
-    peak = float(peaks.get("hbm_gbs") or 6650.0)
-    peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy, burst) - of measured" if peaks.get("hbm_gbs") else
-                "B200_PROFILING.md fallback 6.65 TB/s (MEASURED_PEAKS.json absent) - of fallback")
+    try:
+        peaks = json.load(open(pfile)) if os.path.exists(pfile) else {}
+        measured = float(peaks["hbm_gbs"]) if isinstance(peaks, dict) and peaks.get("hbm_gbs") else None
+    except (ValueError, TypeError, OSError):
+        measured = None
+    peak = measured or 6650.0
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (STREAM-style copy) - of measured" if measured else
+                "B200_PROFILING.md fallback 6.65 TB/s (MEASURED_PEAKS.json absent or without hbm_gbs) - of fallback")
     phases = {}
     for name, tot in prof["ms"].items():
         calls = prof["calls"][name]
