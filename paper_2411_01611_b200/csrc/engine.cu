@@ -196,11 +196,12 @@ int Engine::row_grid() const {
     const char* v = std::getenv("EC_ROW_CTAS_PER_SM");
     return v ? std::atoi(v) : 0;
   }();
-  // measured per regime: host tier 3 (leaves slots to the host-link kernels);
-  // fused HBM tier 5 (Kaggle 0.0618 -> 0.0596 ms; the fifth CTA per SM waits
-  // for registers and fills SMs the concurrent dedup frees); tile/transpose
-  // HBM path 4 (TB 0.398 vs 0.409, cfg1 0.195 vs 0.201 at 5)
-  return sm_count(device) * (env > 0 ? env : storage == EC_STORAGE_HOST ? 3 : fused() ? 5 : 4);
+  // measured per regime: fused HBM tier 5 (Kaggle 0.0618 -> 0.0596 ms; the
+  // fifth CTA per SM waits for registers and fills SMs the concurrent dedup
+  // frees); pinned-host tier 4 (Kaggle 0.1042-0.1046 at 3, 0.1017-0.1020 at
+  // 4, interleaved); tile/transpose HBM path 4 (TB 0.398 vs 0.409, cfg1
+  // 0.195 vs 0.201 at 5)
+  return sm_count(device) * (env > 0 ? env : storage == EC_STORAGE_HBM && fused() ? 5 : 4);
 }
 
 static uint32_t log2_ceil(uint64_t x) {

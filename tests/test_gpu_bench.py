@@ -43,12 +43,24 @@ def test_bench_single_gpu_line():
     assert d["gpu_launches"] > 0
 
 
+def _first_traceback(err):
+    i = err.find("Traceback")
+    return err[i:i + 4000] if i >= 0 else err[-3000:]
+
+
 def test_bench_two_ranks_peer_exchange():
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--no-cpu-baseline", "--schedule-batches", "0", "--workload", "kaggle_hbm"]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stderr[-3000:]
+    # Two ranks time-slice one GPU beside this process's own context, so a
+    # launch can be slow; one retry (fresh port) before the failure is reported.
+    errs = []
+    for _ in range(2):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps",
+               "3", "--warmup", "3", "--no-cpu-baseline", "--schedule-batches", "0", "--workload", "kaggle_hbm"]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+        if r.returncode == 0:
+            break
+        errs.append(_first_traceback(r.stderr))
+    assert r.returncode == 0, "\n----\n".join(errs)
     lines = _json_lines(r.stdout)
     assert len(lines) == 1  # rank 0 only
     d = lines[0]
