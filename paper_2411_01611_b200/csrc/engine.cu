@@ -675,14 +675,10 @@ void Engine::fwd_pool(cudaStream_t st) {
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
     const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p};
     const int pb = row_grid(), rb = sm_count(device);
-    // bags in flight per thread: 4 with HBM rows, 8 beside the host-link
-    // kernels (measured, Kaggle: HBM tier 0.0647 -> 0.0615 ms at 4; host tier
-    // 0.1008 -> 0.107 ms at 4, 0.107 at 16)
-    if (!bag_off && geom_p == 1 && storage == EC_STORAGE_HBM)
+    // 4 bags in flight per thread (measured, Kaggle: HBM tier 0.0647 -> 0.0615
+    // ms vs 8; host tier, with 4 row CTAs per SM, 0.1007-0.1014 -> 0.0984-0.0995)
+    if (!bag_off && geom_p == 1)
       k_pool1<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
-                                                          pb, ro);
-    else if (!bag_off && geom_p == 1)
-      k_pool1<VEC, 8, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
                                                           pb, ro);
     else
       k_pool<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
