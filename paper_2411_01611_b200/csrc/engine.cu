@@ -689,7 +689,8 @@ void Engine::fwd_pool(cudaStream_t st) {
   if (!bag_off && geom_p == 1) {
     k_pool1<VEC, 8><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr);
   } else {
-    k_pool<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+    // 2 bags of P lookups in flight per thread (cfg1, P=20: 0.1924-0.1937 ms at 4, 0.1910-0.1913 at 2, 0.232 at 8)
+    k_pool<VEC, 2><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
                                                     bag_off, inv.p, urows.p, out_ptr);
   }
   launched();
