@@ -659,9 +659,15 @@ void Engine::fwd_gather_local(cudaStream_t st) {
   }
   if (fused()) return;  // the pool reads cached / HBM rows where they are
   PhaseScope ph(prof, kPhaseGather, st);
-  k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
-                                              ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world,
-                                              p2p_peers(), p2p_shard_off());
+  // rows in flight per lane group: 2 for single-rank pooling-1 batches (TB
+  // shape 0.395 -> 0.3855 ms), else 4 (cfg1, P=20: 0.191 at 4, 0.208 at 2)
+  if (world == 1 && geom_p == 1 && !bag_off)
+    k_gather<VEC, 2><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
+                                                ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world);
+  else
+    k_gather<VEC, 4><<<grid, kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, uslot.p, usrc.p, cache.p, urows.p,
+                                                ugrad.p, cnt.p, storage == EC_STORAGE_HBM ? 1 : 0, rank, world,
+                                                p2p_peers(), p2p_shard_off());
   launched();
 }
 
