@@ -170,8 +170,10 @@ int Engine::host_grid() const {
   // and deeper queues only stall the concurrent pool/dedup/scatter.  Measured
   // on the pipelined Kaggle step: 12/16/24/32 CTAs 0.099-0.103/0.100-0.104/
   // 0.103-0.110/0.107-0.113 ms; 8 CTAs starve the link (0.109), TMA at 296
-  // CTAs 0.105-0.107 with the pool slowed 14 -> 30 us.
-  return host_tma() ? sm_count(device) * 2 : 16;
+  // CTAs 0.105-0.107 with the pool slowed 14 -> 30 us.  Re-measured with the
+  // final row grid and pool (gather and write-back together, interleaved):
+  // 16/20/24 CTAs 0.1015-0.1034 / 0.0995-0.1001 / 0.1036-0.1047 ms.
+  return host_tma() ? sm_count(device) * 2 : 20;
 }
 // Host-link row traffic goes through SM loads/stores (k_gather_host /
 // k_apply_host) unless EC_HOST_TMA=1 selects the TMA bulk-copy kernels; with
