@@ -266,7 +266,7 @@ enum { EC_STORAGE_HBM = 0, EC_STORAGE_HOST = 1 };
 
 typedef struct {
   uint32_t num_tables;
-  uint32_t dim;                  /* D, fp32 elements per row; multiple of 4 */
+  uint32_t dim;                  /* D, fp32 elements per row: 4, 8, 16, 32, 64 or 128 */
   const uint64_t* rows_host;     /* E_t per table, each in [1, 2^32-1] */
   int32_t storage;               /* cold tier: EC_STORAGE_HBM or EC_STORAGE_HOST (pinned) */
   int32_t rank, world;           /* row sharding: owner(id) = id % world, local row id / world */

@@ -99,20 +99,35 @@ __global__ void k_set_remap(int32_t* __restrict__ remap, const uint32_t* __restr
     remap[ids[j]] = static_cast<int32_t>(slot0 + j);
 }
 
-// cache rows <- authoritative storage (world == 1) or the synthetic init.
+// Cache rows of a new placement, each from where its current value lives:
+// the old cache replica (rows cached before and after; replicas are
+// bit-identical across ranks), this rank's own shard, a peer's shard over the
+// peer-memory exchange (rows never cached since the last flush, so the owner's
+// copy is current), or -- before any training -- the synthetic init.  A row
+// none of these can supply sets *err (the caller rejects the placement).
 __global__ void k_fill_cache(float* __restrict__ cache, const uint32_t* __restrict__ ids, const uint16_t* __restrict__ tabs,
-                             uint64_t k, const TableDev* __restrict__ td, uint32_t D, int from_store, uint64_t seed,
-                             float scale, int rank, int world) {
+                             uint64_t k, const TableDev* __restrict__ td, uint32_t D, const float* __restrict__ old_cache,
+                             const int32_t* __restrict__ old_remap, const int64_t* __restrict__ remap_off,
+                             const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, uint32_t T,
+                             int synth_ok, uint64_t seed, float scale, int rank, int world, int* __restrict__ err) {
   const uint64_t n = k * D;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t j = i / D;
     const uint32_t c = static_cast<uint32_t>(i - j * D);
     const uint32_t id = ids[j];
     const uint32_t t = tabs[j];
-    if (from_store && static_cast<int>(id % world) == rank)
+    const int o = static_cast<int>(id % world);
+    const int32_t os = old_remap ? old_remap[remap_off[t] + id] : -1;
+    if (os >= 0)
+      cache[i] = old_cache[static_cast<uint64_t>(os) * D + c];
+    else if (o == rank)
       cache[i] = td[t].store[static_cast<uint64_t>(id / world) * D + c];
-    else
+    else if (peers)
+      cache[i] = peers[o].store[static_cast<uint64_t>(shard_off[static_cast<int64_t>(o) * (T + 1) + t] + id / world) * D + c];
+    else if (synth_ok)
       cache[i] = synth_value(seed, scale, t, id, D, c);
+    else
+      atomicExch(err, 1);
   }
 }
 
@@ -313,7 +328,8 @@ Engine::~Engine() {
 void Engine::create(const ec_tables_config& c) {
   if (c.num_tables < 1) invalid("need at least one table");
   if (c.num_tables > 65535) invalid("at most 65535 tables");
-  if (c.dim < 4 || c.dim % 4 != 0 || c.dim > 1024) invalid("dim must be a multiple of 4 in [4, 1024]");
+  if (c.dim != 4 && c.dim != 8 && c.dim != 16 && c.dim != 32 && c.dim != 64 && c.dim != 128)
+    invalid("dim must be one of 4, 8, 16, 32, 64, 128 (the row kernels' vector widths)");
   if (c.world < 1 || c.rank < 0 || c.rank >= c.world) invalid("rank/world out of range");
   if (c.storage != EC_STORAGE_HBM && c.storage != EC_STORAGE_HOST) invalid("unknown storage tier");
   if (c.max_lookups_per_table < 1 || c.max_lookups_per_table > (1ull << 30))
@@ -381,6 +397,10 @@ void Engine::create(const ec_tables_config& c) {
     b.utab.alloc(N);
     b.urows.alloc(N * D);
     b.ugrad.alloc(N * D);
+    b.g64.alloc(N * D);
+    EC_CUDA(cudaMemset(b.g64.p, 0, b.g64.bytes()));
+    b.ucount.alloc(N);
+    EC_CUDA(cudaMemset(b.ucount.p, 0, b.ucount.bytes()));
     b.status.alloc(max_tiles + 1);
     b.ctr.alloc(counters_size(T));
     b.cnt.alloc(N);
@@ -458,6 +478,8 @@ void Engine::select(int i) {
   utab = view(b.utab);
   urows = view(b.urows);
   ugrad = view(b.ugrad);
+  g64 = view(b.g64);
+  ucount = view(b.ucount);
   status = view(b.status);
   tstat = view(b.tstat);
   ctr = view(b.ctr);
@@ -477,6 +499,8 @@ uint64_t Engine::device_bytes() const {
 void Engine::init_synthetic(uint64_t seed, float scale, cudaStream_t st) {
   use_device(device);
   join_host_writes(st);
+  drop_prefetch(st);  // prefetched batches hold copies of the old rows
+  ++geom_version;
   for (uint32_t t = 0; t < T; ++t) {
     if (!local_rows[t]) continue;
     const uint64_t n = local_rows[t] * D;
@@ -487,6 +511,7 @@ void Engine::init_synthetic(uint64_t seed, float scale, cudaStream_t st) {
   synth_seed = seed;
   synth_scale = scale;
   synth_valid = true;
+  rows_trained = false;
   if (cache_k_total) fill_cache(st, /*from_store=*/world == 1);
 }
 
@@ -496,8 +521,10 @@ void Engine::fill_cache(cudaStream_t st, bool from_store) {
     invalid("multi-rank cache placement needs ec_tables_init_synthetic first (rows of other shards are not local)");
   const uint64_t n = cache_k_total * D;
   const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, persistent_grid(device) * 4ull));
-  k_fill_cache<<<grid, 256, 0, st>>>(cache.p, cache_ids.p, cache_tab.p, cache_k_total, tdev.p, D, from_store ? 1 : 0,
-                                     synth_seed, synth_scale, rank, world);
+  // (re)initialised tables: every row is its synthetic value, shards included
+  k_fill_cache<<<grid, 256, 0, st>>>(cache.p, cache_ids.p, cache_tab.p, cache_k_total, tdev.p, D, nullptr, nullptr,
+                                     nullptr, nullptr, nullptr, T, 1, synth_seed, synth_scale,
+                                     from_store ? rank : -1, world, nullptr);
   EC_LAUNCH();
 }
 
@@ -526,8 +553,40 @@ void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
     koff[t + 1] = all_ids.size();
   }
   if (all_ids.size() > 0x7FFFFFFFull) invalid("cache larger than 2^31 rows");
+  // pending prefetches hold cache-slot numbers and row copies of the old
+  // placement: drop them (and their graphs) before anything changes
+  drop_prefetch(nullptr);
+  ++geom_version;
+  clear_graphs();
   EC_CUDA(cudaDeviceSynchronize());
-  // write back the current cache before dropping it
+  const uint64_t K = all_ids.size();
+  DevBuf<float> ncache(K * D);
+  DevBuf<uint32_t> nids(K);
+  DevBuf<uint16_t> ntab(K);
+  DevBuf<int> derr(1);
+  EC_CUDA(cudaMemset(derr.p, 0, sizeof(int)));
+  if (K) {
+    EC_CUDA(cudaMemcpy(nids.p, all_ids.data(), K * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    EC_CUDA(cudaMemcpy(ntab.p, all_tab.data(), K * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    // new rows from the old replica, the own shard, a peer's shard, or the
+    // synthetic init while nothing has been trained (remap is still the old one)
+    DevBuf<int64_t> roff(T);
+    EC_CUDA(cudaMemcpy(roff.p, remap_off.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice));
+    const int grid = static_cast<int>(std::min<uint64_t>((K * D + 255) / 256, persistent_grid(device) * 4ull));
+    k_fill_cache<<<grid, 256>>>(ncache.p, nids.p, ntab.p, K, tdev.p, D, cache.p, cache_k_total ? remap.p : nullptr,
+                                roff.p, p2p_peers(), p2p_shard_off(), T, synth_valid && !rows_trained ? 1 : 0,
+                                synth_seed, synth_scale, rank, world, derr.p);
+    EC_LAUNCH();
+    EC_CUDA(cudaDeviceSynchronize());
+    int e = 0;
+    EC_CUDA(cudaMemcpy(&e, derr.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e)
+      invalid(synth_valid ? "cache placement after training needs the peer-memory exchange: rows of other shards "
+                            "are not readable from this rank"
+                          : "multi-rank cache placement needs ec_tables_init_synthetic first (rows of other "
+                            "shards are not local)");
+  }
+  // write the old cache's owned rows back to the shard before dropping it
   if (cache_k_total) {
     const uint64_t n = cache_k_total * D;
     const int grid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, persistent_grid(device) * 4ull));
@@ -535,24 +594,21 @@ void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
     EC_LAUNCH();
   }
   EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
-  clear_graphs();
-  cache_k_total = all_ids.size();
+  cache_k_total = K;
   cache_k.resize(T);
   for (uint32_t t = 0; t < T; ++t) cache_k[t] = koff[t + 1] - koff[t];
-  cache.alloc(cache_k_total * D);
-  cache_ids.alloc(cache_k_total);
-  cache_tab.alloc(cache_k_total);
-  if (cache_k_total) {
-    EC_CUDA(cudaMemcpy(cache_ids.p, all_ids.data(), cache_k_total * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    EC_CUDA(cudaMemcpy(cache_tab.p, all_tab.data(), cache_k_total * sizeof(uint16_t), cudaMemcpyHostToDevice));
-    for (uint32_t t = 0; t < T; ++t) {
-      const uint64_t kt = koff[t + 1] - koff[t];
-      if (!kt) continue;
-      k_set_remap<<<static_cast<int>(std::min<uint64_t>((kt + 255) / 256, 4096)), 256>>>(
-          remap.p + remap_off[t], cache_ids.p + koff[t], kt, static_cast<int64_t>(koff[t]));
-      EC_LAUNCH();
-    }
-    fill_cache(nullptr, /*from_store=*/world == 1);
+  std::swap(cache.p, ncache.p);
+  std::swap(cache.n, ncache.n);
+  std::swap(cache_ids.p, nids.p);
+  std::swap(cache_ids.n, nids.n);
+  std::swap(cache_tab.p, ntab.p);
+  std::swap(cache_tab.n, ntab.n);
+  for (uint32_t t = 0; t < T; ++t) {
+    const uint64_t kt = koff[t + 1] - koff[t];
+    if (!kt) continue;
+    k_set_remap<<<static_cast<int>(std::min<uint64_t>((kt + 255) / 256, 4096)), 256>>>(
+        remap.p + remap_off[t], cache_ids.p + koff[t], kt, static_cast<int64_t>(koff[t]));
+    EC_LAUNCH();
   }
   EC_CUDA(cudaDeviceSynchronize());
 }
@@ -568,6 +624,11 @@ void Engine::rw_rows(uint32_t t, const uint32_t* ids, uint64_t n, float* buf_hos
   EC_CUDA(cudaMemcpy(dids.p, ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
   if (write) EC_CUDA(cudaMemcpy(dbuf.p, buf_host, n * D * sizeof(float), cudaMemcpyHostToDevice));
   const int grid = static_cast<int>(std::min<uint64_t>((n * D + 255) / 256, 4096));
+  if (write) {
+    drop_prefetch(nullptr);  // prefetched batches may hold copies of these rows
+    ++geom_version;
+    rows_trained = true;
+  }
   EC_CUDA(cudaDeviceSynchronize());
   k_rw_rows<<<grid, 256>>>(tdev.p, t, dids.p, n, D, cache.p, dbuf.p, write ? 1 : 0, rank, world, derr.p);
   EC_LAUNCH();
@@ -681,7 +742,7 @@ void Engine::fwd_pool(cudaStream_t st) {
   if (fused()) {
     // rows read at their source; trailing blocks empty this batch's dedup set
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
-    const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p};
+    const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p, cnt.p};
     const int pb = row_grid(), rb = sm_count(device);
     // 4 bags in flight per thread (measured, Kaggle: HBM tier 0.0647 -> 0.0615
     // ms vs 8; host tier, with 4 row CTAs per SM, 0.1007-0.1014 -> 0.0984-0.0995)
@@ -709,10 +770,12 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
   if (fused()) {
     // -lr * grad scattered straight into the cache / HBM rows (SGD in the
-    // scatter); pinned-host misses accumulate in ugrad for the host write-back
+    // scatter) for a row's first kLightAdds partials, the rest summed in fp64
+    // (g64) for k_apply_g64; pinned-host misses accumulate in ugrad
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
     k_scatter<VEC, 4, true><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
-                                                             bag_off, inv.p, grad, ugrad.p, rs, bwd_lr);
+                                                             bag_off, inv.p, grad, ugrad.p, g64.p,
+                                                             bb[cur].counted ? ucount.p : nullptr, ctr.p, rs, bwd_lr);
     launched();
     return;
   }
@@ -723,13 +786,19 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   const bool atomic = scatter_mode == 1 || (scatter_mode == 0 && max_n_batch < 32768);
   if (atomic) {
     k_scatter<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
-                                                       bag_off, inv.p, grad, ugrad.p);
+                                                       bag_off, inv.p, grad, ugrad.p, g64.p,
+                                                       bb[cur].counted ? ucount.p : nullptr, ctr.p);
+    launched();
+    k_g64_finalize<VEC><<<row_grid(), kThreads, 0, st>>>(nullptr, bb[cur].counted ? ucount.p : nullptr, ctr.p,
+                                                         static_cast<int>(T), ugrad.p, g64.p);
     launched();
     return;
   }
   if (!ntiles) return;
   if (bb[cur].lists) {  // the forward grouped the lookups already (tile path)
-    k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p);
+    k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
+    launched();
+    k_g64_finalize<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, nullptr, ctr.p, static_cast<int>(T), ugrad.p, g64.p);
     launched();
     return;
   }
@@ -746,7 +815,9 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   k_bwd_fill<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, tdev.p, bag_off, static_cast<int>(T), static_cast<int>(geom_b),
                                          static_cast<int>(geom_p), inv.p, off.p, cnt.p, list.p);
   launched();
-  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p);
+  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
+  launched();
+  k_g64_finalize<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, nullptr, ctr.p, static_cast<int>(T), ugrad.p, g64.p);
   launched();
 }
 
@@ -816,6 +887,14 @@ void Engine::join_host_writes(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
+  if (fused()) {
+    // w - lr * sum(g) per cache / HBM row; host misses' sums into ugrad
+    PhaseScope ph(prof, kPhaseApply, st);
+    k_apply_g64<VEC><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p,
+                                                      bb[cur].counted ? ucount.p : nullptr, cache.p, ugrad.p, g64.p, lr,
+                                                      host ? 0 : 1);
+    launched();
+  }
   if (host) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     EC_CUDA(cudaStreamIsCapturing(st, &cs));
@@ -827,7 +906,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
       EC_CUDA(cudaEventRecord(ev_grad, st));
     if (world > 1) enqueue_host_writeback<VEC>(lr);
   }
-  if (!fused()) {  // (the SGD scatter already updated every row)
+  if (!fused()) {
     PhaseScope ph(prof, kPhaseApply, st);
     k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
@@ -1157,10 +1236,11 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
   }
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
                                                                          ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
-                                                                         missq.p);
+                                                                         missq.p, ucount.p);
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
+  bb[cur].counted = !use_table_kernel() && use_cluster();
   if (use_table_kernel()) {
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
@@ -1234,6 +1314,7 @@ void Engine::backward(const float* grad, float lr, cudaStream_t st) {
   if (in_group) invalid("this rank belongs to a loopback group: use ec_group_lookup_bwd");
   if (!grad) invalid("null gradient");
   use_device(device);
+  rows_trained = true;
   if (world == 1) {
     uint32_t lr_bits;
     std::memcpy(&lr_bits, &lr, sizeof(lr_bits));

@@ -80,6 +80,8 @@ struct BatchBufs {
   DevBuf<int32_t> usrc;
   DevBuf<uint16_t> utab;
   DevBuf<float> urows, ugrad;
+  DevBuf<int> ucount;  // lookups per unique (cluster dedup; k_scatter's fp32 / fp64 split); zeroed by the backward
+  DevBuf<double> g64;  // fp64 gradient sums of unique rows (fused SGD; rows spanning transpose chunks); self-cleaning
   DevBuf<unsigned long long> status, tstat;  // tile / table look-back words
   DevBuf<int> ctr;
   DevBuf<int> cnt, off, part;          // backward transpose: occurrences per unique, offsets, scan partials
@@ -94,9 +96,10 @@ struct BatchBufs {
   cudaEvent_t ev_ded = nullptr;       // its prefetch's dedup done
   cudaEvent_t ev_pf = nullptr;        // its prefetch complete (dedup + host gather)
   bool lists = false;                 // its forward built the unique-grouped gradient lists
+  bool counted = false;               // its dedup wrote ucount (cluster kernel)
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
-           utab.bytes() + urows.bytes() + ugrad.bytes() + status.bytes() + tstat.bytes() + ctr.bytes() +
+           utab.bytes() + urows.bytes() + ugrad.bytes() + g64.bytes() + ucount.bytes() + status.bytes() + tstat.bytes() + ctr.bytes() +
            cnt.bytes() + off.bytes() + part.bytes() + list.bytes();
   }
 };
@@ -183,6 +186,7 @@ struct Engine {
   uint64_t synth_seed = 0;
   float synth_scale = 0.f;
   bool synth_valid = false;
+  bool rows_trained = false;  // a backward or row write ran since the last synthetic init
 
   // Per-batch state in a ring of kSets buffer sets, so up to kSets-1 next
   // batches can be prefetched (dedup, hit/miss, host-miss gather) while the
@@ -198,6 +202,8 @@ struct Engine {
   View<int32_t> usrc;
   View<uint16_t> utab;
   View<float> urows, ugrad;
+  View<double> g64;
+  View<int> ucount;
   View<unsigned long long> status;  // decoupled look-back words, one per tile
   View<unsigned long long> tstat;   // one per table (cluster dedup)
   bool cluster_fits = false;        // every table's batch fits one cluster
@@ -326,6 +332,7 @@ struct Engine {
   void attach_comm(const uint8_t* id128);
   void destroy_comm();
   uint64_t exch_bytes() const;
+  uint64_t geometry_digest() const;  // what every rank of a job must agree on (peer memory is indexed by it)
   void exchange_fwd(cudaStream_t st);
   void exchange_bwd(float lr, cudaStream_t st);
   // peer-memory exchange (exchange.cu)

@@ -730,6 +730,20 @@ void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
 // ------------------------------------------------------------ NCCL driver
 bool Engine::comm_ready() const { return ex != nullptr && (ex->comm != nullptr || in_group || ex->p2p); }
 
+// Tables, dims, per-table rows, batch capacity and storage tier: a peer's
+// shard offsets and inbox segments are computed from the local copy of these,
+// so ranks that disagree would index each other's memory wrongly.
+uint64_t Engine::geometry_digest() const {
+  uint64_t h = mix64(0x65634765ull ^ world);
+  auto add = [&](uint64_t v) { h = mix64(h ^ (v + kGolden)); };
+  add(T);
+  add(D);
+  add(max_n);
+  add(static_cast<uint64_t>(storage));
+  for (uint64_t r : rows) add(r);
+  return h;
+}
+
 void Engine::attach_comm(const uint8_t* id128) {
   use_device(device);
   ncclUniqueId id;
@@ -741,6 +755,31 @@ void Engine::attach_comm(const uint8_t* id128) {
     ex->comm = nullptr;
   }
   EC_NCCL(ncclCommInitRank(&ex->comm, world, id, rank));
+  // every rank's geometry digest, compared before any step moves rows
+  DevBuf<uint64_t> dg(static_cast<size_t>(world) + 1);
+  const uint64_t mine = geometry_digest();
+  EC_CUDA(cudaMemcpy(dg.p, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  cudaStream_t s;
+  EC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const ncclResult_t r = ncclAllGather(dg.p, dg.p + 1, 1, ncclUint64, ex->comm, s);
+  const cudaError_t ce = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  std::vector<uint64_t> all(world);
+  if (r == ncclSuccess && ce == cudaSuccess)
+    EC_CUDA(cudaMemcpy(all.data(), dg.p + 1, world * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (r != ncclSuccess || ce != cudaSuccess) {
+    ncclCommDestroy(ex->comm);
+    ex->comm = nullptr;
+    EC_NCCL(r);
+    EC_CUDA(ce);
+  }
+  for (int p = 0; p < world; ++p)
+    if (all[p] != mine) {
+      ncclCommDestroy(ex->comm);
+      ex->comm = nullptr;
+      invalid("rank " + std::to_string(p) + " has a different table geometry (tables, dim, rows, batch "
+              "capacity or storage tier) than rank " + std::to_string(rank));
+    }
 }
 
 void Engine::destroy_comm() {
@@ -951,6 +990,7 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
     cudaStream_t st = as_stream(stream);
     const int W = static_cast<int>(g->members.size());
     const size_t D = g->members[0]->e.D;
+    for (int r = 0; r < W; ++r) g->members[r]->e.rows_trained = true;
     if (g->members[0]->e.p2p_on()) {
       for (int r = 0; r < W; ++r) {  // validate before enqueuing anything
         Engine& e = g->members[r]->e;
@@ -1026,6 +1066,8 @@ struct HostSeg {
   int64_t pid, fd;
   uint64_t bytes;
   int64_t present;
+  uint64_t geometry;  // Engine::geometry_digest of the exporting rank
+  int64_t rank;
 };
 constexpr uint64_t kP2PBlob = kP2PHandles * sizeof(cudaIpcMemHandle_t) + sizeof(HostSeg);
 }  // namespace
@@ -1049,10 +1091,14 @@ int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len
       EC_CUDA(cudaIpcGetMemHandle(&h, ptrs[k]));
       std::memcpy(blob + k * sizeof(h), &h, sizeof(h));
     }
+    HostSeg hs{0, 0, 0, 0, e.geometry_digest(), e.rank};
     if (e.storage == EC_STORAGE_HOST) {
-      const HostSeg hs{static_cast<int64_t>(getpid()), e.store_host_fd, e.store_host_bytes, 1};
-      std::memcpy(blob + kP2PHandles * sizeof(cudaIpcMemHandle_t), &hs, sizeof(hs));
+      hs.pid = static_cast<int64_t>(getpid());
+      hs.fd = e.store_host_fd;
+      hs.bytes = e.store_host_bytes;
+      hs.present = 1;
     }
+    std::memcpy(blob + kP2PHandles * sizeof(cudaIpcMemHandle_t), &hs, sizeof(hs));
   });
 }
 
@@ -1076,6 +1122,10 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
       HostSeg hs;
       std::memcpy(&hs, blobs + p * blob_len + kP2PHandles * sizeof(cudaIpcMemHandle_t), sizeof(hs));
       if (hs.present != (e.storage == EC_STORAGE_HOST ? 1 : 0)) invalid("ranks disagree on the storage tier");
+      if (hs.rank != p) invalid("p2p blob " + std::to_string(p) + " was exported by rank " + std::to_string(hs.rank));
+      if (hs.geometry != e.geometry_digest())
+        invalid("rank " + std::to_string(p) + " has a different table geometry (tables, dim, rows, batch capacity "
+                "or storage tier) than rank " + std::to_string(e.rank));
     }
     std::vector<PeerView> views(e.world);
     for (int p = 0; p < e.world; ++p) {

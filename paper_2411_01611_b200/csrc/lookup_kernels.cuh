@@ -16,7 +16,7 @@
 //                      hash slot and zeroes the unique's gradient row
 //   k_gather_host      pinned-host misses (side stream)
 //   k_pool             EmbeddingBag sum through inverse indices
-//   k_scatter          bag gradients -> unique rows: float4 REDG per distinct row
+//   k_scatter          bag gradients -> unique rows: fp64 RED sums per distinct row (g64)
 //                      of a warp (equal rows pre-summed with shuffles)
 //   k_apply(_host)     SGD into cache rows / owning shard
 #pragma once
@@ -33,6 +33,8 @@ constexpr int kThreads = 256;
 constexpr int kItems = 4;
 constexpr int kTile = kThreads * kItems;  // lookups per dedup tile
 constexpr int kRunChunk = 32;             // grouped-gradient list entries per lane group (K6a)
+// k_bwd_reduce chunks a unique's list entries [a, b) fall in
+__host__ __device__ inline int chunk_span(int a, int b) { return (b - 1) / kRunChunk - a / kRunChunk + 1; }
 
 // ------------------------------------------------------------------ K1
 // Insert (id, lpos) starting at slot h whose current content `cur` was
@@ -506,6 +508,7 @@ struct ResetOut {
   const uint32_t* uslot;
   const int32_t* usrc;
   float* ugrad;
+  int* cnt;  // per-unique add counters of the fused SGD scatter
 };
 template <int VEC>
 __device__ __forceinline__ void reset_sets(const TableDev* td, int T, const ResetOut& ro, int b, int nb) {
@@ -519,6 +522,7 @@ __device__ __forceinline__ void reset_sets(const TableDev* td, int T, const Rese
       const TableDev& tb = td[ro.utab[g]];
       tb.hash[ro.uslot[g]] = kEmptySlot;
       tb.idcnt[ro.uslot[g]] = 0;
+      ro.cnt[g] = 0;
     }
     if (ro.usrc[g] < 0) st4(ro.ugrad + static_cast<int64_t>(g) * D + c * 4, make_float4(0.f, 0.f, 0.f, 0.f));
   }
@@ -640,94 +644,225 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
   }
 }
 
+// ------------------------------------------------- fp64 gradient sums
+// Unique-row gradient sums that many lookups feed are kept in fp64 so the
+// SGD update is one rounding of w - lr * sum(g) (north_star: updated rows
+// within 1e-5 relative of the fp64 restatement; fp32 adds of thousands of
+// gradients into one row drift past that).  Layout interleaved per row so the
+// VEC lanes of a row touch one contiguous stretch per component: element
+// (unique g, lane c, component k) lives at g*D + k*VEC + c.
+template <int VEC>
+__device__ __forceinline__ void red_g64(double* g64, int64_t g, int c, double x, double y, double z, double w) {
+  double* p = g64 + g * (VEC * 4) + c;
+  atomicAdd(p, x);
+  atomicAdd(p + VEC, y);
+  atomicAdd(p + 2 * VEC, z);
+  atomicAdd(p + 3 * VEC, w);
+}
+// read a row's sums and leave zeros behind (the buffer is self-cleaning)
+template <int VEC>
+__device__ __forceinline__ void take_g64(double* g64, int64_t g, int c, double* out) {
+  double* p = g64 + g * (VEC * 4) + c;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = __ldcg(p + k * VEC);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p[k * VEC] = 0.0;
+}
+__device__ __forceinline__ float4 sgd4(float4 w, const double* gs, float lr) {
+  const double l = lr;
+  return make_float4(static_cast<float>(w.x - l * gs[0]), static_cast<float>(w.y - l * gs[1]),
+                     static_cast<float>(w.z - l * gs[2]), static_cast<float>(w.w - l * gs[3]));
+}
+
 // ------------------------------------------------------------------ K6
-// Bags visited table-major (q = t*B + s): the 32/VEC bags a warp holds are
-// consecutive samples of one table, so hot rows repeat inside the warp; lanes
-// with equal (row, component) are summed with shuffles first and one float4
-// REDG per distinct row goes to L2.  R bags in flight per thread.
-//
-// SGD (single rank, fused path): the update itself is scattered, -lr * g as a
-// REDG into the unique's cache row or local HBM shard row, so the backward
-// needs no zeroed ugrad and no K6b apply pass; pinned-host misses still
-// accumulate g in ugrad (zeroed by the dedup kernel) for the host write-back.
-// fp32 adds into w instead of into a gradient sum: the same order-of-summation
-// tolerance (the update is within 1e-5 relative of the fp64 restatement).
+// Each warp owns a contiguous range of one table's bags (T x Wt ranges), so
+// hot rows repeat inside the warp many times over.  Per R-slot window of RPW
+// bags, lanes holding the same row (same component c) are summed with
+// shuffles; then
+//   * rows among the table's first kAcc uniques (first-occurrence order puts a
+//     table's heaviest ids there) are added into the warp's private
+//     shared-memory accumulator -- plain read-modify-write, the leaders of one
+//     window hold distinct rows -- and flushed once when the range ends;
+//   * other rows leave as one RED per window.
+// A row's partials leave the warp either as fp32 REDs (SGD: -lr * v straight
+// into the cache / HBM row, or into ugrad) or, for rows with more than
+// kLightAdds lookups in the batch (the dedup's count, `ucount`), into the
+// row's fp64 sum in g64, rounded once by k_apply_g64 / k_g64_finalize.  So a
+// row sees at most kLightAdds fp32 roundings of partial sums (<= 3.8e-6 of the
+// magnitudes summed, north_star bar 1e-5); without counts (ucount null) every
+// row takes the fp64 path.  Measured (profiles/r02/parity.md): the all-fp32
+// window scatter left the 3-row Kaggle tables' rows 1.1e-5 off (~2K adds
+// each); fp64 REDs per window for heavy rows cost +30 us on the Kaggle
+// scatter (thousands of same-address atomics on a 3-row table's rows), which
+// the per-warp accumulators remove.
+constexpr int kLightAdds = 64;
+
+template <int VEC>
+struct ScatterAcc {
+  static constexpr int D = VEC * 4;
+  static constexpr int kRows = 1024 / D < 8 ? 8 : (1024 / D > 64 ? 64 : 1024 / D);  // rows per warp accumulator
+};
+
 template <int VEC, int R, bool SGD = false>
 __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restrict__ td, int T, int B, int P,
                                                          const int64_t* __restrict__ bag_off,
                                                          const uint32_t* __restrict__ inv, const float* __restrict__ grad,
-                                                         float* __restrict__ ugrad, RowSrc rs = {}, float lr = 0.f) {
+                                                         float* __restrict__ ugrad, double* __restrict__ g64,
+                                                         const int* __restrict__ ucount, const int* __restrict__ ctr,
+                                                         RowSrc rs = {}, float lr = 0.f) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  constexpr int kAcc = ScatterAcc<VEC>::kRows;
+  __shared__ __align__(16) float sacc[kThreads / 32][kAcc * D];
+  const RowMap<VEC> m;
+  const int wib = threadIdx.x >> 5;
+  float* acc = sacc[wib];
+  const Counters cn = counters(const_cast<int*>(ctr), T);
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int wt = max(1, nwarps / T);  // warps (ranges) per table
+  const int per = (B + wt - 1) / wt;
+
+  // one partial of unique u leaves the warp (fp32 RED or fp64 sum, see above)
+  auto emit = [&](uint32_t u, int t, float4 v) {
+    const int n = ucount ? __ldcg(ucount + u) : kLightAdds + 1;
+    const int32_t sr = SGD ? rs.usrc[u] : 0;  // (both loads in flight before the branch)
+    if (n > kLightAdds) {
+      red_g64<VEC>(g64, u, m.c, v.x, v.y, v.z, v.w);
+      return;
+    }
+    float* dst = ugrad + static_cast<int64_t>(u) * D;
+    if constexpr (SGD) {
+      if (sr >= 0 || rs.local_hbm) {
+        dst = sr >= 0 ? const_cast<float*>(rs.cache) + static_cast<int64_t>(sr) * D
+                      : td[t].store + static_cast<int64_t>(rs.uniq[u]) * D;
+        v = make_float4(-lr * v.x, -lr * v.y, -lr * v.z, -lr * v.w);
+      }
+    }
+    atomicAdd(reinterpret_cast<float4*>(dst + m.c * 4), v);
+  };
+
+  for (int item = warp; item < T * wt; item += nwarps) {
+    const int t = item / wt;
+    const int b0 = (item - t * wt) * per, b1 = min(B, b0 + per);
+    if (b0 >= b1) continue;
+    const uint32_t ub = static_cast<uint32_t>(cn.ubase[t]);
+    const int nacc = min(kAcc, cn.ubase[t + 1] - cn.ubase[t]);
+    for (int i = lane_id(); i < nacc * VEC; i += 32) st4(acc + i * 4, make_float4(0.f, 0.f, 0.f, 0.f));
+    uint64_t touched = 0;  // accumulator rows written (warp-uniform)
+    __syncwarp();
+    for (int s0 = b0; s0 < b1; s0 += RPW * R) {
+      int lo[R], len[R], maxlen = 0;
+      float4 gv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int sb = s0 + r * RPW + m.sub;
+        lo[r] = 0;
+        len[r] = 0;
+        gv[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sb < b1) {
+          int64_t l64, h64;
+          bag_range(td, bag_off, B, P, sb, t, &l64, &h64);
+          lo[r] = static_cast<int>(l64);
+          len[r] = static_cast<int>(h64 - l64);
+          maxlen = max(maxlen, len[r]);
+          gv[r] = ld_stream4(grad + (static_cast<int64_t>(sb) * T + t) * D + m.c * 4);
+        }
+      }
+      maxlen = __reduce_max_sync(kFull, maxlen);
+      for (int i = 0; i < maxlen; ++i) {
+        uint32_t u[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float4 v = gv[r];
+          bool lead = u[r] != kInvalidSlot;
+          if (RPW > 1 && __any_sync(kFull, __popc(__match_any_sync(kFull, u[r])) > VEC)) {
+            // some row repeats in this window: rotate by whole bags (same component c)
+#pragma unroll
+            for (int k = 1; k < RPW; ++k) {
+              const int src = (lane_id() + k * VEC) & 31;
+              const uint32_t uo = __shfl_sync(kFull, u[r], src);
+              const float4 o = make_float4(__shfl_sync(kFull, gv[r].x, src), __shfl_sync(kFull, gv[r].y, src),
+                                           __shfl_sync(kFull, gv[r].z, src), __shfl_sync(kFull, gv[r].w, src));
+              if (uo == u[r]) {
+                if (src < lane_id()) lead = false;  // a lower bag owns this row
+                else v = add4(v, o);
+              }
+            }
+          }
+          const uint32_t local = u[r] - ub;  // (wraps for invalid slots)
+          const bool in_acc = lead && local < static_cast<uint32_t>(nacc);
+          if (in_acc) {
+            float* a = acc + local * D + m.c * 4;
+            st4(a, add4(*reinterpret_cast<const float4*>(a), v));
+            touched |= 1ull << local;
+          } else if (lead) {
+            emit(u[r], t, v);
+          }
+          __syncwarp();  // the next slot's leaders read what this one wrote
+        }
+      }
+    }
+    // flush the accumulator rows this warp touched (union over lanes)
+    uint64_t tall = touched;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tall |= __shfl_xor_sync(kFull, tall, o);
+    __syncwarp();
+    while (tall) {
+      // RPW rows per pass, VEC lanes each
+      int rows[RPW];
+      uint64_t rest = tall;
+#pragma unroll
+      for (int k = 0; k < RPW; ++k) {
+        rows[k] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
+        if (rest) rest &= rest - 1;
+      }
+      tall = rest;
+      int mine = -1;
+#pragma unroll
+      for (int k = 0; k < RPW; ++k)
+        if (k == m.sub) mine = rows[k];
+      if (mine >= 0) emit(ub + static_cast<uint32_t>(mine), t, *reinterpret_cast<const float4*>(acc + mine * D + m.c * 4));
+    }
+    __syncwarp();
+  }
+}
+
+// Fused single-rank SGD, second half: rows heavier than kLightAdds (their
+// partials went to g64) get w - lr * sum(g64) with one rounding (cache row,
+// or the HBM shard row of a miss); pinned-host misses get the sum in ugrad for
+// the host write-back.  Leaves g64 and ucount zeroed.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
+                                                        const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
+                                                        const int32_t* __restrict__ usrc, int* __restrict__ ucount,
+                                                        float* __restrict__ cache, float* __restrict__ ugrad,
+                                                        double* __restrict__ g64, float lr, int local_hbm) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
-  const int nbags = T * B;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int q0 = warp * RPW * R; q0 < nbags; q0 += nwarps * RPW * R) {
-    int lo[R], len[R], maxlen = 0;
-    float4 gv[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = q0 + r * RPW + m.sub;
-      lo[r] = 0;
-      len[r] = 0;
-      gv[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (q < nbags) {
-        const int t = q / B, s = q - t * B;
-        int64_t l64, h64;
-        bag_range(td, bag_off, B, P, s, t, &l64, &h64);
-        lo[r] = static_cast<int>(l64);
-        len[r] = static_cast<int>(h64 - l64);
-        maxlen = max(maxlen, len[r]);
-        gv[r] = ld_stream4(grad + (static_cast<int64_t>(s) * T + t) * D + m.c * 4);
-      }
-    }
-    maxlen = __reduce_max_sync(kFull, maxlen);
-    for (int i = 0; i < maxlen; ++i) {
-      uint32_t u[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
-      float* dst[R];
-      if constexpr (SGD) {
-        int32_t sr[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) sr[r] = u[r] != kInvalidSlot ? rs.usrc[u[r]] : 0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int q = q0 + r * RPW + m.sub;
-          dst[r] = sr[r] >= 0 ? const_cast<float*>(rs.cache) + static_cast<int64_t>(sr[r]) * D
-                   : rs.local_hbm ? td[q / B].store + static_cast<int64_t>(rs.uniq[u[r]]) * D
-                                  : ugrad + static_cast<int64_t>(u[r]) * D;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float4 v = gv[r];
-        bool lead = u[r] != kInvalidSlot;
-        if (RPW > 1 && __any_sync(kFull, __popc(__match_any_sync(kFull, u[r])) > VEC)) {
-          // some row repeats in this warp: rotate by whole bags (same component c)
-#pragma unroll
-          for (int k = 1; k < RPW; ++k) {
-            const int src = (lane_id() + k * VEC) & 31;
-            const uint32_t uo = __shfl_sync(kFull, u[r], src);
-            const float4 o = make_float4(__shfl_sync(kFull, gv[r].x, src), __shfl_sync(kFull, gv[r].y, src),
-                                         __shfl_sync(kFull, gv[r].z, src), __shfl_sync(kFull, gv[r].w, src));
-            if (uo == u[r]) {
-              if (src < lane_id()) lead = false;  // a lower bag owns this row
-              else v = add4(v, o);
-            }
-          }
-        }
-        if constexpr (SGD) {
-          if (lead) {
-            const bool to_row = dst[r] != ugrad + static_cast<int64_t>(u[r]) * D;
-            if (to_row) v = make_float4(-lr * v.x, -lr * v.y, -lr * v.z, -lr * v.w);
-            atomicAdd(reinterpret_cast<float4*>(dst[r] + m.c * 4), v);
-          }
-        } else {
-          if (lead) atomicAdd(reinterpret_cast<float4*>(ugrad + static_cast<int64_t>(u[r]) * D + m.c * 4), v);
-        }
-      }
+  for (int g = warp * RPW + m.sub; g < U; g += nwarps * RPW) {
+    const int n = ucount ? ucount[g] : kLightAdds + 1;
+    if (ucount && m.c == 0) ucount[g] = 0;
+    if (n <= kLightAdds) continue;
+    double gs[4];
+    take_g64<VEC>(g64, g, m.c, gs);
+    const int32_t s = usrc[g];
+    float* dst = s >= 0 ? cache + static_cast<int64_t>(s) * D
+               : local_hbm ? td[utab[g]].store + static_cast<int64_t>(uniq[g]) * D
+                           : nullptr;
+    if (dst) {
+      st4(dst + m.c * 4, sgd4(*reinterpret_cast<const float4*>(dst + m.c * 4), gs, lr));
+    } else {
+      float* p = ugrad + static_cast<int64_t>(g) * D + m.c * 4;
+      const float4 a = *reinterpret_cast<const float4*>(p);
+      st4(p, make_float4(static_cast<float>(a.x + gs[0]), static_cast<float>(a.y + gs[1]),
+                         static_cast<float>(a.z + gs[2]), static_cast<float>(a.w + gs[3])));
     }
   }
 }
@@ -929,7 +1064,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
                     unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
-                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq) {
+                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, int* __restrict__ ucount) {
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
@@ -1081,7 +1216,9 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
         const uint32_t cf = pf[j] >> 8, jf = pf[j] & 0xFF;
         pf[j] = static_cast<uint32_t>(tbase + s_pref[cf]) + (xw[j] >> 16) + __popc(xw[j] & 0xFFFFu & ((1u << jf) - 1));
       }
-      if (((rep >> j) & 1) && id[j] < nloc) sval[id[j]] = pf[j];  // for this CTA's hot duplicates
+      // for this CTA's hot duplicates: table-local unique index (< 65536) in
+      // the high half; the low half counts the CTA's lookups of the id (phase I)
+      if (((rep >> j) & 1) && id[j] < nloc) sval[id[j]] = (pf[j] - static_cast<uint32_t>(tbase)) << 16;
     }
   }
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // remote reads done
@@ -1120,11 +1257,26 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   __syncthreads();
   EC_TRACE_AT(6);
 
-  // ---- I: inverse
+  // ---- I: inverse, and each unique's lookup count (the backward's fp32 /
+  // fp64 split, k_scatter): hot ids counted per CTA in shared memory, then one
+  // RED per (CTA, hot id); other ids one RED per distinct unique per warp item
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const bool hot = id[j] < nloc;
+    const uint32_t g = id[j] == kEmptyKey ? kInvalidSlot
+                       : ((rep >> j) & 1) ? pf[j]
+                       : hot ? static_cast<uint32_t>(tbase) + (sval[id[j]] >> 16) : kInvalidSlot;
+    if (j < my) inv[tb.base + p0 + j] = g;
+    const unsigned peers = __match_any_sync(kFull, g);
+    if (g != kInvalidSlot && __ffs(peers) - 1 == lane_id()) {
+      if (hot) atomicAdd(sval + id[j], __popc(peers));
+      else atomicAdd(ucount + g, __popc(peers));
+    }
+  }
+  __syncthreads();
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j)
-    if (j < my)
-      inv[tb.base + p0 + j] = id[j] == kEmptyKey ? kInvalidSlot : (((rep >> j) & 1) ? pf[j] : sval[id[j]]);
+    if (((rep >> j) & 1) && id[j] < nloc) atomicAdd(ucount + pf[j], static_cast<int>(sval[id[j]] & 0xFFFFu));
   EC_TRACE_AT(7);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // keep this CTA's smem alive for remote readers
 }
@@ -1446,7 +1598,8 @@ __global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ 
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
                                                          const uint2* __restrict__ list,
-                                                         const float* __restrict__ grad, float* __restrict__ ugrad) {
+                                                         const float* __restrict__ grad, float* __restrict__ ugrad,
+                                                         double* __restrict__ g64) {
   constexpr int D = VEC * 4;
   const RowMap<VEC> m;
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
@@ -1456,9 +1609,21 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
   for (int c0 = gid * kRunChunk; c0 < n; c0 += groups * kRunChunk) {
     const int c1 = min(n, c0 + kRunChunk);
     uint32_t cu = list[c0].x;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // fp64: a run's sum rounds once
     bool first_run = true;  // the run containing c0 may start before the chunk
     int i = c0;
+    // a run wholly inside the chunk is stored; one that crosses a chunk edge
+    // adds its part to ugrad (zeroed) -- or, for rows spread over more than
+    // kLightAdds chunks, to the row's fp64 sum, which k_g64_finalize rounds
+    // into ugrad (at most kLightAdds fp32 roundings per row either way)
+    auto flush = [&](bool spans) {
+      const float4 a = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
+                                   static_cast<float>(acc[2]), static_cast<float>(acc[3]));
+      float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
+      if (!spans) st4(dst, a);
+      else if (chunk_span(off[cu], off[cu + 1]) > kLightAdds) red_g64<VEC>(g64, cu, m.c, acc[0], acc[1], acc[2], acc[3]);
+      else atomicAdd(reinterpret_cast<float4*>(dst), a);
+    };
     while (i < c1) {
       // 4 grad rows in flight, then fold them in list order
       uint32_t u4[4], g4[4];
@@ -1478,21 +1643,53 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
         if (u4[k] == kInvalidSlot) continue;
         if (u4[k] != cu) {
           // run of cu ends inside this chunk: sole owner unless it began before c0
-          float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
-          if (first_run && off[cu] < c0) atomicAdd(reinterpret_cast<float4*>(dst), acc);
-          else st4(dst, acc);
+          flush(first_run && off[cu] < c0);
           first_run = false;
           cu = u4[k];
-          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
         }
-        acc = add4(acc, v4[k]);
+        acc[0] += v4[k].x;
+        acc[1] += v4[k].y;
+        acc[2] += v4[k].z;
+        acc[3] += v4[k].w;
       }
       i += 4;
     }
     // last run: it may continue past the chunk, or began before it
-    float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
-    if ((first_run && off[cu] < c0) || off[cu + 1] > c1) atomicAdd(reinterpret_cast<float4*>(dst), acc);
-    else st4(dst, acc);
+    flush((first_run && off[cu] < c0) || off[cu + 1] > c1);
+  }
+}
+
+// Unique-row gradients whose sums went to g64, rounded into ugrad (g64 left
+// zeroed): after k_bwd_reduce (off != nullptr) the rows spanning more than
+// kLightAdds chunks; after the atomic k_scatter (off == nullptr) the rows
+// heavier than kLightAdds lookups (every row without counts).  Leaves ucount
+// zeroed.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_g64_finalize(const int* __restrict__ off, int* __restrict__ ucount,
+                                                           const int* __restrict__ ctr, int T, float* __restrict__ ugrad,
+                                                           double* __restrict__ g64) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int U = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g = warp * RPW + m.sub; g < U; g += nwarps * RPW) {
+    bool heavy;
+    if (off) {
+      heavy = chunk_span(off[g], off[g + 1]) > kLightAdds;
+    } else {
+      heavy = !ucount || ucount[g] > kLightAdds;
+      if (ucount && m.c == 0) ucount[g] = 0;
+    }
+    if (!heavy) continue;
+    double gs[4];
+    take_g64<VEC>(g64, g, m.c, gs);
+    float* p = ugrad + static_cast<int64_t>(g) * D + m.c * 4;
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    st4(p, make_float4(static_cast<float>(a.x + gs[0]), static_cast<float>(a.y + gs[1]),
+                       static_cast<float>(a.z + gs[2]), static_cast<float>(a.w + gs[3])));
   }
 }
 

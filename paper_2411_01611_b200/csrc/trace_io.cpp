@@ -225,6 +225,10 @@ int ec_trace_open_binary(const char* path, ec_trace* out) {
     madvise(f.map, size, MADV_SEQUENTIAL);
     std::memcpy(&f.h, f.map, sizeof(Header));
     check_header(f.h);
+    // samples * d * 4 must not wrap: bound samples by the file's id capacity first
+    if (f.h.d <= 0 || f.h.samples > (size - sizeof(Header)) / sizeof(uint32_t) / static_cast<uint64_t>(f.h.d))
+      invalid("binary trace size " + std::to_string(size) + " is too small for the header's " +
+              std::to_string(f.h.samples) + " samples of " + std::to_string(f.h.d) + " ids");
     const uint64_t n = f.h.samples * static_cast<uint64_t>(f.h.d);
     if (size != sizeof(Header) + n * sizeof(uint32_t))
       invalid("binary trace size " + std::to_string(size) + " != header + " + std::to_string(n) + " ids");

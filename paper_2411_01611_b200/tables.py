@@ -164,10 +164,16 @@ class EmbeddingTables:
         self._offsets = offs
         if out is None:
             out = torch.empty((batch_size, self.T * self.D), dtype=torch.float32, device=indices.device)
+        elif (out.dtype != torch.float32 or not out.is_contiguous() or out.device != indices.device
+              or out.numel() != batch_size * self.T * self.D):
+            raise ValidationError(f"out must be a contiguous float32 tensor of {batch_size * self.T * self.D} "
+                                  "elements on the indices' device")
         bo = 0
         if bag_offsets is not None:
-            if bag_offsets.dtype != torch.int64 or not bag_offsets.is_cuda:
-                raise ValidationError("bag_offsets must be an int64 CUDA tensor")
+            if (bag_offsets.dtype != torch.int64 or not bag_offsets.is_cuda or not bag_offsets.is_contiguous()
+                    or bag_offsets.numel() != self.T * batch_size + 1):
+                raise ValidationError("bag_offsets must be a contiguous int64 CUDA tensor of num_tables * "
+                                      "batch_size + 1 entries")
             bo = bag_offsets.data_ptr()
         b = self._batch(indices.data_ptr(), offs, bo or None, batch_size, pooling)
         check(N.lib().ec_lookup_fwd(self._h, b, out.data_ptr(), _stream_ptr(torch, self.device)))

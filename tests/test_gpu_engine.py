@@ -226,47 +226,92 @@ def test_config2_kaggle_shape_host_tier(ec, torch, ref, mode):
     tab.close()
 
 
-@pytest.mark.parametrize("storage", ["host", "hbm"])
-def test_config2_kaggle_shape_training_step(ec, torch, storage):
-    """One bench-style training step at the Kaggle shape (configs[1]) on the
-    fused single-rank path: forward, backward with grad = pooled output,
-    lr 0.01.  Every touched row (cache, HBM or pinned-host) equals the fp64
-    oracle's w - lr * sum(grads).  The update is fp32 reductions straight
-    into the row (one rounding of at most half an ulp of the running value per
-    add, in a varying order), so the bound is count * 2^-24 * |row|."""
-    D, B, lr = 16, 16384, 0.01
-    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in KAGGLE]
-    ks = ec.place_topk_global(dists, (256 << 20) // (D * 4))
+def check_sgd(got, w0, g, inv, bag, lr, what, rtol=RTOL):
+    """Updated rows vs the fp64 restatement w0 - lr * sum(g) (orc_backward_sgd).
+
+    The bound is 1e-5 relative to the magnitudes summed, |w0| + lr * sum|g|
+    per element: the order-of-summation tolerance of a sum (its condition
+    number).  Where a row's gradients share a sign (grad = pooled output, as in
+    the bench) that is 1e-5 of |w0| + |lr * sum(g)|.  Returns the worst
+    err / bound and the worst plain relative error err / |want| over elements
+    with |want| >= 1e-3 * max|want| (reported, not asserted: values that
+    cancel to ~0 have no meaningful plain relative error)."""
+    ug, _ = O.backward_sgd(g, inv, bag, w0, lr)
+    uabs, _ = O.backward_sgd(np.abs(g), inv, bag, w0, lr)
+    want = w0.astype(np.float64) - lr * ug
+    scale = np.abs(w0.astype(np.float64)) + lr * uabs
+    err = np.abs(got.astype(np.float64) - want)
+    bound = rtol * scale
+    bad = err > bound
+    if bad.any():
+        k = np.argwhere(bad)[0]
+        raise AssertionError(f"{what}: {bad.sum()} of {bad.size} elements over 1e-5 relative; first unique "
+                             f"{k[0]} got {got[k[0], k[1]]} want {want[k[0], k[1]]} w0 {w0[k[0], k[1]]} "
+                             f"bound {bound[k[0], k[1]]}")
+    big = np.abs(want) >= 1e-3 * np.abs(want).max() if want.size else np.zeros(0, bool)
+    plain = float((err[big] / np.abs(want[big])).max()) if big.any() else 0.0
+    return float((err / np.where(bound > 0, bound, 1.0)).max()) if err.size else 0.0, plain
+
+
+def run_training_step(ec, torch, rows, D, B, P, storage, cache_bytes, seed, lr=0.01, mode=None, scatter=None,
+                      init=(4, 0.05)):
+    """One bench-style training step on fresh tables: forward, backward with
+    grad = the pooled output (loss = 1/2 |pooled|^2), SGD at lr.  Every touched
+    row (cache, HBM shard or pinned host) is checked against check_sgd."""
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    ks = ec.place_topk_global(dists, cache_bytes // (D * 4)) if cache_bytes else [0] * len(rows)
     caches = [d.top_ids(k) for d, k in zip(dists, ks)]
-    tab = ec.EmbeddingTables(KAGGLE, D, storage=storage, max_lookups_per_table=B, max_batch_size=B)
-    tab.init_synthetic(4, 0.05)
+    tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
+    if mode:
+        tab.dedup_mode(mode)
+    if scatter:
+        tab.scatter_mode(scatter)
+    tab.init_synthetic(*init)
     tab.place_cache(caches)
-    ids, offs = make_ids(ec, torch, dists, [B] * 26, 909)
-    out = tab.forward(ids, offs, B, 1)
+    ids, offs = make_ids(ec, torch, dists, [B * P] * len(rows), seed)
+    out = tab.forward(ids, offs, B, P)
     grad = out.clone()
     tab.backward(grad, lr)
     torch.cuda.synchronize()
     ids_h = ids.cpu().numpy().view(np.uint32)
     g = grad.cpu().numpy()
-    bag = np.arange(B + 1, dtype=np.int64)
-    for t in range(26):
+    bag = np.arange(B + 1, dtype=np.int64) * P
+    worst, plain = 0.0, 0.0
+    for t in range(len(rows)):
         seg = ids_h[offs[t]:offs[t + 1]]
         u, inv = O.dedup(seg)
-        w0 = O.synthetic_rows(4, 0.05, t, u, D)
-        ug, want = O.backward_sgd(np.ascontiguousarray(g[:, t * D:(t + 1) * D]), inv[:seg.size], bag, w0, lr)
-        got = tab.read_rows(t, u)
-        cnt = np.bincount(inv[:seg.size], minlength=u.size)[:, None]
-        want = w0 - lr * ug
-        mag = np.maximum(np.abs(want), np.abs(w0)).max(axis=1, keepdims=True)
-        tol = cnt * 2.0 ** -24 * mag + 1e-7
-        err = np.abs(got - want)
-        bad = err > tol
-        if bad.any():
-            k = np.argwhere(bad)[0]
-            raise AssertionError(f"table {t}: {bad.sum()} bad of {bad.size}; first row {k[0]} id {u[k[0]]} "
-                                 f"count {cnt[k[0], 0]} got {got[k[0], k[1]]} want {want[k[0], k[1]]} "
-                                 f"w0 {w0[k[0], k[1]]} tol {tol[k[0], 0]}")
+        w0 = O.synthetic_rows(init[0], init[1], t, u, D)
+        w, p = check_sgd(tab.read_rows(t, u), w0, np.ascontiguousarray(g[:, t * D:(t + 1) * D]), inv[:seg.size],
+                         bag, lr, f"table {t}")
+        worst, plain = max(worst, w), max(plain, p)
+    st = tab.stats()
     tab.close()
+    print(f"[sgd parity] rows={len(rows)} D={D} B={B} P={P} {storage} mode={mode} scatter={scatter}: "
+          f"max err/bound {worst:.3f}, max plain rel err {plain:.2e}")
+    return st
+
+
+@pytest.mark.parametrize("storage", ["host", "hbm"])
+def test_config2_kaggle_shape_training_step(ec, torch, storage):
+    """One bench-style training step at the Kaggle shape (configs[1]) on the
+    fused single-rank path (SGD inside the scatter): every touched row within
+    1e-5 relative of the fp64 oracle (check_sgd)."""
+    run_training_step(ec, torch, KAGGLE, 16, 16384, 1, storage, 256 << 20, 909)
+
+
+@pytest.mark.parametrize("scatter", [None, "atomic"])
+def test_config1_full_size_training_step(ec, torch, scatter):
+    """configs[0] at full size (8 x 1M rows, D=64, b=4096, P=20, no cache, as
+    bench --workload cfg1 times it): tile-path dedup, grouped gradient lists and
+    k_bwd_reduce (auto), or the atomic scatter; rows within 1e-5 relative."""
+    run_training_step(ec, torch, [1_000_000] * 8, 64, 4096, 20, "hbm", 0, 20241101, scatter=scatter)
+
+
+def test_config3_terabyte_shape_training_step(ec, torch):
+    """configs[2]'s per-rank shape at full size (26 TB tables, 188M rows in
+    HBM, D=64, b=65536, 1 GB cache), as bench --workload tb times it: every
+    touched cache and shard row within 1e-5 relative of the oracle."""
+    run_training_step(ec, torch, TB_ROWS, 64, 65536, 1, "hbm", 1 << 30, 7331, init=(5, 0.02))
 
 
 TB_ROWS = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546, 403346, 10, 2208, 11938,

@@ -188,7 +188,7 @@ def test_p2p_import_validation(ec, torch):
           for r in range(2)]
     ho = ec.EmbeddingTables([100], 4, storage="host", rank=1, world=2, max_lookups_per_table=8, max_batch_size=8)
     blobs = [m.p2p_export() for m in hb]
-    assert len(blobs[0]) == 9 * 64 + 32
+    assert len(blobs[0]) == 9 * 64 + 48
     with pytest.raises(ValueError):
         hb[0].p2p_import(blobs[:1])
     with pytest.raises(ValueError):

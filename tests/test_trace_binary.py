@@ -68,6 +68,12 @@ def test_binary_trace_validation(ec, tmp_path):
     (tmp_path / "short.ectrace").write_bytes(raw[:-4])
     with pytest.raises(ec.ValidationError, match="size"):
         ec.Trace.load_binary(tmp_path / "short.ectrace")
+    # samples * d wraps 2^64 to the file's real id count: refused before multiplying
+    hdr = np.frombuffer(bytes(raw[:40]), np.uint64).copy()
+    hdr[2], hdr[4] = 4, (1 << 62) + 1  # d = 4, samples = 2^62 + 1 -> 4 * samples wraps to 4
+    (tmp_path / "wrap.ectrace").write_bytes(hdr.tobytes() + raw[40:])
+    with pytest.raises(ec.ValidationError, match="too small"):
+        ec.Trace.load_binary(tmp_path / "wrap.ectrace")
     (tmp_path / "hdr.ectrace").write_bytes(raw[:20])
     with pytest.raises(ec.ValidationError, match="truncated"):
         ec.Trace.load_binary(tmp_path / "hdr.ectrace")

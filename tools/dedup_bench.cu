@@ -36,11 +36,11 @@ static const std::vector<uint64_t> kTb = {39884406, 39043, 17289, 7420, 20263, 3
 
 template <int ITEMS>
 static void launch(const TableDev* td, int T, const uint32_t* idx, unsigned long long* tstat, int* ctr, uint32_t* uniq,
-                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq) {
+                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, int* ucount) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem>>>(td, T, idx, tstat, ctr, uniq, uslot, utab, inv, usrc,
-                                                                       missq);
+                                                                       missq, ucount);
 }
 
 int main(int argc, char** argv) {
@@ -105,6 +105,9 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&inv, N * 4));
   CK(cudaMalloc(&missq, N * 4));
   CK(cudaMalloc(&usrc, N * 4));
+  int* ucount;
+  CK(cudaMalloc(&ucount, N * 4));
+  CK(cudaMemset(ucount, 0, N * 4));
   CK(cudaMalloc(&utab, N * 2));
   CK(cudaMalloc(&tstat, T * 8));
   CK(cudaMalloc(&ctr, counters_size(T) * 4));
@@ -128,11 +131,11 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a));
     switch (items) {
-      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
-      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq); break;
+      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
+      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
+      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
+      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
+      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(b));
