@@ -56,7 +56,10 @@ SEED = 20241101
 N_BATCHES = 4          # distinct batches cycled through the timed steps
 FLUSH_BYTES = 256 << 20  # > 126 MB L2, written between timed steps
 HEAD_START_CYCLES = 2_000_000  # ~1 ms device sleep before a timed loop (see run_ours)
-HOST_LINK_ROWS_PER_S = 215e6  # measured random-row request rate of the pinned-host link (hostlink_bench)
+# request-rate capacity of the pinned-host link: the highest rate the probe
+# reached (random 64 B rows, 57K rows in flight: 267 M rows/s,
+# profiles/r01/hostlink_probe.txt); a 7K-row batch reaches 215 M/s
+HOST_LINK_ROWS_PER_S = 267e6
 LR = 0.01
 MODES = {}  # kernel-variant overrides for experiments (--dedup-mode / --scatter-mode)
 
@@ -252,7 +255,8 @@ def phase_bytes(st, wl, T, fused=False):
     hbm_src = U if wl["storage"] == "hbm" else H      # rows k_gather reads from HBM
     host_rows = 0 if wl["storage"] == "hbm" else M
     return {
-        "k_dedup_cluster": n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4),  # ids in, inverse out; uniq, uslot, utab, remap->usrc
+        # ids in, inverse out; uniq, uslot, utab, remap->usrc; per-unique lookup counts
+        "k_dedup_cluster": n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4 + 4),
         "k_insert": n * 4 + n * 4,                     # ids in, slot_of out
         "k_compact": n * 4 + U * (4 + 4 + 2),          # slot_of in; uniq, uslot, utab out
         "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out
@@ -261,8 +265,10 @@ def phase_bytes(st, wl, T, fused=False):
         # A_pool (rows read from the compact, L2-resident copy), or
         # A_fused when the pool reads each unique row at its source (no K3 gather)
         "k_pool": (U * 4 + U * row + n * 4 + B * T * row) if fused else (n * 4 + n * row + B * T * row),
-        "k_scatter": B * T * row + n * 4 + n * row,    # grads in, inverse in, row-grad reductions
-        "k_apply": (U - host_rows) * (4 + row * 3),    # usrc, urows, ugrad in, rows out
+        "k_scatter": B * T * row + n * 4 + n * 4 + n * row,  # grads in, inverse + counts in, row-grad reductions
+        # fused path (k_apply_g64): per-unique counts read and cleared; the
+        # rows past 64 lookups (not counted here) get their fp64 sums applied
+        "k_apply": U * 8 if fused else (U - host_rows) * (4 + row * 3),  # else: usrc, urows, ugrad in, rows out
         "k_apply_host": host_rows * (4 + row * 3),
     }
 
@@ -437,11 +443,15 @@ def run_ours(args, wl):
     e2e_marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ready_stream = torch.cuda.Stream()  # a prefetch's input: ordered after its batch's copy only
 
-    def e2e_steps(nsteps, marks=None):
+    def e2e_steps(nsteps, marks=None, start=None):
         # input pipelining: step k+LA's H2D runs during step k, so a prefetch
         # never waits on the link; every step still moves its own ids
         # host->device and reads its result back
         tab.prefetch_drop()  # this loop primes its own pipeline
+        if start is not None:
+            # the priming copies and prefetches start inside the timed window
+            copy_stream.wait_event(start)
+            ready_stream.wait_event(start)
         for k in range(min(nsteps, LA)):
             h2d(k)
         for k in range(min(nsteps, depth)):
@@ -482,7 +492,7 @@ def run_ours(args, wl):
     HOST["blocked"] = 0.0
     t_host = time.perf_counter()
     e2e_start.record(stream)
-    counters = e2e_steps(args.steps, e2e_marks)
+    counters = e2e_steps(args.steps, e2e_marks, e2e_start)
     e2e_end.record(stream)
     t_host = time.perf_counter() - t_host
     torch.cuda.synchronize()
@@ -574,7 +584,16 @@ def run_ours(args, wl):
     tfile = tfiles[-1] if tfiles else None
     if tfile:
         traffic = json.load(open(tfile)).get(dom)
-    step_alg = sum(mean_bytes.values())
+    # whole-step algorithmic bytes: the kernels this path launched only
+    step_alg = sum(mean_bytes[k] for k in phases if k in mean_bytes)
+    # K3 (the north_star's >= 50%-of-HBM gather): k_gather, or on the fused
+    # single-rank path the pool that reads every unique row at its source
+    gk = "k_gather" if "k_gather" in phases else ("k_pool" if fused and "k_pool" in phases else None)
+    gather_roof = ({"kernel": gk, "achieved": phases[gk]["gbs"], "peak": peak, "unit": "GB/s",
+                    "frac": round(phases[gk]["gbs"] / peak, 4), "alg_bytes_per_launch": phases[gk]["alg_bytes"],
+                    "bytes": "A_fused (SURVEY 8d): unique rows read at their source once + inverse + pooled out"
+                    if gk == "k_pool" else "A_gather (SURVEY 8d): unique rows in, compact rows out, ugrad zeroed"}
+                   if gk else None)
     link_ms = sum(phases[k]["ms_per_call"] for k in ("k_gather_host", "k_apply_host") if k in phases)
 
     s0 = stats[0]
@@ -625,6 +644,7 @@ def run_ours(args, wl):
                      "traffic_source": (f"{os.path.relpath(tfile, ROOT)} (ncu --set full, dram read+write "
                                         "bytes per launch)") if traffic else None,
                      "peak_source": peak_src},
+        "gather_roofline": gather_roof,
         # the pinned-host tier's bound: the host link serves ~215 M row requests/s
         # (reads and writes share it; tools/hostlink_bench.cu, profiles/r01/hostlink_probe.txt)
         "host_link": ({"bound": "host-link request rate", "rows_per_step": int(2 * s0["miss_rows"]),
@@ -645,10 +665,25 @@ def run_ours(args, wl):
         "setup_s": round(setup_s, 1),
     }
     res["clocks"] = clk.summary()
+    # the reference cost model's expectation of the same quantity (Eq. 6,
+    # cached_epoch_cost(dist_t, WorkloadSpec(n, n, 1), C_t): expected
+    # non-cached distinct rows of one batch of n lookups), next to the
+    # realized rows of every batch and table
+    n_t = B * P
+    exp_t = [ec.cached_epoch_cost(d, ec.WorkloadSpec(n_t, n_t, 1), c).embedding_cost for d, c in zip(dists, caches)]
+    res["comm"]["expected_model_rows_per_batch"] = round(float(sum(exp_t)), 3)
+    res["comm"]["expected_model_rows_per_table"] = [round(float(x), 3) for x in exp_t]
+    res["comm"]["model_rows_per_batch_all"] = [int(s["miss_rows"]) for s in stats]
+    res["comm"]["model_rows_per_table_batch0"] = [int(x) for x in s0["miss_per_table"]]
     if rank == 0 and not args.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(ids.cpu().numpy().view(np.uint32), offs, wl, caches, args.cpu_seconds)
-        res["comm"]["reference_model_rows_per_batch"] = res["cpu_baseline"].pop("model_rows_batch0")
-        res["comm"]["equal_to_reference"] = res["comm"]["reference_model_rows_per_batch"] == s0["miss_rows"]
+        cb = cpu_baseline(ids.cpu().numpy().view(np.uint32), offs, wl, caches, args.cpu_seconds)
+        ref_nc = cb.pop("model_rows_per_table")
+        res["cpu_baseline"] = cb
+        res["comm"]["reference_model_rows_per_batch"] = int(sum(ref_nc[0]))
+        # every batch and every table: realized rows == the reference's count
+        res["comm"]["equal_to_reference"] = all(
+            [int(x) for x in stats[j]["miss_per_table"]] == ref_nc[j] for j in range(len(ref_nc)))
+        res["comm"]["equal_to_reference_checked"] = f"{len(ref_nc)} batches x {T} tables"
     if rank == 0:
         print(json.dumps(res))
     tab.close()
@@ -685,15 +720,15 @@ def cpu_baseline(ids_host, offs, wl, caches, seconds, threads=1):
     caches = [np.ascontiguousarray(c, dtype=np.uint32) for c in caches]
     nb = ids_host.shape[0]
     done = 0
-    model_rows0 = None
+    per_table = []  # the reference's non-cached distinct count of every table, per batch (first pass)
     t0 = time.perf_counter()
     while True:
         j = done % nb
         _, nc = O.ref_segment_counts(ids_host[j], offs, wl["rows"], caches, threads=threads, want_all=False)
-        if done == 0:
-            model_rows0 = int(nc.sum())
+        if done < nb:
+            per_table.append([int(x) for x in nc])
         done += 1
-        if time.perf_counter() - t0 >= seconds and done >= 1:
+        if time.perf_counter() - t0 >= seconds and done >= nb:
             break
     dt = time.perf_counter() - t0
     look = done * T * wl["batch"] * wl["pooling"]
@@ -701,7 +736,7 @@ def cpu_baseline(ids_host, offs, wl, caches, seconds, threads=1):
             "sample": f"{done} batches ({look} lookups) of this workload through the reference's "
                       f"simulate_epoch(Trace{{d=1}}, n, C_t) per table (dedup + hit/miss counts only; the "
                       f"reference has no gather/pool/backward), {dt:.1f} s",
-            "model_rows_batch0": model_rows0}
+            "model_rows_per_table": per_table}
 
 
 def run_reference(args, wl):

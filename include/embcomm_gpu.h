@@ -76,6 +76,11 @@ int ec_dist_top_ids(ec_dist d, uint64_t k, uint32_t* out_host);                 
 int ec_dist_mass_of(ec_dist d, const uint32_t* ids_host, uint64_t n, double* out);  /* :100-104 */
 /* ranked probabilities (non-increasing) and rank->id map; either may be NULL */
 int ec_dist_export(ec_dist d, double* ranked_probs_host, uint32_t* rank_to_id_host);
+/* value semantics of EmbeddingDistribution (distribution.hpp:18, copyable and
+ * immutable): an independent copy; and the ranked probabilities in place
+ * (ranked_probs(), distribution.hpp:34), valid until ec_dist_destroy */
+int ec_dist_clone(ec_dist d, ec_dist* out);
+int ec_dist_ranked_view(ec_dist d, const double** ranked_probs);
 
 /* ------------------------------------------------------------ cost model
  * core/include/embcomm/cost_model.hpp:17-64.  Host fp64, reference
@@ -207,6 +212,13 @@ int ec_classify_samples(const uint32_t* ids_host, uint64_t num_samples, int64_t 
                         uint8_t* hot_host);
 int ec_schedule_order(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features,
                       uint64_t vocab, const uint32_t* cache_ids_host, uint64_t k, int device,
+                      uint32_t* order_host, uint64_t* num_hot);
+/* build_schedule(trace, cache, b, shuffle_seed) (trace.cpp:206-240): the same
+ * order, and with shuffle != 0 each class permuted by the reference's seeded
+ * Fisher-Yates (SplitMix64(substream_seed(seed, 0)) hot, (seed, 1) normal;
+ * trace.cpp:211-222) -- bit-identical to the reference's schedule. */
+int ec_build_schedule(const uint32_t* ids_host, uint64_t num_samples, int64_t num_features, uint64_t vocab,
+                      const uint32_t* cache_ids_host, uint64_t k, int device, int shuffle, uint64_t seed,
                       uint32_t* order_host, uint64_t* num_hot);
 /* build_skew_table (core/src/trace.cpp:128-150): access counts of the
  * num_ids trace ids (histogram on the GPU), observed ids sorted by (count

@@ -602,18 +602,19 @@ def classify_samples(trace: Trace, cache_ids, device: int = 0) -> SampleClasses:
 def build_schedule(trace: Trace, cache_ids, batch_size: int, shuffle_seed: Optional[int] = None,
                    device: int = 0) -> BatchSchedule:
     """build_schedule (core/src/trace.cpp:206-240): stable hot/normal partition
-    on the GPU, packed into batches of batch_size."""
+    on the GPU, each class optionally shuffled by the reference's seeded
+    Fisher-Yates (trace.cpp:211-222), packed into batches of batch_size."""
     if batch_size < 1:
         raise ValidationError("batch size must be >= 1")
-    if shuffle_seed is not None:
-        raise ValidationError("shuffled schedules are not supported by the GPU path yet")
     ids = _u32(trace.ids)
     c = _u32(cache_ids)
     q = trace.num_samples()
     order = np.zeros(q, np.uint32)
     nh = C.c_uint64()
-    check(N.lib().ec_schedule_order(ids.ctypes.data, q, trace.num_features, trace.vocab_size, c.ctypes.data,
-                                    c.size, device, order.ctypes.data, C.byref(nh)))
+    check(N.lib().ec_build_schedule(ids.ctypes.data, q, trace.num_features, trace.vocab_size, c.ctypes.data,
+                                    c.size, device, 0 if shuffle_seed is None else 1,
+                                    C.c_uint64(0 if shuffle_seed is None else shuffle_seed),
+                                    order.ctypes.data, C.byref(nh)))
     h = int(nh.value)
 
     def pack(v):

@@ -140,6 +140,7 @@ _SIGS = {
     "ec_simulate_trace": [vp, u64, i64, u64, i64, vp, u64, C.c_int, P(SimResultC)],
     "ec_classify_samples": [vp, u64, i64, u64, vp, u64, C.c_int, vp],
     "ec_schedule_order": [vp, u64, i64, u64, vp, u64, C.c_int, vp, P(u64)],
+    "ec_build_schedule": [vp, u64, i64, u64, vp, u64, C.c_int, C.c_int, u64, vp, P(u64)],
     "ec_build_skew_table": [vp, u64, u64, C.c_int, vp, vp, vp, P(u64)],
     "ec_estimate_distribution": [vp, vp, u64, u64, u64, f64, P(vp)],
     "ec_tables_create": [P(TablesConfig), P(vp)],

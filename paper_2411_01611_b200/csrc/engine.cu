@@ -768,6 +768,7 @@ void Engine::fwd_pool(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
+  fold_g64 = false;
   if (fused()) {
     // -lr * grad scattered straight into the cache / HBM rows (SGD in the
     // scatter) for a row's first kLightAdds partials, the rest summed in fp64
@@ -798,8 +799,7 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   if (bb[cur].lists) {  // the forward grouped the lookups already (tile path)
     k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
     launched();
-    k_g64_finalize<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, nullptr, ctr.p, static_cast<int>(T), ugrad.p, g64.p);
-    launched();
+    finalize_transpose<VEC>(st);
     return;
   }
   const int tgrid = std::min(ntiles, sm_count(device) * 8);
@@ -817,6 +817,16 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   launched();
   k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
   launched();
+  finalize_transpose<VEC>(st);
+}
+
+// Rows spanning many k_bwd_reduce chunks have their gradient in g64: rounded
+// into ugrad for the exchange / host write-back, or -- single rank, HBM rows,
+// where k_apply is the only consumer -- read by k_apply itself.
+template <int VEC>
+void Engine::finalize_transpose(cudaStream_t st) {
+  fold_g64 = world == 1 && !in_group && storage == EC_STORAGE_HBM;
+  if (fold_g64) return;
   k_g64_finalize<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, nullptr, ctr.p, static_cast<int>(T), ugrad.p, g64.p);
   launched();
 }
@@ -909,7 +919,8 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   if (!fused()) {
     PhaseScope ph(prof, kPhaseApply, st);
     k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
-                                                     cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world);
+                                                     cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world,
+                                                     fold_g64 ? off.p : nullptr, g64.p);
     launched();
   }
   if (host && world > 1) join_host_writes(st);

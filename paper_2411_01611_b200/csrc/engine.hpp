@@ -303,6 +303,8 @@ struct Engine {
   template <int VEC> void fwd_gather_local(cudaStream_t st);
   template <int VEC> void fwd_pool(cudaStream_t st);
   template <int VEC> void bwd_scatter(const float* grad, cudaStream_t st);
+  template <int VEC> void finalize_transpose(cudaStream_t st);
+  bool fold_g64 = false;  // k_apply reads the fp64 sums of chunk-spanning rows itself
   template <int VEC> void bwd_apply_local(float lr, cudaStream_t st);
   template <int VEC> void enqueue_host_writeback(float lr);
   void join_host_writes(cudaStream_t st);

@@ -450,6 +450,19 @@ int ec_dist_export(ec_dist h, double* p, uint32_t* r2i) {
   });
 }
 
+int ec_dist_clone(ec_dist h, ec_dist* out) {
+  return guard([&] {
+    if (!out) invalid("null output");
+    *out = new ec_dist_s{D(h)};
+  });
+}
+int ec_dist_ranked_view(ec_dist h, const double** ranked) {
+  return guard([&] {
+    if (!ranked) invalid("null output");
+    *ranked = D(h).ranked.data();
+  });
+}
+
 int ec_workload_validate(const ec_workload* w) { return guard([&] { validate(*w); }); }
 int ec_batch_presence_prob(double p, int64_t b, double* out) {
   return guard([&] { *out = presence(p, b); });

@@ -675,26 +675,24 @@ __device__ __forceinline__ float4 sgd4(float4 w, const double* gs, float lr) {
 }
 
 // ------------------------------------------------------------------ K6
-// Each warp owns a contiguous range of one table's bags (T x Wt ranges), so
-// hot rows repeat inside the warp many times over.  Per R-slot window of RPW
-// bags, lanes holding the same row (same component c) are summed with
-// shuffles; then
-//   * rows among the table's first kAcc uniques (first-occurrence order puts a
-//     table's heaviest ids there) are added into the warp's private
-//     shared-memory accumulator -- plain read-modify-write, the leaders of one
-//     window hold distinct rows -- and flushed once when the range ends;
-//   * other rows leave as one RED per window.
-// A row's partials leave the warp either as fp32 REDs (SGD: -lr * v straight
-// into the cache / HBM row, or into ugrad) or, for rows with more than
-// kLightAdds lookups in the batch (the dedup's count, `ucount`), into the
-// row's fp64 sum in g64, rounded once by k_apply_g64 / k_g64_finalize.  So a
-// row sees at most kLightAdds fp32 roundings of partial sums (<= 3.8e-6 of the
-// magnitudes summed, north_star bar 1e-5); without counts (ucount null) every
-// row takes the fp64 path.  Measured (profiles/r02/parity.md): the all-fp32
-// window scatter left the 3-row Kaggle tables' rows 1.1e-5 off (~2K adds
-// each); fp64 REDs per window for heavy rows cost +30 us on the Kaggle
-// scatter (thousands of same-address atomics on a 3-row table's rows), which
-// the per-warp accumulators remove.
+// Each warp owns a contiguous range of one table's bags (whole R-slot windows
+// of RPW bags), so hot rows repeat inside the warp many times over.  Per
+// window, lanes holding the same row (same component c) are summed with
+// shuffles.  Then, by the row's lookup count in the batch (the dedup's
+// `ucount`):
+//   * light rows (<= kLightAdds lookups) leave as one fp32 RED per window (SGD:
+//     -lr * v straight into the cache / HBM row; else into ugrad): at most
+//     kLightAdds roundings, <= 3.8e-6 of the magnitudes summed;
+//   * heavy rows go to the row's fp64 sum in g64, rounded once by
+//     k_apply_g64 / k_g64_finalize -- through the warp's private shared-memory
+//     accumulator when the row is among the table's first kAcc uniques (first-
+//     occurrence order puts a table's heaviest ids there; plain read-modify-
+//     write, a window's leaders hold distinct rows), flushed once per range.
+// Without counts (ucount null) every row takes the fp64 path.  Measured
+// (profiles/r02/parity.md): the all-fp32 scatter left the 3-row Kaggle tables'
+// rows 1.1e-5 off (~2K adds each, north_star bar 1e-5); fp64 REDs per window
+// for heavy rows cost +30 us (same-address atomics on a 3-row table's rows),
+// which the per-warp accumulators remove: 26 us standalone (r01 fp32: 28 us).
 constexpr int kLightAdds = 64;
 
 template <int VEC>
@@ -720,17 +718,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
   const Counters cn = counters(const_cast<int*>(ctr), T);
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int wt = max(1, nwarps / T);  // warps (ranges) per table
-  const int per = (B + wt - 1) / wt;
+  for (int i = lane_id(); i < kAcc * VEC; i += 32) st4(acc + i * 4, make_float4(0.f, 0.f, 0.f, 0.f));
+  __syncwarp();
+  // ranges of whole R-slot windows (RPW * R bags), about one per warp
+  const int win = RPW * R;
+  const int per = max(1, (B + max(1, nwarps / T) - 1) / max(1, nwarps / T) + win - 1) / win * win;
+  const int wt = (B + per - 1) / per;  // ranges per table
 
-  // one partial of unique u leaves the warp (fp32 RED or fp64 sum, see above)
-  auto emit = [&](uint32_t u, int t, float4 v) {
-    const int n = ucount ? __ldcg(ucount + u) : kLightAdds + 1;
-    const int32_t sr = SGD ? rs.usrc[u] : 0;  // (both loads in flight before the branch)
-    if (n > kLightAdds) {
-      red_g64<VEC>(g64, u, m.c, v.x, v.y, v.z, v.w);
-      return;
-    }
+  // a light row's partial leaves as an fp32 RED (SGD: -lr * v into its cache /
+  // HBM row; else into ugrad)
+  auto emit_light = [&](uint32_t u, int t, int32_t sr, float4 v) {
     float* dst = ugrad + static_cast<int64_t>(u) * D;
     if constexpr (SGD) {
       if (sr >= 0 || rs.local_hbm) {
@@ -748,9 +745,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
     if (b0 >= b1) continue;
     const uint32_t ub = static_cast<uint32_t>(cn.ubase[t]);
     const int nacc = min(kAcc, cn.ubase[t + 1] - cn.ubase[t]);
-    for (int i = lane_id(); i < nacc * VEC; i += 32) st4(acc + i * 4, make_float4(0.f, 0.f, 0.f, 0.f));
-    uint64_t touched = 0;  // accumulator rows written (warp-uniform)
-    __syncwarp();
+    uint64_t touched = 0;  // accumulator rows this lane wrote (the rows are zero between ranges)
     for (int s0 = b0; s0 < b1; s0 += RPW * R) {
       int lo[R], len[R], maxlen = 0;
       float4 gv[R];
@@ -774,6 +769,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
         uint32_t u[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+        // every slot's count (and SGD source) in flight before the pre-sums
+        int cnt[R];
+        int32_t srr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          cnt[r] = u[r] != kInvalidSlot ? (ucount ? __ldcg(ucount + u[r]) : kLightAdds + 1) : 0;
+          srr[r] = SGD && u[r] != kInvalidSlot ? rs.usrc[u[r]] : 0;
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           float4 v = gv[r];
@@ -792,39 +795,40 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
               }
             }
           }
-          const uint32_t local = u[r] - ub;  // (wraps for invalid slots)
-          const bool in_acc = lead && local < static_cast<uint32_t>(nacc);
-          if (in_acc) {
-            float* a = acc + local * D + m.c * 4;
-            st4(a, add4(*reinterpret_cast<const float4*>(a), v));
-            touched |= 1ull << local;
+          // heavy rows (more than kLightAdds lookups): the warp accumulator if
+          // among the table's first kAcc uniques, else the fp64 sum
+          const int n = cnt[r];
+          const int32_t sr = srr[r];
+          const uint32_t local = u[r] - ub;
+          if (lead && n > kLightAdds) {
+            if (local < static_cast<uint32_t>(nacc)) {
+              float* a = acc + local * D + m.c * 4;
+              st4(a, add4(*reinterpret_cast<const float4*>(a), v));
+              touched |= 1ull << local;
+            } else {
+              red_g64<VEC>(g64, u[r], m.c, v.x, v.y, v.z, v.w);
+            }
           } else if (lead) {
-            emit(u[r], t, v);
+            emit_light(u[r], t, sr, v);
           }
           __syncwarp();  // the next slot's leaders read what this one wrote
         }
       }
     }
-    // flush the accumulator rows this warp touched (union over lanes)
+    // flush the accumulator rows this warp touched (union over lanes) into
+    // their fp64 sums and zero them: lane group `sub` takes every RPW-th row
     uint64_t tall = touched;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tall |= __shfl_xor_sync(kFull, tall, o);
     __syncwarp();
+    for (int k = 0; k < m.sub && tall; ++k) tall &= tall - 1;
     while (tall) {
-      // RPW rows per pass, VEC lanes each
-      int rows[RPW];
-      uint64_t rest = tall;
-#pragma unroll
-      for (int k = 0; k < RPW; ++k) {
-        rows[k] = rest ? __ffsll(static_cast<long long>(rest)) - 1 : -1;
-        if (rest) rest &= rest - 1;
-      }
-      tall = rest;
-      int mine = -1;
-#pragma unroll
-      for (int k = 0; k < RPW; ++k)
-        if (k == m.sub) mine = rows[k];
-      if (mine >= 0) emit(ub + static_cast<uint32_t>(mine), t, *reinterpret_cast<const float4*>(acc + mine * D + m.c * 4));
+      const int row = __ffsll(static_cast<long long>(tall)) - 1;
+      float* a = acc + row * D + m.c * 4;
+      const float4 x = *reinterpret_cast<const float4*>(a);
+      st4(a, make_float4(0.f, 0.f, 0.f, 0.f));
+      red_g64<VEC>(g64, ub + static_cast<uint32_t>(row), m.c, x.x, x.y, x.z, x.w);
+      for (int k = 0; k < RPW && tall; ++k) tall &= tall - 1;
     }
     __syncwarp();
   }
@@ -842,27 +846,48 @@ __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restri
                                                         double* __restrict__ g64, float lr, int local_hbm) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  constexpr int R = 4;  // rows per lane group in flight
   const RowMap<VEC> m;
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int g = warp * RPW + m.sub; g < U; g += nwarps * RPW) {
-    const int n = ucount ? ucount[g] : kLightAdds + 1;
-    if (ucount && m.c == 0) ucount[g] = 0;
-    if (n <= kLightAdds) continue;
-    double gs[4];
-    take_g64<VEC>(g64, g, m.c, gs);
-    const int32_t s = usrc[g];
-    float* dst = s >= 0 ? cache + static_cast<int64_t>(s) * D
-               : local_hbm ? td[utab[g]].store + static_cast<int64_t>(uniq[g]) * D
-                           : nullptr;
-    if (dst) {
-      st4(dst + m.c * 4, sgd4(*reinterpret_cast<const float4*>(dst + m.c * 4), gs, lr));
-    } else {
-      float* p = ugrad + static_cast<int64_t>(g) * D + m.c * 4;
-      const float4 a = *reinterpret_cast<const float4*>(p);
-      st4(p, make_float4(static_cast<float>(a.x + gs[0]), static_cast<float>(a.y + gs[1]),
-                         static_cast<float>(a.z + gs[2]), static_cast<float>(a.w + gs[3])));
+  for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
+    int n[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      n[r] = g < U ? (ucount ? __ldcg(ucount + g) : kLightAdds + 1) : 0;
+    }
+    if (ucount && m.c == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (g0 + r * RPW + m.sub < U) ucount[g0 + r * RPW + m.sub] = 0;
+    }
+    double gs[R][4];
+    float* dst[R];
+    float4 w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int g = g0 + r * RPW + m.sub;
+      dst[r] = nullptr;
+      if (n[r] <= kLightAdds) continue;
+      take_g64<VEC>(g64, g, m.c, gs[r]);
+      const int32_t s = usrc[g];
+      dst[r] = s >= 0 ? cache + static_cast<int64_t>(s) * D
+             : local_hbm ? td[utab[g]].store + static_cast<int64_t>(uniq[g]) * D
+                         : ugrad + static_cast<int64_t>(g) * D;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r] = dst[r] ? *reinterpret_cast<const float4*>(dst[r] + m.c * 4) : float4{};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!dst[r]) continue;
+      const int g = g0 + r * RPW + m.sub;
+      if (dst[r] == ugrad + static_cast<int64_t>(g) * D)  // pinned-host miss: its gradient for the write-back
+        st4(dst[r] + m.c * 4, make_float4(static_cast<float>(w[r].x + gs[r][0]), static_cast<float>(w[r].y + gs[r][1]),
+                                          static_cast<float>(w[r].z + gs[r][2]), static_cast<float>(w[r].w + gs[r][3])));
+      else
+        st4(dst[r] + m.c * 4, sgd4(w[r], gs[r], lr));
     }
   }
 }
@@ -874,7 +899,8 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
                                                     const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                                                     const int32_t* __restrict__ usrc, const float* __restrict__ urows,
                                                     const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
-                                                    int hits, int misses_local, int rank, int world) {
+                                                    int hits, int misses_local, int rank, int world,
+                                                    const int* __restrict__ off = nullptr, double* __restrict__ g64 = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -896,6 +922,14 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
       }
       if (!dst) continue;
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
+      if (off && chunk_span(off[g], off[g + 1]) > kLightAdds) {
+        // (k_g64_finalize folded in) a row spread over many k_bwd_reduce chunks:
+        // its fp64 sum, one rounding
+        double gs[4];
+        take_g64<VEC>(g64, g, m.c, gs);
+        st4(dst + m.c * 4, sgd4(w, gs, lr));
+        continue;
+      }
       const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
       st4(dst + m.c * 4, make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
     }

@@ -553,6 +553,35 @@ int ec_schedule_order(const uint32_t* ids, uint64_t q, int64_t d, uint64_t vocab
   });
 }
 
+// build_schedule with a shuffle seed (core/src/trace.cpp:206-240): the GPU's
+// stable hot/normal partition, then each class permuted on the host by a
+// Fisher-Yates walk from the top index down, drawing j = next() % (i + 1) from
+// SplitMix64(substream_seed(seed, class)) -- class 0 hot, 1 normal
+// (trace.cpp:211-222).  The permutation is a serial chain of 64-bit draws, so it
+// stays on the host; the partition (the O(Q*d) part) runs on the device.
+int ec_build_schedule(const uint32_t* ids, uint64_t q, int64_t d, uint64_t vocab, const uint32_t* cache, uint64_t k,
+                      int device, int shuffle, uint64_t seed, uint32_t* order_host, uint64_t* num_hot) {
+  return guard([&] {
+    use_device(device);
+    Stream st;
+    TraceOnDevice t;
+    classify_and_order(t, ids, q, d, vocab, cache, k, device, st.s, true);
+    EC_CUDA(cudaMemcpy(order_host, t.order.p, q * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    *num_hot = t.nhot;
+    if (!shuffle) return;
+    const uint64_t lo[2] = {0, t.nhot}, hi[2] = {t.nhot, q};
+    for (int cls = 0; cls < 2; ++cls) {
+      uint64_t state = substream(seed, static_cast<uint64_t>(cls));
+      uint32_t* v = order_host + lo[cls];
+      for (uint64_t len = hi[cls] - lo[cls]; len > 1; --len) {
+        state += kGolden;
+        const uint64_t j = mix64(state) % len;
+        std::swap(v[len - 1], v[j]);
+      }
+    }
+  });
+}
+
 // simulate_epoch(Trace, b, C), core/src/simulator.cpp:222-273.
 int ec_simulate_trace(const uint32_t* ids, uint64_t q, int64_t d, uint64_t vocab, int64_t b,
                       const uint32_t* cache, uint64_t k, int device, ec_sim_result* out) {

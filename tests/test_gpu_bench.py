@@ -41,6 +41,9 @@ def test_bench_single_gpu_line():
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(d["roofline"])
     assert d["gpu_launches"] > 0
+    assert d["gather_roofline"]["kernel"] in ("k_pool", "k_gather") and d["gather_roofline"]["frac"] > 0
+    assert d["comm"]["expected_model_rows_per_batch"] > 0
+    assert len(d["comm"]["model_rows_per_table_batch0"]) == 26
 
 
 def _first_traceback(err):

@@ -58,3 +58,24 @@ def test_multi_table_hot_batches_have_no_misses(ec, torch):
         if first + B <= nh:
             assert st["miss_rows"] == 0  # a hot batch never reaches the cold tier
     tab.close()
+
+
+@pytest.mark.parametrize("seed", [None, 0, 1, 20241101, (1 << 62) + 7])
+@pytest.mark.parametrize("d_feat,q", [(1, 1), (3, 5000), (2, 777)])
+def test_build_schedule_shuffle_matches_reference(ec, ref, seed, d_feat, q):
+    """build_schedule(trace, cache, b, shuffle_seed) (trace.cpp:206-240): the
+    GPU partition plus the seeded per-class Fisher-Yates equal the reference's
+    schedule batch for batch (order and batch sizes), including a one-sample
+    trace and classes of one sample."""
+    E, b = 400, 64
+    dist = ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, E, 1.05))
+    ids = ec.sample_batch(dist, q, d_feat, ec.SplitMix64(99 + q))
+    tr = ec.Trace(d_feat, E, ids)
+    cache = dist.top_ids(30)
+    s = ec.build_schedule(tr, cache, b, shuffle_seed=seed)
+    ref_order, ref_sizes, ref_nh = ref.ref_build_schedule(ids, d_feat, E, cache, b,
+                                                          shuffle_seed=-1 if seed is None else seed)
+    flat = [x for bt in s.hot_batches + s.normal_batches for x in bt]
+    assert flat == ref_order.tolist()
+    assert [len(bt) for bt in s.hot_batches + s.normal_batches] == ref_sizes.tolist()
+    assert sum(len(bt) for bt in s.hot_batches) == ref_nh
