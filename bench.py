@@ -660,7 +660,10 @@ def run_ours(args, wl):
         "phases": phases,
         "comm": {"model_rows_per_batch": s0["miss_rows"], "model_bytes_per_batch": s0["model_bytes"],
                  "unique_rows_per_batch": s0["unique_rows"], "hit_rows_per_batch": s0["hit_rows"],
-                 "wire_bytes_per_batch": s0["wire_bytes"]},
+                 "wire_bytes_per_batch": s0["wire_bytes"],
+                 # N>1: the replicated hot cache's sync (gradients to slot owners, updated rows back),
+                 # reported apart from the reference-priced miss rows; included in wire_bytes
+                 "hot_sync_bytes_per_batch": s0.get("hot_sync_bytes", 0)},
         "hot_normal_schedule": hot_normal,
         "setup_s": round(setup_s, 1),
     }

@@ -417,6 +417,9 @@ typedef struct {
   uint64_t wire_rows;      /* misses owned by another rank (fetched over the exchange) */
   uint64_t wire_bytes;     /* bytes actually sent + received by this rank's exchange */
   uint64_t hot_tables;     /* tables whose batch touched no uncached row */
+  uint64_t hot_sync_rows;  /* peer exchange: hot-row gradients sent to other owners + updated hot rows copied
+                              from them (the replicated cache's sync; outside the reference's cost model) */
+  uint64_t hot_sync_bytes; /* their bytes (slot index + row); included in wire_bytes */
 } ec_batch_stats;
 /* Synchronises `stream`; per-table arrays (length num_tables) may be NULL. */
 int ec_lookup_stats(ec_tables t, void* stream, ec_batch_stats* out, int64_t* unique_per_table_host,

@@ -86,7 +86,8 @@ class Batch(C.Structure):
 
 class BatchStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("lookups", "unique_rows", "hit_rows", "miss_rows", "index_units",
-                                          "model_bytes", "wire_rows", "wire_bytes", "hot_tables")]
+                                          "model_bytes", "wire_rows", "wire_bytes", "hot_tables",
+                                          "hot_sync_rows", "hot_sync_bytes")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

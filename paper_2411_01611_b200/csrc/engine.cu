@@ -1637,11 +1637,15 @@ static void decode_stats(Engine& e, int* h, uint64_t lookups, uint64_t wire_rows
   s.wire_rows = wire_rows;
   s.wire_bytes = wire_bytes;
   if (e.p2p_on()) {
-    // peer-memory exchange: rows this rank pulled (device count), their
-    // gradient atomics back, and its hot list read by every other rank
+    // peer-memory exchange: rows this rank pulled (device count) and their
+    // gradient atomics back (the reference-priced miss rows), plus the hot-row
+    // sync (not in the reference's model): gradients to other owners, updated
+    // rows from them (counted on the device, complete once the backward ran)
     const uint64_t rowb = static_cast<uint64_t>(e.D) * sizeof(float);
     s.wire_rows = static_cast<uint64_t>(*c.wire);
-    s.wire_bytes = 2 * s.wire_rows * rowb + s.hit_rows * (4 + rowb) * static_cast<uint64_t>(e.world - 1);
+    s.hot_sync_rows = static_cast<uint64_t>(*c.hot_out) + static_cast<uint64_t>(*c.hot_in);
+    s.hot_sync_bytes = s.hot_sync_rows * (4 + rowb);
+    s.wire_bytes = 2 * s.wire_rows * rowb + s.hot_sync_bytes;
   }
   *out = s;
 }

@@ -33,15 +33,16 @@ struct Tile {
 };
 
 // Per-batch device counters, one int array:
-//   M[T] ubase[T+1] miss_total tile_counter wire err   (err last: survives resets)
-// wire: rows pulled from peer shards by the P2P exchange.
+//   M[T] ubase[T+1] miss_total tile_counter wire hot_out hot_in err   (err last: survives resets)
+// wire: rows pulled from peer shards by the P2P exchange; hot_out / hot_in:
+// hot-row gradients sent to other owners / updated hot rows copied from them.
 struct Counters {
-  int *M, *ubase, *miss_total, *tile_counter, *wire, *err;
+  int *M, *ubase, *miss_total, *tile_counter, *wire, *hot_out, *hot_in, *err;
 };
 __host__ __device__ inline Counters counters(int* p, int T) {
-  return Counters{p, p + T, p + 2 * T + 1, p + 2 * T + 2, p + 2 * T + 3, p + 2 * T + 4};
+  return Counters{p, p + T, p + 2 * T + 1, p + 2 * T + 2, p + 2 * T + 3, p + 2 * T + 4, p + 2 * T + 5, p + 2 * T + 6};
 }
-inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 5; }
+inline size_t counters_size(int T) { return 2 * static_cast<size_t>(T) + 7; }
 
 // What a rank sees of a peer for the peer-memory exchange (K4 over NVLink
 // loads/stores/atomics): the peer's HBM shard and its published hot-row
@@ -50,9 +51,13 @@ constexpr int kP2PBarriers = 2;  // device barriers per step of the peer-memory 
 
 struct PeerView {
   float* store;             // the peer's whole shard (row = shard_off[peer][t] + id / world)
-  const uint32_t* pub_slot; // its hot list: cache slots ...
-  const float* pub_grad;    // ... and their gradient rows
-  const int* pub_cnt;       // ... and its length
+  // hot rows (replicated cache) owned by the peer (cache slot % world == peer):
+  const uint32_t* upd_slot; // slots it updated this step ...
+  const float* upd_rows;    // ... their new values ...
+  const int* upd_cnt;       // ... and how many
+  uint32_t* hin_slot;       // its inbox of hit gradients for its slots, one segment per source rank:
+  float* hin_grad;          //   [world][cap] slots / gradient rows
+  int* hin_cnt;             //   [world] counts
   unsigned* flags;          // the peer's barrier words: [kP2PBarriers * world]
   // pinned-host shards: the owner's inbox of miss-row gradients, one segment
   // per source rank ([world][cap] row indices / gradient rows, [world] counts)
@@ -354,7 +359,11 @@ struct Engine {
   void p2p_signal(int b, cudaStream_t st);
   void p2p_wait(int b, unsigned epoch, cudaStream_t st);
   void p2p_bwd_finish(float lr, cudaStream_t st);
+  void p2p_bwd_owner(float lr, cudaStream_t st);   // (finish, part 1) owners apply misses and their hot rows
+  void p2p_bwd_replica(cudaStream_t st);           // (finish, part 2) every replica copies the owners' hot rows
   template <int VEC> void p2p_hot(float lr, cudaStream_t st);
+  template <int VEC> void p2p_hot_copy(cudaStream_t st);
+  void p2p_hot_alloc();  // owner accumulators, sized by the cache
 };
 
 // Instantiate FN<VEC> for the row width (D/4 float4 lanes per row).

@@ -68,9 +68,17 @@ struct Exchange {
   bool step_open = false;           // a forward whose step was not applied yet
   DevBuf<PeerView> peers;           // [W]
   std::vector<PeerView> peers_host;
-  DevBuf<uint32_t> pub_slot;        // this rank's published hot list
-  DevBuf<float> pub_grad;
-  DevBuf<int> pub_cnt;
+  // hot rows this rank owns (cache slot % W == rank): sources' gradients in,
+  // the updated rows out (PeerView::hin_* / upd_*)
+  DevBuf<uint32_t> hin_slot;        // [W * hcap]
+  DevBuf<float> hin_grad;           // [W * hcap * D]
+  DevBuf<int> hin_cnt;              // [W]
+  int64_t hcap = 0;
+  DevBuf<float> hacc;               // [ceil(K / W) * D] gradient sums of owned slots (zero between steps)
+  DevBuf<unsigned> hmark;           // [ceil(K / W)] owned slot touched this step
+  DevBuf<uint32_t> upd_slot;        // [min(W * hcap, K / W)] owned slots updated this step
+  DevBuf<float> upd_rows;           //   and their new values
+  DevBuf<int> upd_cnt;              // [1]
   DevBuf<unsigned> flags;           // [2W] barrier words peers write into
   DevBuf<unsigned> done;            // arrival counter of a kernel that signals a barrier
   std::vector<void*> ipc_opened;    // peer allocations mapped by cudaIpcOpenMemHandle
@@ -269,8 +277,7 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
                             const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
                             const int32_t* __restrict__ usrc, const float* __restrict__ ugrad, float lr,
                             const PeerView* __restrict__ peers, const int64_t* __restrict__ shard_off, int rank,
-                            int world, uint32_t* __restrict__ pub_slot, float* __restrict__ pub_grad,
-                            int* __restrict__ pub_cnt, int64_t inbox_cap, int part, P2PSync sync) {
+                            int world, int64_t hcap, int64_t inbox_cap, int part, P2PSync sync) {
   constexpr int D = VEC * 4;
   p2p_prologue(sync);
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
@@ -282,16 +289,23 @@ __global__ void k_p2p_apply(const TableDev* __restrict__ td, int T, const int* _
     const bool live = g < U;
     const int32_t s = live ? usrc[g] : -1;
     const float4 gv = live ? ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    // part & 1 -- hits: one list slot per row (lane c == 0 of the row's group claims it)
+    // part & 1 -- hits: the gradient goes to the slot's owner (slot % world),
+    // appended to this rank's segment of the owner's hot inbox; lane c == 0 of
+    // a row's group claims the position, one atomic per (warp, owner)
     const bool hit = (part & 1) && live && s >= 0;
-    const unsigned hb = __ballot_sync(kFull, hit && c == 0);
-    int b0 = 0;
-    if (hb && lane_id() == __ffs(hb) - 1) b0 = atomicAdd(pub_cnt, __popc(hb));
-    b0 = __shfl_sync(kFull, b0, __ffs(hb ? hb : 1u) - 1);
-    const int pos = b0 + __popc(hb & ((1u << (sub * VEC)) - 1));
+    const int ho = hit ? s % world : -1;
+    const unsigned same = __match_any_sync(kFull, hit && c == 0 ? ho : -1);
+    int pos = 0;
+    if (hit && c == 0 && __ffs(same) - 1 == lane_id())
+      pos = atomicAdd(peers[ho].hin_cnt + rank, __popc(same));
+    pos = __shfl_sync(kFull, pos, hit && c == 0 ? __ffs(same) - 1 : 0) + __popc(same & ((1u << lane_id()) - 1));
+    pos = __shfl_sync(kFull, pos, sub * VEC);  // (lane c == 0 of this row's group)
+    const int sent = __popc(__ballot_sync(kFull, hit && c == 0 && ho != rank));
+    if (sent && lane_id() == 0) atomicAdd(counters(const_cast<int*>(ctr), T).hot_out, sent);
     if (hit) {
-      if (c == 0) pub_slot[pos] = static_cast<uint32_t>(s);
-      st4(pub_grad + static_cast<int64_t>(pos) * D + c * 4, gv);
+      const int64_t k = static_cast<int64_t>(rank) * hcap + pos;
+      if (c == 0) peers[ho].hin_slot[k] = static_cast<uint32_t>(s);
+      st4(peers[ho].hin_grad + k * D + c * 4, gv);
     }
     // part & 2 -- misses: the owner's row (index in its shard)
     const bool miss = (part & 2) && live && s < 0;
@@ -369,26 +383,78 @@ __global__ void k_p2p_patch(const int* __restrict__ ctr, int T, const uint32_t* 
 }
 
 
-// One source rank's published hot gradients into this rank's cache replica
-// (launched for p = 0..world-1: every replica sees the same order).
+// Hot rows (the replicated cache), owner-partitioned: slot s is owned by rank
+// s % world.  After barrier 0 every owner sums the gradients its inbox holds
+// for its slots (every source rank's segment; fp32 REDs, at most `world` per
+// slot) and marks each touched slot once; then it applies w - lr * sum to its
+// replica, publishes (slot, new row), and signals barrier 1; then every rank
+// copies every owner's updated rows into its own replica.  Replicas stay
+// bit-identical (all copy the owner's value), and a rank moves ~H rows out
+// and |union of hits| rows in per step instead of reading W-1 peers' full
+// hot lists and applying them in W rank-ordered passes.
 template <int VEC>
-__global__ void k_p2p_hot_apply(const PeerView* __restrict__ peers, int p, float* __restrict__ cache, float lr,
-                                P2PSync sync) {
+__global__ void k_p2p_hot_reduce(const uint32_t* __restrict__ hin_slot, const float* __restrict__ hin_grad,
+                                 const int* __restrict__ hin_cnt, int64_t hcap, int world, float* __restrict__ hacc,
+                                 unsigned* __restrict__ hmark, uint32_t* __restrict__ upd_slot, int* __restrict__ upd_cnt) {
   constexpr int D = VEC * 4;
-  p2p_prologue(sync);
-  const PeerView pv = peers[p];
-  const int n = *reinterpret_cast<const volatile int*>(pv.pub_cnt);
-  const int64_t total = static_cast<int64_t>(n) * VEC;
+  for (int p = 0; p < world; ++p) {
+    const int n = hin_cnt[p];
+    const int64_t total = static_cast<int64_t>(n) * VEC;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t k = i / VEC;
+      const int c = static_cast<int>(i - k * VEC);
+      const int64_t e = static_cast<int64_t>(p) * hcap + k;
+      const uint32_t slot = hin_slot[e];
+      const uint32_t j = slot / static_cast<uint32_t>(world);
+      atomicAdd(reinterpret_cast<float4*>(hacc + static_cast<int64_t>(j) * D + c * 4), ldg4(hin_grad + e * D + c * 4));
+      if (c == 0 && atomicExch(hmark + j, 1u) == 0u) upd_slot[atomicAdd(upd_cnt, 1)] = slot;
+    }
+  }
+}
+
+template <int VEC>
+__global__ void k_p2p_hot_update(const uint32_t* __restrict__ upd_slot, const int* __restrict__ upd_cnt, int world,
+                                 float* __restrict__ cache, float* __restrict__ hacc, unsigned* __restrict__ hmark,
+                                 float* __restrict__ upd_rows, int* __restrict__ hin_cnt, float lr, P2PSync sync) {
+  constexpr int D = VEC * 4;
+  const int64_t total = static_cast<int64_t>(*upd_cnt) * VEC;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i / VEC;
     const int c = static_cast<int>(i - k * VEC);
-    float* w = cache + static_cast<int64_t>(pv.pub_slot[k]) * D + c * 4;
-    const float4 gv = *reinterpret_cast<const float4*>(pv.pub_grad + k * D + c * 4);
+    const uint32_t slot = upd_slot[k];
+    const uint32_t j = slot / static_cast<uint32_t>(world);
+    float* a = hacc + static_cast<int64_t>(j) * D + c * 4;
+    const float4 g = *reinterpret_cast<const float4*>(a);
+    float* w = cache + static_cast<int64_t>(slot) * D + c * 4;
     float4 v = *reinterpret_cast<const float4*>(w);
-    v = make_float4(v.x - lr * gv.x, v.y - lr * gv.y, v.z - lr * gv.z, v.w - lr * gv.w);
+    v = make_float4(v.x - lr * g.x, v.y - lr * g.y, v.z - lr * g.z, v.w - lr * g.w);
     st4(w, v);
+    st4(upd_rows + k * D + c * 4, v);
+    st4(a, make_float4(0.f, 0.f, 0.f, 0.f));
+    if (c == 0) hmark[j] = 0u;
   }
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < world) hin_cnt[threadIdx.x] = 0;  // (read by the reduce)
   p2p_epilogue(sync);
+}
+
+// Every other owner's updated hot rows into this rank's replica (one launch).
+template <int VEC>
+__global__ void k_p2p_hot_copy(const PeerView* __restrict__ peers, int world, int rank, float* __restrict__ cache,
+                               int* __restrict__ ctr, int T) {
+  constexpr int D = VEC * 4;
+  for (int o = 0; o < world; ++o) {
+    if (o == rank) continue;
+    const PeerView pv = peers[o];
+    const int n = *reinterpret_cast<const volatile int*>(pv.upd_cnt);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counters(ctr, T).hot_in, n);
+    const int64_t total = static_cast<int64_t>(n) * VEC;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t k = i / VEC;
+      const int c = static_cast<int>(i - k * VEC);
+      st4(cache + static_cast<int64_t>(pv.upd_slot[k]) * D + c * 4,
+          *reinterpret_cast<const float4*>(pv.upd_rows + k * D + c * 4));
+    }
+  }
 }
 
 // Device barrier over peer memory, split in two so a loopback group can
@@ -609,12 +675,20 @@ void Engine::p2p_alloc() {
     x.ver.alloc(std::max<uint64_t>(store_off[T], 1));
     EC_CUDA(cudaMemset(x.ver.p, 0, x.ver.bytes()));  // generation 0 is never a step
   }
-  if (x.pub_slot.n < N) x.pub_slot.alloc(N);
-  if (x.pub_grad.n < N * D) x.pub_grad.alloc(N * D);
-  if (!x.pub_cnt.n) {
-    x.pub_cnt.alloc(1);
-    EC_CUDA(cudaMemset(x.pub_cnt.p, 0, sizeof(int)));
+  if (x.hcap < static_cast<int64_t>(N)) {  // a source sends at most its batch's N unique rows
+    x.hcap = static_cast<int64_t>(N);
+    x.hin_slot.alloc(x.W * N);
+    x.hin_grad.alloc(x.W * N * D);
+    x.hin_cnt.alloc(x.W);
+    EC_CUDA(cudaMemset(x.hin_cnt.p, 0, x.hin_cnt.bytes()));
+    x.upd_slot.alloc(x.W * N);
+    x.upd_rows.alloc(x.W * N * D);
   }
+  if (!x.upd_cnt.n) {
+    x.upd_cnt.alloc(1);
+    EC_CUDA(cudaMemset(x.upd_cnt.p, 0, sizeof(int)));
+  }
+  p2p_hot_alloc();
   if (!x.done.n) {
     x.done.alloc(1);
     EC_CUDA(cudaMemset(x.done.p, 0, sizeof(unsigned)));
@@ -625,9 +699,22 @@ void Engine::p2p_alloc() {
   }
 }
 
+// owner-side accumulators for the slots this rank owns (re-sized with the cache)
+void Engine::p2p_hot_alloc() {
+  if (!ex) return;
+  Exchange& x = *ex;
+  const size_t own = (cache_k_total + x.W - 1) / x.W;
+  if (x.hmark.n >= std::max<size_t>(own, 1)) return;
+  x.hacc.alloc(std::max<size_t>(own, 1) * D);
+  x.hmark.alloc(std::max<size_t>(own, 1));
+  EC_CUDA(cudaMemset(x.hacc.p, 0, x.hacc.bytes()));
+  EC_CUDA(cudaMemset(x.hmark.p, 0, x.hmark.bytes()));
+}
+
 PeerView Engine::p2p_self() const {
-  return PeerView{store_base,      ex->pub_slot.p,   ex->pub_grad.p,  ex->pub_cnt.p, ex->flags.p,
-                  ex->inbox_idx.p, ex->inbox_grad.p, ex->inbox_cnt.p, ex->ver.p};
+  const Exchange& x = *ex;
+  return PeerView{store_base,  x.upd_slot.p,  x.upd_rows.p,  x.upd_cnt.p,  x.hin_slot.p, x.hin_grad.p,
+                  x.hin_cnt.p, x.flags.p,     x.inbox_idx.p, x.inbox_grad.p, x.inbox_cnt.p, x.ver.p};
 }
 
 void Engine::p2p_set_peers(const std::vector<PeerView>& v) {
@@ -673,10 +760,8 @@ void Engine::p2p_fwd_begin(cudaStream_t st) {
 template <int VEC>
 void Engine::p2p_publish(float lr, cudaStream_t st, int part, int wait_b, int sig_b) {
   Exchange& x = *ex;
-  if (part & 1) EC_CUDA(cudaMemsetAsync(x.pub_cnt.p, 0, sizeof(int), st));  // peers finished reading it (barrier 1)
   k_p2p_apply<VEC><<<row_grid(), 256, 0, st>>>(tdev.p, static_cast<int>(T), ctr.p, uniq.p, utab.p, usrc.p,
-                                                   ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.pub_slot.p,
-                                                   x.pub_grad.p, x.pub_cnt.p,
+                                                   ugrad.p, lr, x.peers.p, x.shard_off.p, rank, world, x.hcap,
                                                    storage == EC_STORAGE_HOST ? x.inbox_cap : 0, part,
                                                    p2p_sync(x, rank, wait_b, sig_b));
   launched();
@@ -706,12 +791,27 @@ void Engine::p2p_hot(float lr, cudaStream_t st) {
     }
     EC_CUDA(cudaMemsetAsync(x.inbox_cnt.p, 0, x.inbox_cnt.bytes(), st));  // sources append after barrier 1
   }
-  for (int p = 0; p < ex->W; ++p) {
-    k_p2p_hot_apply<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, p, cache.p, lr,
-                                                                p2p_sync(x, rank, -1, p == ex->W - 1 ? 1 : -1));
-    launched();
-  }
+  // owner: every source's hit gradients for this rank's slots, then the
+  // update (its last block signals barrier 1); upd_cnt is free to reset:
+  // every replica finished copying the last step's rows before barrier 0
+  p2p_hot_alloc();
+  EC_CUDA(cudaMemsetAsync(x.upd_cnt.p, 0, sizeof(int), st));
+  const int hg = sm_count(device) * 2;
+  k_p2p_hot_reduce<VEC><<<hg, 256, 0, st>>>(x.hin_slot.p, x.hin_grad.p, x.hin_cnt.p, x.hcap, x.W, x.hacc.p, x.hmark.p,
+                                            x.upd_slot.p, x.upd_cnt.p);
+  launched();
+  k_p2p_hot_update<VEC><<<hg, 256, 0, st>>>(x.upd_slot.p, x.upd_cnt.p, x.W, cache.p, x.hacc.p, x.hmark.p,
+                                            x.upd_rows.p, x.hin_cnt.p, lr, p2p_sync(x, rank, -1, 1));
+  launched();
 }
+
+template <int VEC>
+void Engine::p2p_hot_copy(cudaStream_t st) {
+  k_p2p_hot_copy<VEC><<<sm_count(device) * 2, 256, 0, st>>>(ex->peers.p, ex->W, rank, cache.p, ctr.p,
+                                                            static_cast<int>(T));
+  launched();
+}
+
 template <int VEC>
 void Engine::p2p_patch(cudaStream_t st) {
   k_p2p_patch<VEC><<<host_grid(), 256, 0, st>>>(ctr.p, static_cast<int>(T), missq.p, uniq.p, utab.p, urows.p,
@@ -720,11 +820,20 @@ void Engine::p2p_patch(cudaStream_t st) {
 }
 void Engine::p2p_patch_prefetched(cudaStream_t st) { EC_DISPATCH_VEC(p2p_patch, st); }
 
-void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
+void Engine::p2p_bwd_owner(float lr, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseExchange, st);
   p2p_wait(0, ex->epoch, st);
   EC_DISPATCH_VEC(p2p_hot, lr, st);  // its last kernel signals barrier 1
+}
+void Engine::p2p_bwd_replica(cudaStream_t st) {
+  PhaseScope ph(prof, kPhaseExchange, st);
+  p2p_wait(1, ex->epoch, st);  // every owner applied its rows
+  EC_DISPATCH_VEC(p2p_hot_copy, st);
   ex->step_open = false;
+}
+void Engine::p2p_bwd_finish(float lr, cudaStream_t st) {
+  p2p_bwd_owner(lr, st);
+  p2p_bwd_replica(st);
 }
 
 // ------------------------------------------------------------ NCCL driver
@@ -1004,7 +1113,9 @@ int ec_group_lookup_bwd(ec_group g, const float* const* grads, float lr, void* s
         e.scatter_grads(grads[r], st);
         e.p2p_bwd_publish(lr, st);  // (its last block signals barrier 0)
       }
-      for (int r = 0; r < W; ++r) g->members[r]->e.p2p_bwd_finish(lr, st);
+      // every owner's barrier-1 signal precedes every replica's wait on one stream
+      for (int r = 0; r < W; ++r) g->members[r]->e.p2p_bwd_owner(lr, st);
+      for (int r = 0; r < W; ++r) g->members[r]->e.p2p_bwd_replica(st);
       return;
     }
     for (int r = 0; r < W; ++r) {
@@ -1056,12 +1167,12 @@ int ec_group_set_p2p(ec_group g, int enable) {
 
 // Multi-process: this rank's peer-visible allocations, to be all-gathered
 // and passed to every rank's ec_tables_p2p_import.  Blob: CUDA IPC handles of
-// {shard (HBM), hot list, its gradients, its length, barrier words, inbox
-// indices, inbox gradients, inbox counts, row generations} (unused ones
-// zero), then the host
+// {shard (HBM), updated hot slots, their rows, their count, hot inbox slots,
+// gradients, counts, barrier words, miss inbox indices, gradients, counts,
+// row generations} (unused ones zero), then the host
 // shard's memfd as {pid, fd, bytes} (pinned-host tier; zeros for HBM).
 namespace {
-constexpr int kP2PHandles = 9;
+constexpr int kP2PHandles = 12;
 struct HostSeg {
   int64_t pid, fd;
   uint64_t bytes;
@@ -1083,8 +1194,9 @@ int ec_tables_p2p_export(ec_tables t, uint8_t* blob, uint64_t cap, uint64_t* len
     if (cap < kP2PBlob) invalid("p2p export blob needs " + std::to_string(kP2PBlob) + " bytes");
     std::memset(blob, 0, kP2PBlob);
     const Exchange& x = *e.ex;
-    void* ptrs[kP2PHandles] = {e.store_dev.p, x.pub_slot.p,   x.pub_grad.p,  x.pub_cnt.p, x.flags.p,
-                               x.inbox_idx.p, x.inbox_grad.p, x.inbox_cnt.p, x.ver.p};
+    void* ptrs[kP2PHandles] = {e.store_dev.p,  x.upd_slot.p,  x.upd_rows.p,   x.upd_cnt.p,
+                               x.hin_slot.p,   x.hin_grad.p,  x.hin_cnt.p,    x.flags.p,
+                               x.inbox_idx.p,  x.inbox_grad.p, x.inbox_cnt.p, x.ver.p};
     for (int k = 0; k < kP2PHandles; ++k) {
       if (!ptrs[k]) continue;
       cudaIpcMemHandle_t h;
@@ -1164,9 +1276,10 @@ int ec_tables_p2p_import(ec_tables t, const uint8_t* blobs, uint64_t blob_len) {
       }
       views[p] = PeerView{static_cast<float*>(ptrs[0]),       static_cast<const uint32_t*>(ptrs[1]),
                           static_cast<const float*>(ptrs[2]), static_cast<const int*>(ptrs[3]),
-                          static_cast<unsigned*>(ptrs[4]),    static_cast<uint32_t*>(ptrs[5]),
-                          static_cast<float*>(ptrs[6]),       static_cast<int*>(ptrs[7]),
-                          static_cast<uint32_t*>(ptrs[8])};
+                          static_cast<uint32_t*>(ptrs[4]),    static_cast<float*>(ptrs[5]),
+                          static_cast<int*>(ptrs[6]),         static_cast<unsigned*>(ptrs[7]),
+                          static_cast<uint32_t*>(ptrs[8]),    static_cast<float*>(ptrs[9]),
+                          static_cast<int*>(ptrs[10]),        static_cast<uint32_t*>(ptrs[11])};
     }
     e.p2p_set_peers(views);
   });

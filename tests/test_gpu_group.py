@@ -39,8 +39,9 @@ def _current_rows(members, t, ids, world, cached):
 
 
 @pytest.mark.parametrize("world,storage,p2p", [(2, "hbm", False), (3, "host", False), (4, "hbm", False),
-                                               (2, "hbm", True), (3, "hbm", True), (4, "hbm", True),
-                                               (2, "host", True), (3, "host", True)])
+                                               (8, "hbm", False), (2, "hbm", True), (3, "hbm", True),
+                                               (4, "hbm", True), (8, "hbm", True), (2, "host", True),
+                                               (3, "host", True), (8, "host", True)])
 def test_group_forward_backward(ec, torch, ref, world, storage, p2p):
     rows, D, B, P = [5000, 37, 20000, 1], 16, 64, 5
     n = B * P
@@ -109,6 +110,10 @@ def test_group_forward_backward(ec, torch, ref, world, storage, p2p):
                         before[key] = _current_rows(members, t, [i], world, cached[t])[0].astype(np.float64)
         group.backward(grads, lr)
         torch.cuda.synchronize()
+        if p2p:  # hot-row sync of this backward: gradients to other owners, their updated rows back
+            for m in members:
+                st = m.stats()
+                assert st["hot_sync_rows"] > 0 and st["hot_sync_bytes"] == st["hot_sync_rows"] * (4 + 4 * D)
         # fp32 atomics sum each row's gradients in a varying order: the bound
         # is 1e-5 relative to the largest updated value
         scale = max(np.abs(before[k] - lr * g).max() for k, g in acc.items())
@@ -188,7 +193,7 @@ def test_p2p_import_validation(ec, torch):
           for r in range(2)]
     ho = ec.EmbeddingTables([100], 4, storage="host", rank=1, world=2, max_lookups_per_table=8, max_batch_size=8)
     blobs = [m.p2p_export() for m in hb]
-    assert len(blobs[0]) == 9 * 64 + 48
+    assert len(blobs[0]) == 12 * 64 + 48
     with pytest.raises(ValueError):
         hb[0].p2p_import(blobs[:1])
     with pytest.raises(ValueError):
