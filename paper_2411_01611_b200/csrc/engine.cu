@@ -31,6 +31,7 @@
 //            cap_t = pow2 >= 2*min(max lookups, E_t); self-cleaning per batch
 //   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
 //            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
+#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 #include <unistd.h>
 
@@ -742,7 +743,8 @@ void Engine::fwd_pool(cudaStream_t st) {
   if (fused()) {
     // rows read at their source; trailing blocks empty this batch's dedup set
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
-    const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p, cnt.p};
+    const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p, cnt.p,
+                      !bb[cur].counted ? kResetAll : storage == EC_STORAGE_HOST ? kResetMisses : kResetNone};
     const int pb = row_grid(), rb = sm_count(device);
     // 4 bags in flight per thread (measured, Kaggle: HBM tier 0.0647 -> 0.0615
     // ms vs 8; host tier, with 4 row CTAs per SM, 0.1007-0.1014 -> 0.0984-0.0995)
@@ -1247,7 +1249,8 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
   }
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
                                                                          ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
-                                                                         missq.p, ucount.p);
+                                                                         missq.p, ucount.p,
+                                                                         storage == EC_STORAGE_HOST ? 1 : 0);
 }
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
@@ -1364,7 +1367,17 @@ void Engine::read_counters(cudaStream_t st, std::vector<int>& h) {
 
 
 // ------------------------------------------------------------ profiling
-PhaseScope::PhaseScope(Profiler& p, int phase, cudaStream_t st) : p_(p), phase_(phase), st_(st) {
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+const char* phase_name(int phase) {
+  static const char* const names[kNumPhases] = {"ec:insert",  "ec:compact", "ec:inverse_partition", "ec:gather",
+                                                "ec:gather_host", "ec:exchange", "ec:pool", "ec:scatter",
+                                                "ec:apply", "ec:apply_host", "ec:dedup_cluster"};
+  return phase >= 0 && phase < kNumPhases ? names[phase] : "ec:?";
+}
+
+PhaseScope::PhaseScope(Profiler& p, int phase, cudaStream_t st)
+    : nvtx_(phase_name(phase)), p_(p), phase_(phase), st_(st) {
   if (!p_.on) return;
   a_ = p_.take();
   EC_CUDA(cudaEventRecord(a_, st_));
@@ -1544,6 +1557,7 @@ int ec_tables_write_rows(ec_tables t, uint32_t table, const uint32_t* ids, uint6
 
 int ec_lookup_fwd(ec_tables t, const ec_batch* b, float* out, void* stream) {
   return guard([&] {
+    NvtxRange r("ec_lookup_fwd");
     if (!b || !out) invalid("null argument");
     E(t).forward(*b, out, as_stream(stream));
   });
@@ -1551,6 +1565,7 @@ int ec_lookup_fwd(ec_tables t, const ec_batch* b, float* out, void* stream) {
 
 int ec_lookup_prefetch(ec_tables t, const ec_batch* b, void* stream) {
   return guard([&] {
+    NvtxRange r("ec_lookup_prefetch");
     if (!b) invalid("null batch");
     E(t).prefetch(*b, as_stream(stream));
   });
@@ -1615,7 +1630,10 @@ int ec_lookup_prefetch_wait(ec_tables t, void* stream) {
 }
 
 int ec_lookup_bwd(ec_tables t, const float* grad, float lr, void* stream) {
-  return guard([&] { E(t).backward(grad, lr, as_stream(stream)); });
+  return guard([&] {
+    NvtxRange r("ec_lookup_bwd");
+    E(t).backward(grad, lr, as_stream(stream));
+  });
 }
 
 static void decode_stats(Engine& e, int* h, uint64_t lookups, uint64_t wire_rows, uint64_t wire_bytes,

@@ -133,9 +133,18 @@ struct Profiler {
   ~Profiler();
 };
 
+// NVTX range over the host-side enqueue of one phase / one API call (header-
+// only NVTX v3: a no-op unless a tool such as Nsight or ncu --nvtx attaches).
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+};
+const char* phase_name(int phase);
+
 struct PhaseScope {
   PhaseScope(Profiler& p, int phase, cudaStream_t st);
   ~PhaseScope();
+  NvtxRange nvtx_;
   Profiler& p_;
   int phase_;
   cudaStream_t st_;

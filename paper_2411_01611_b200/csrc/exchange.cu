@@ -32,7 +32,10 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <numeric>
 #include <vector>
 
@@ -916,6 +919,44 @@ static void nccl_alltoallv(ncclComm_t comm, int W, int rank, const void* send, c
   EC_NCCL(ncclGroupEnd());
 }
 
+// Host wait for the counts all-gather (the one host synchronisation of the
+// NCCL transport: ncclSend/ncclRecv sizes are host arguments).  Polls the
+// stream and ncclCommGetAsyncError instead of blocking in
+// cudaStreamSynchronize, so a peer that died or a broken link fails the step
+// with EC_ENCCL (communicator aborted) instead of hanging it; same for a wait
+// longer than EC_NCCL_TIMEOUT_S seconds (default 60).
+static void nccl_wait(ncclComm_t& comm, cudaStream_t st) {
+  static const double limit = [] {
+    const char* v = std::getenv("EC_NCCL_TIMEOUT_S");
+    return v && *v ? std::atof(v) : 60.0;
+  }();
+  cudaEvent_t ev;
+  EC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  EC_CUDA(cudaEventRecord(ev, st));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned k = 0;; ++k) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      EC_CUDA(q);
+    }
+    ncclResult_t ar = ncclSuccess;
+    const ncclResult_t r = ncclCommGetAsyncError(comm, &ar);
+    const bool late = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit;
+    if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress) || late) {
+      cudaEventDestroy(ev);
+      ncclCommAbort(comm);  // unblocks the kernels still waiting on the dead peer
+      comm = nullptr;
+      throw Error(EC_ENCCL, late ? "NCCL exchange: counts all-gather exceeded EC_NCCL_TIMEOUT_S; communicator aborted"
+                                 : std::string("NCCL exchange: asynchronous error: ") +
+                                       ncclGetErrorString(r != ncclSuccess ? r : ar) + "; communicator aborted");
+    }
+    if (k > 64) std::this_thread::yield();
+  }
+  cudaEventDestroy(ev);
+}
+
 void Engine::exchange_fwd(cudaStream_t st) {
   Exchange& x = *ex;
   PhaseScope ph(prof, kPhaseExchange, st);
@@ -923,7 +964,7 @@ void Engine::exchange_fwd(cudaStream_t st) {
   EC_NCCL(ncclAllGather(x.cnt.p, x.allcnt.p, x.W + 1, ncclInt32, x.comm, st));
   EC_CUDA(cudaMemcpyAsync(x.allcnt_host, x.allcnt.p, static_cast<size_t>(x.W) * (x.W + 1) * sizeof(int),
                           cudaMemcpyDeviceToHost, st));
-  EC_CUDA(cudaStreamSynchronize(st));  // request sizes are needed on the host
+  nccl_wait(x.comm, st);  // request sizes are needed on the host
   ex_plan();
   nccl_alltoallv(x.comm, x.W, rank, x.send_idx.p, x.scnt, x.soff, x.recv_idx.p, x.rcnt, x.roff, sizeof(uint32_t), st);
   ex_serve(st);

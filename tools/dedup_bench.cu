@@ -1,7 +1,7 @@
 // Standalone microbenchmark of the K1+K2 cluster dedup kernel with per-phase
 // timestamps (EC_TRACE).  Not part of the product; built by tools/Makefile.
 //
-//   ./dedup_bench [kaggle|tb] [iters]
+//   ./dedup_bench [kaggle|tb] [iters] [zipf|uniform] [tag 0|1]
 //
 // Zipf(1.05) ids per table (host inverse-CDF sampler, not the reference
 // stream: only the shape matters here), a top-k cache remap, one L2 hash per
@@ -36,16 +36,18 @@ static const std::vector<uint64_t> kTb = {39884406, 39043, 17289, 7420, 20263, 3
 
 template <int ITEMS>
 static void launch(const TableDev* td, int T, const uint32_t* idx, unsigned long long* tstat, int* ctr, uint32_t* uniq,
-                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, int* ucount) {
+                   uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, int* ucount, int tag) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem>>>(td, T, idx, tstat, ctr, uniq, uslot, utab, inv, usrc,
-                                                                       missq, ucount);
+                                                                       missq, ucount, tag);
 }
 
 int main(int argc, char** argv) {
   const bool tb = argc > 1 && !std::strcmp(argv[1], "tb");
   const int iters = argc > 2 ? std::atoi(argv[2]) : 20;
+  const bool uniform = argc > 3 && !std::strcmp(argv[3], "uniform");
+  const int tag = argc > 4 ? std::atoi(argv[4]) : 1;
   const std::vector<uint64_t>& rows = tb ? kTb : kKaggle;
   const int T = static_cast<int>(rows.size());
   const int64_t n = tb ? 65536 : 16384;
@@ -60,7 +62,7 @@ int main(int argc, char** argv) {
     const uint64_t E = rows[t];
     std::vector<double> cdf(E);
     double s = 0;
-    for (uint64_t i = 0; i < E; ++i) cdf[i] = (s += std::pow(static_cast<double>(i + 1), -1.05));
+    for (uint64_t i = 0; i < E; ++i) cdf[i] = (s += uniform ? 1.0 : std::pow(static_cast<double>(i + 1), -1.05));
     std::uniform_real_distribution<double> u(0.0, s);
     std::unordered_set<uint32_t> seen;
     for (int64_t i = 0; i < n; ++i) {
@@ -131,11 +133,11 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a));
     switch (items) {
-      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
-      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
-      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
-      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
-      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount); break;
+      case 1: launch<1>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount, tag); break;
+      case 2: launch<2>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount, tag); break;
+      case 4: launch<4>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount, tag); break;
+      case 8: launch<8>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount, tag); break;
+      default: launch<16>(dtd, T, didx, tstat, ctr, uniq, uslot, utab, inv, usrc, missq, ucount, tag); break;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(b));
@@ -167,7 +169,20 @@ int main(int argc, char** argv) {
       if (husrc[g] != want) ++bad_src;
       miss += want < 0;
     }
-    std::printf("validate: bad inverse %ld, bad usrc %ld, expected misses %ld\n", bad_inv, bad_src, miss);
+    // the L2 set after the kernel: the tagged misses (tag) or nothing
+    long left = 0, bad_tag = 0;
+    for (int t = 0; t < T; ++t) {
+      std::vector<unsigned long long> hs(hslots[t]);
+      CK(cudaMemcpy(hs.data(), td[t].hash, hslots[t] * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < hslots[t]; ++i)
+        if (hs[i] != ~0ull) {
+          ++left;
+          const uint32_t g = static_cast<uint32_t>(hs[i]) & ~kRankTag;
+          if ((hs[i] >> 32) != i || g >= static_cast<uint32_t>(U) || huniq[g] != i || husrc[g] >= 0) ++bad_tag;
+        }
+    }
+    std::printf("validate: bad inverse %ld, bad usrc %ld, expected misses %ld, L2 slots left %ld (want %ld), bad tags %ld\n",
+                bad_inv, bad_src, miss, left, tag ? miss : 0L, bad_tag);
   }
   std::vector<unsigned long long> tr(nblk * 8);
   CK(cudaMemcpy(tr.data(), trace, tr.size() * 8, cudaMemcpyDeviceToHost));
