@@ -509,9 +509,9 @@ struct ResetOut {
   const int32_t* usrc;
   float* ugrad;
   int* cnt;  // per-unique add counters of the fused SGD scatter
-  // L2 set slots the batch's dedup left behind: kResetAll (tile / per-table
-  // kernels: every unique, plus its idcnt), kResetMisses (cluster kernel with
-  // `tag`: the tagged misses), kResetNone (cluster kernel, no tags)
+  // set slots the batch's dedup left behind: kResetAll (tile / per-table
+  // kernels: every unique's slot and idcnt), kResetMisses (cluster kernel
+  // with `tag`: the tagged misses), kResetNone (cluster kernel, no tags)
   int hash_reset;
 };
 constexpr int kResetNone = 0, kResetMisses = 1, kResetAll = 2;
@@ -1048,18 +1048,11 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
 //
 //   L  hot ids (id < kClusterLocal: the top ranks of a parametric table, or
 //      all of a small table) are deduplicated per CTA in shared memory
-//      (direct-mapped atomicMin after a warp match-any collapse), so the
-//      cluster-wide set sees one insert per (CTA, hot id) instead of thousands
-//      of same-address atomics.
-//   G  representatives insert (id, position) into the table's dedup set, which
-//      lives in the cluster's distributed shared memory, partitioned over the
-//      8 CTAs: hot ids in a direct-mapped array (owner id & 7, 32-bit
-//      atomicMin of the position), colder ids in open-addressing hash
-//      partitions (owner and start slot from a Fibonacci hash, 64-bit
-//      CAS/atomicMin on id << 32 | position, at most kClusterProbe probes).
-//      A cold id whose probe window is full falls back to its direct-mapped
-//      L2 slot; slots only go from empty to taken within a batch, so every
-//      lookup of that id makes the same choice.         -- cluster barrier
+//      (direct-mapped atomicMin after a warp match-any collapse): the L2 set
+//      then sees one insert per (CTA, hot id) instead of thousands of
+//      same-address atomics.  Colder ids go straight to L2.
+//   G  representatives: one 64-bit atomicMin (id << 32 | position) on the
+//      id's slot keeps its first position                  -- cluster barrier
 //   F  each representative reads its id's first position p_f; firsts are the
 //      representatives with p_f == own position; CTA scan; per-thread words
 //      (exclusive count << 16 | first mask) to shared memory -- cluster barrier
@@ -1067,18 +1060,11 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
 //      look-back over the lower tables (clusters are dispatched in order)
 //   E  unique index of every representative: its own rank if first, else
 //      computed from p_f and the owning thread's word (DSMEM) -- no third
-//      barrier; emit the firsts with the K2 hit/miss partition (usrc, miss
-//      queue, per-table miss counts).  The L2 set is written only where a
-//      later kernel reads it: misses are tagged (id -> unique index) when
-//      `tag` is set (pinned-host tier: k_patch_prefetch finds them there),
-//      and overflowed ids that were not tagged are emptied again.
+//      barrier and no re-read of the L2 set; emit the firsts with the K2
+//      hit/miss partition (usrc, miss queue, per-table miss counts); empty
+//      their L2 slots, or with `tag` tag the misses' (read by k_patch_prefetch)
 //   I  inverse: representatives hold their index, hot duplicates read it from
 //      shared memory
-// Global-memory traffic per batch is the ids, the inverse and the per-unique
-// outputs plus one remap word per first (SURVEY 8d's K1+K2 bytes); the set
-// itself never leaves the SMs (r01 kept it in a direct-mapped uint64[E] in
-// HBM: 32 B sectors read and written back per unique, 2.14x the algorithmic
-// bytes, profiles/r01/kaggle_ncu_full.md).
 // ===================================================================
 #ifdef EC_TRACE  // phase timestamps for tools/dedup_bench.cu only
 __device__ unsigned long long* g_trace;
@@ -1108,113 +1094,11 @@ constexpr int kClusterCtas = EC_CLUSTER_CTAS;
 #endif
 constexpr int kClusterThreads = EC_CLUSTER_THREADS;
 constexpr int kClusterMaxItems = 16;     // per thread -> n_t <= 8 * 512 * 16 = 65536
-// Shared-memory budget per CTA, measured (tools/dedup_bench, Kaggle shape):
-// the same kernel at 104 KB per CTA ran 42 us against 31 us at 64 KB, so the
-// three structures below are sized to stay near 64 KB at <= 8 items per
-// thread (two CTAs per SM) and ~112 KB at 16 (one CTA per SM).
-#ifndef EC_CL_LOCAL
-#define EC_CL_LOCAL 8192
-#endif
-#ifndef EC_CL_HOT
-#define EC_CL_HOT 32768
-#endif
-#ifndef EC_CL_LG_SMALL
-#define EC_CL_LG_SMALL 11
-#endif
-#ifndef EC_CL_LG_BIG
-#define EC_CL_LG_BIG 13
-#endif
-#ifndef EC_CL_PROBE
-#define EC_CL_PROBE 8
-#endif
-constexpr uint32_t kClusterLocal = EC_CL_LOCAL;  // ids < this: per-CTA dedup in shared memory (sval)
-constexpr uint32_t kClusterHot = EC_CL_HOT;      // ids < this: the cluster set's direct-mapped part (shot)
-constexpr int kClusterProbe = EC_CL_PROBE;       // probe window of a cold id in its hash partition
+constexpr uint32_t kClusterLocal = 16384;  // hot ids deduplicated in shared memory
 // per-table look-back word: count [0,32), CTA arrivals [32,40), inclusive flag
 constexpr unsigned long long kTabInc = 1ull << 40;
-// cold-id hash partition per CTA: 2^LG slots of 8 B.  Expected load per
-// partition: cold uniques of a table / 8 / 2^LG (Kaggle Zipf <= 0.25,
-// TB-shaped Zipf <= 0.4); fuller partitions overflow to the L2 set.
-__host__ __device__ constexpr int cluster_hash_lg(int items) { return items >= 16 ? EC_CL_LG_BIG : EC_CL_LG_SMALL; }
-__host__ __device__ constexpr size_t cluster_smem_bytes(int items) {
-  return kClusterLocal * sizeof(uint32_t)                                        // sval: per-CTA hot dedup
-         + (kClusterHot / kClusterCtas) * sizeof(uint32_t)                       // shot: cluster hot set part
-         + (static_cast<size_t>(1) << cluster_hash_lg(items)) * sizeof(unsigned long long);  // scold
-}
+__host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLocal * sizeof(uint32_t); }
 
-// Distributed shared memory through 32-bit shared::cluster addresses (mapa),
-// not generic pointers: the accesses below are ld/atom.shared::cluster.
-__device__ __forceinline__ uint32_t dsmem(const void* local, unsigned rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(local))), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ uint32_t dsmem_ld32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long dsmem_ld64(uint32_t a) {
-  unsigned long long v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void dsmem_min32(uint32_t a, uint32_t v) {
-  asm volatile("red.shared::cluster.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void dsmem_min64(uint32_t a, unsigned long long v) {
-  asm volatile("red.shared::cluster.min.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long dsmem_cas64(uint32_t a, unsigned long long cmp, unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.shared::cluster.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(v) : "memory");
-  return old;
-}
-
-// Owner CTA (top 3 bits) and start slot (next LG bits) of a cold id.
-template <int LG>
-__device__ __forceinline__ void cold_home(uint32_t id, unsigned* owner, uint32_t* slot) {
-  const uint32_t h = id * 0x9E3779B1u;
-  *owner = h >> 29;
-  *slot = (h >> (29 - LG)) & ((1u << LG) - 1);
-}
-
-// Insert (id, pos) into a cold hash partition (shared::cluster address of a
-// CTA's partition).  Returns false when the probe window holds kClusterProbe
-// other ids (the caller falls back to the L2 set).
-template <int LG>
-__device__ __forceinline__ bool cold_insert(uint32_t part, uint32_t h, uint32_t id, uint32_t pos, int k0 = 0) {
-  const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | pos;
-#pragma unroll 1
-  for (int k = k0; k < kClusterProbe; ++k) {
-    const uint32_t a = part + h * 8;
-    unsigned long long cur = dsmem_ld64(a);
-    if (cur == kEmptySlot) {
-      cur = dsmem_cas64(a, kEmptySlot, mine);
-      if (cur == kEmptySlot) return true;
-    }
-    if (static_cast<uint32_t>(cur >> 32) == id) {
-      if (static_cast<uint32_t>(cur) > pos) dsmem_min64(a, mine);
-      return true;
-    }
-    h = (h + 1) & ((1u << LG) - 1);
-  }
-  return false;
-}
-
-// First position of a cold id after every insert is done (read-only probe);
-// kEmptyKey when the id overflowed to the L2 set.
-template <int LG>
-__device__ __forceinline__ uint32_t cold_find(uint32_t part, uint32_t h, uint32_t id, int k0 = 0) {
-#pragma unroll 1
-  for (int k = k0; k < kClusterProbe; ++k) {
-    const unsigned long long cur = dsmem_ld64(part + h * 8);
-    if (static_cast<uint32_t>(cur >> 32) == id) return static_cast<uint32_t>(cur);
-    if (cur == kEmptySlot) break;
-    h = (h + 1) & ((1u << LG) - 1);
-  }
-  return kEmptyKey;
-}
 
 template <int ITEMS>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1)
@@ -1224,12 +1108,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
                     int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, int* __restrict__ ucount, int tag) {
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
-  static_assert(kClusterCtas == 8, "set partitions: owner = id & 7 (hot), top 3 hash bits (cold)");
-  constexpr int LG = cluster_hash_lg(ITEMS);
-  constexpr uint32_t kHotPart = kClusterHot / kClusterCtas;
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
-  uint32_t* const shot = sval + kClusterLocal;      // cluster hot set, this CTA's part: id >> 3 -> first position
-  unsigned long long* const scold = reinterpret_cast<unsigned long long*>(shot + kHotPart);  // cold hash partition
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
   __shared__ int s_total, s_base, s_pref[kClusterCtas];
   __shared__ int sw[kClusterThreads / 32];
@@ -1252,19 +1131,11 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   uint32_t id[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) id[j] = j < my ? __ldcs(indices + tb.base + p0 + j) : kEmptyKey;
-  {  // clear the hot-id slots and this CTA's parts of the set (while the ids are in flight)
+  {  // clear the hot-id slots (while the ids are in flight)
     uint4* s4 = reinterpret_cast<uint4*>(sval);
     const uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
     for (uint32_t i = threadIdx.x; i < (nloc + 3) / 4; i += kClusterThreads) s4[i] = e;
-    uint4* h4 = reinterpret_cast<uint4*>(shot);
-    for (uint32_t i = threadIdx.x; i < kHotPart / 4; i += kClusterThreads) h4[i] = e;
-    if (tb.rows > kClusterHot) {  // only tables with cold ids use the hash partitions
-      uint4* c4 = reinterpret_cast<uint4*>(scold);
-      for (uint32_t i = threadIdx.x; i < (1u << LG) / 2; i += kClusterThreads) c4[i] = e;
-    }
   }
-  // peers insert into this CTA's parts after the cluster barrier's wait (phase G)
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   __syncthreads();
   EC_TRACE_AT(1);
 
@@ -1283,92 +1154,23 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   __syncthreads();
   EC_TRACE_AT(2);
 
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every part of the set is cleared
-
-  // ---- G: representatives insert into the cluster's set (DSMEM).  Hot ids:
-  // fire-and-forget min-reductions.  Cold ids: the first probe of kGrp items
-  // is issued as one CAS each before any result is examined (one DSMEM round
-  // trip per group, not per item); collisions continue probing one by one.
-  constexpr int kGrp = 4;
+  // ---- G: representatives insert into the direct-mapped L2 set
   uint32_t rep = 0;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const bool r = id[j] < nloc ? sval[id[j]] == static_cast<uint32_t>(p0 + j) : id[j] != kEmptyKey;
-    if (r) rep |= 1u << j;
-  }
-#pragma unroll
-  for (int j0 = 0; j0 < ITEMS; j0 += kGrp) {
-    unsigned long long cur[kGrp];
-    uint32_t home[kGrp];  // partition base (shared::cluster address), 0 = no cold insert
-#pragma unroll
-    for (int k = 0; k < kGrp && j0 + k < ITEMS; ++k) {
-      const int j = j0 + k;
-      home[k] = 0;
-      cur[k] = 0;
-      if (!((rep >> j) & 1)) continue;
-      const uint32_t pos = static_cast<uint32_t>(p0 + j);
-      if (id[j] < kClusterHot) {
-        dsmem_min32(dsmem(shot + (id[j] >> 3), id[j] & 7), pos);
-      } else {
-        unsigned o;
-        uint32_t h;
-        cold_home<LG>(id[j], &o, &h);
-        home[k] = dsmem(scold, o);
-        cur[k] = dsmem_cas64(home[k] + h * 8, kEmptySlot, (static_cast<unsigned long long>(id[j]) << 32) | pos);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kGrp && j0 + k < ITEMS; ++k) {
-      const int j = j0 + k;
-      if (!home[k] || cur[k] == kEmptySlot) continue;  // none, or inserted
-      const uint32_t pos = static_cast<uint32_t>(p0 + j);
-      unsigned o;
-      uint32_t h;
-      cold_home<LG>(id[j], &o, &h);
-      if (static_cast<uint32_t>(cur[k] >> 32) == id[j]) {
-        if (static_cast<uint32_t>(cur[k]) > pos)
-          dsmem_min64(home[k] + h * 8, (static_cast<unsigned long long>(id[j]) << 32) | pos);
-      } else if (!cold_insert<LG>(home[k], (h + 1) & ((1u << LG) - 1), id[j], pos, 1)) {
-        atomicMin(tb.hash + id[j], (static_cast<unsigned long long>(id[j]) << 32) | pos);
-      }
+    if (r) {
+      rep |= 1u << j;
+      atomicMin(tb.hash + id[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p0 + j));
     }
   }
   EC_TRACE_AT(3);
   cluster.sync();  // every insert of this table is done
 
-  // ---- F: first positions (all first probes in flight); firsts; CTA scan
-  uint32_t pf[ITEMS], first = 0, ovf = 0;
-  unsigned long long fw[ITEMS];
+  // ---- F: first positions; firsts; CTA scan
+  uint32_t pf[ITEMS], first = 0;
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    fw[j] = 0;
-    pf[j] = 0;
-    if (!((rep >> j) & 1)) continue;
-    if (id[j] < kClusterHot) {
-      pf[j] = dsmem_ld32(dsmem(shot + (id[j] >> 3), id[j] & 7));
-    } else {
-      unsigned o;
-      uint32_t h;
-      cold_home<LG>(id[j], &o, &h);
-      fw[j] = dsmem_ld64(dsmem(scold, o) + h * 8);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    if (!((rep >> j) & 1) || id[j] < kClusterHot) continue;
-    if (static_cast<uint32_t>(fw[j] >> 32) == id[j]) {
-      pf[j] = static_cast<uint32_t>(fw[j]);
-      continue;
-    }
-    unsigned o;
-    uint32_t h;
-    cold_home<LG>(id[j], &o, &h);
-    pf[j] = fw[j] == kEmptySlot ? kEmptyKey : cold_find<LG>(dsmem(scold, o), (h + 1) & ((1u << LG) - 1), id[j], 1);
-    if (pf[j] == kEmptyKey) {  // overflowed: the L2 slot holds it
-      ovf |= 1u << j;
-      pf[j] = static_cast<uint32_t>(__ldcg(tb.hash + id[j]));
-    }
-  }
+  for (int j = 0; j < ITEMS; ++j) pf[j] = ((rep >> j) & 1) ? static_cast<uint32_t>(__ldcg(tb.hash + id[j])) : 0u;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j)
     if (((rep >> j) & 1) && pf[j] == static_cast<uint32_t>(p0 + j)) first |= 1u << j;
@@ -1473,10 +1275,11 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
       utab[g] = static_cast<uint16_t>(t);
       usrc[g] = rm[j];  // cache row, or -1: a miss iff the id is not cached (core/src/simulator.cpp:99)
       if (rm[j] < 0) missm |= 1u << j;
-      if (tag && rm[j] < 0)
-        tb.hash[id[j]] = (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g;  // for k_patch_prefetch
-      else if ((ovf >> j) & 1)
-        tb.hash[id[j]] = kEmptySlot;  // every read of the slot was before the second cluster barrier
+      // the set is left holding only what a later kernel reads: with `tag`
+      // (pinned-host tier) each miss's unique index for k_patch_prefetch; every
+      // other slot goes back to empty here (every read of it was before the
+      // second cluster barrier), so the pool's reset tail touches misses only
+      tb.hash[id[j]] = tag && rm[j] < 0 ? (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g : kEmptySlot;
     }
     // miss queue: one atomic per warp
     const int nm = __popc(missm);
