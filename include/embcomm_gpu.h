@@ -292,12 +292,13 @@ void ec_tables_destroy(ec_tables t);
 /* bytes of device / pinned-host memory held */
 int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
 /* Per-kernel CUDA-event timing of ec_lookup_fwd/bwd (events on the launching
- * streams; CUDA graphs are bypassed while enabled).  Slots (11): 0 k_insert,
+ * streams; CUDA graphs are bypassed while enabled).  Slots (12): 0 k_insert,
  * 1 k_compact (K1), 2 k_inverse_partition (K1 inverse + K2), 3 k_gather (K3
  * HBM), 4 k_gather_host (K3 pinned host, side stream), 5 exchange (K4),
  * 6 k_pool (K5), 7 k_scatter (K6a), 8 k_apply (K6b), 9 k_apply_host (K6b
  * pinned host, side stream), 10 k_dedup_cluster (K1+K2, one cluster per
- * table).  profile_read returns accumulated ms and call counts per slot (11
+ * table), 11 k_g64_misses (K6 pinned-host misses' fp64 sums, fused path).
+ * profile_read returns accumulated ms and call counts per slot (12
  * entries) and the number of kernels the engine launched; reset != 0 clears
  * them. */
 int ec_tables_profile(ec_tables t, int enable);

@@ -899,12 +899,12 @@ void Engine::join_host_writes(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
-  if (fused()) {
-    // w - lr * sum(g) per cache / HBM row; host misses' sums into ugrad
-    PhaseScope ph(prof, kPhaseApply, st);
-    k_apply_g64<VEC><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p,
-                                                      bb[cur].counted ? ucount.p : nullptr, cache.p, ugrad.p, g64.p, lr,
-                                                      host ? 0 : 1);
+  if (fused() && host) {
+    // the misses' gradients first (heavy ones' fp64 sums into ugrad): the host
+    // write-back starts at ev_grad, right after, and overlaps k_apply_g64
+    PhaseScope ph(prof, kPhaseG64Misses, st);
+    k_g64_misses<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, missq.p,
+                                                             bb[cur].counted ? ucount.p : nullptr, ugrad.p, g64.p);
     launched();
   }
   if (host) {
@@ -917,6 +917,14 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     else
       EC_CUDA(cudaEventRecord(ev_grad, st));
     if (world > 1) enqueue_host_writeback<VEC>(lr);
+  }
+  if (fused()) {
+    // w - lr * sum(g) per cache / HBM row (one rounding for heavy rows)
+    PhaseScope ph(prof, kPhaseApply, st);
+    k_apply_g64<VEC><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p,
+                                                      bb[cur].counted ? ucount.p : nullptr, cache.p, ugrad.p, g64.p, lr,
+                                                      host ? 0 : 1);
+    launched();
   }
   if (!fused()) {
     PhaseScope ph(prof, kPhaseApply, st);
@@ -1372,7 +1380,7 @@ NvtxRange::~NvtxRange() { nvtxRangePop(); }
 const char* phase_name(int phase) {
   static const char* const names[kNumPhases] = {"ec:insert",  "ec:compact", "ec:inverse_partition", "ec:gather",
                                                 "ec:gather_host", "ec:exchange", "ec:pool", "ec:scatter",
-                                                "ec:apply", "ec:apply_host", "ec:dedup_cluster"};
+                                                "ec:apply", "ec:apply_host", "ec:dedup_cluster", "ec:g64_misses"};
   return phase >= 0 && phase < kNumPhases ? names[phase] : "ec:?";
 }
 

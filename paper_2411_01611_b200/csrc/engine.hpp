@@ -111,7 +111,7 @@ struct BatchBufs {
 
 // One timing slot per kernel of the batch pipeline (ec_tables_profile_read order).
 enum { kPhaseInsert = 0, kPhaseCompact, kPhaseInversePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange,
-       kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kPhaseDedupCluster, kNumPhases };
+       kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kPhaseDedupCluster, kPhaseG64Misses, kNumPhases };
 
 // Optional per-phase CUDA-event timing on the launching streams.
 struct Profiler {

@@ -842,10 +842,52 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
   }
 }
 
+// Fused single-rank SGD, pinned-host tier, first: the misses' gradients for
+// the host write-back.  A miss heavier than kLightAdds gets its fp64 sum
+// rounded once into ugrad; every miss's count and sums are left zeroed.  Walks
+// the miss queue (M entries, not U), so the host write-back that waits for it
+// starts early while k_apply_g64 updates the cached rows beside it.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_g64_misses(int T, const int* __restrict__ ctr,
+                                                         const uint32_t* __restrict__ missq, int* __restrict__ ucount,
+                                                         float* __restrict__ ugrad, double* __restrict__ g64) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  constexpr int R = 4;
+  const RowMap<VEC> m;
+  const int nm = *counters(const_cast<int*>(ctr), T).miss_total;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q0 = warp * RPW * R; q0 < nm; q0 += nwarps * RPW * R) {
+    uint32_t g[R];
+    int n[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = q0 + r * RPW + m.sub;
+      g[r] = q < nm ? missq[q] : kInvalidSlot;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) n[r] = g[r] == kInvalidSlot ? 0 : ucount ? __ldcg(ucount + g[r]) : kLightAdds + 1;
+    __syncwarp();  // every lane of a row read its count before lane 0 clears it
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (g[r] == kInvalidSlot) continue;
+      if (ucount && m.c == 0) ucount[g[r]] = 0;
+      if (n[r] <= kLightAdds) continue;
+      double gs[4];
+      take_g64<VEC>(g64, g[r], m.c, gs);
+      float* dst = ugrad + static_cast<int64_t>(g[r]) * D + m.c * 4;
+      const float4 w = *reinterpret_cast<const float4*>(dst);
+      st4(dst, make_float4(static_cast<float>(w.x + gs[0]), static_cast<float>(w.y + gs[1]),
+                           static_cast<float>(w.z + gs[2]), static_cast<float>(w.w + gs[3])));
+    }
+  }
+}
+
 // Fused single-rank SGD, second half: rows heavier than kLightAdds (their
 // partials went to g64) get w - lr * sum(g64) with one rounding (cache row,
-// or the HBM shard row of a miss); pinned-host misses get the sum in ugrad for
-// the host write-back.  Leaves g64 and ucount zeroed.
+// or the HBM shard row of a miss).  Pinned-host misses are k_g64_misses' (and
+// skipped here).  Leaves g64 and ucount zeroed.
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                                                         const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
@@ -861,15 +903,18 @@ __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restri
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
     int n[R];
+    bool own[R];  // not a pinned-host miss (those are k_g64_misses')
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = g0 + r * RPW + m.sub;
-      n[r] = g < U ? (ucount ? __ldcg(ucount + g) : kLightAdds + 1) : 0;
+      own[r] = g < U && (local_hbm || usrc[g] >= 0);
+      n[r] = own[r] ? (ucount ? __ldcg(ucount + g) : kLightAdds + 1) : 0;
     }
+    __syncwarp();
     if (ucount && m.c == 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (g0 + r * RPW + m.sub < U) ucount[g0 + r * RPW + m.sub] = 0;
+        if (own[r]) ucount[g0 + r * RPW + m.sub] = 0;
     }
     double gs[R][4];
     float* dst[R];
@@ -881,22 +926,13 @@ __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restri
       if (n[r] <= kLightAdds) continue;
       take_g64<VEC>(g64, g, m.c, gs[r]);
       const int32_t s = usrc[g];
-      dst[r] = s >= 0 ? cache + static_cast<int64_t>(s) * D
-             : local_hbm ? td[utab[g]].store + static_cast<int64_t>(uniq[g]) * D
-                         : ugrad + static_cast<int64_t>(g) * D;
+      dst[r] = s >= 0 ? cache + static_cast<int64_t>(s) * D : td[utab[g]].store + static_cast<int64_t>(uniq[g]) * D;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) w[r] = dst[r] ? *reinterpret_cast<const float4*>(dst[r] + m.c * 4) : float4{};
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (!dst[r]) continue;
-      const int g = g0 + r * RPW + m.sub;
-      if (dst[r] == ugrad + static_cast<int64_t>(g) * D)  // pinned-host miss: its gradient for the write-back
-        st4(dst[r] + m.c * 4, make_float4(static_cast<float>(w[r].x + gs[r][0]), static_cast<float>(w[r].y + gs[r][1]),
-                                          static_cast<float>(w[r].z + gs[r][2]), static_cast<float>(w[r].w + gs[r][3])));
-      else
-        st4(dst[r] + m.c * 4, sgd4(w[r], gs[r], lr));
-    }
+    for (int r = 0; r < R; ++r)
+      if (dst[r]) st4(dst[r] + m.c * 4, sgd4(w[r], gs[r], lr));
   }
 }
 
