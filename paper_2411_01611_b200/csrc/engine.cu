@@ -170,6 +170,12 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
 }
 
 // ------------------------------------------------------------ host side
+// Largest table (rows) whose dedup set is direct-mapped (slot = id) even when
+// it exceeds the hash capacity; EC_DIRECT_ROWS overrides (read at creation).
+static uint64_t direct_rows_limit() {
+  const char* v = std::getenv("EC_DIRECT_ROWS");
+  return v && *v ? std::strtoull(v, nullptr, 10) : Engine::kDirectRows;
+}
 static int persistent_grid(int device) { return sm_count(device) * 8; }
 // Row kernels share the SMs with the side-stream host-link kernels: size the
 // main grids so every CTA stays resident beside them.
@@ -350,24 +356,18 @@ void Engine::create(const ec_tables_config& c) {
   local_rows.resize(T);
   store_off.assign(T + 1, 0);
   remap_off.assign(T + 1, 0);
-  hash_off.assign(T + 1, 0);
-  hash_lg.resize(T);
-  hash_direct.resize(T);
-  uint64_t direct_bytes = 0;
   for (uint32_t t = 0; t < T; ++t) {
     if (rows[t] < 1 || rows[t] > 0xFFFFFFFFull) invalid("table " + std::to_string(t) + " rows out of [1, 2^32-1]");
     local_rows[t] = rows[t] > static_cast<uint64_t>(rank) ? (rows[t] - rank + world - 1) / world : 0;
     store_off[t + 1] = store_off[t] + local_rows[t];
     remap_off[t + 1] = remap_off[t] + rows[t];
-    hash_lg[t] = std::max<uint32_t>(5, log2_ceil(2 * std::min<uint64_t>(max_n, rows[t])));
-    // small tables: one slot per id (no hashing, no probing, one atomic per insert)
-    hash_direct[t] = rows[t] <= std::max<uint64_t>(1ull << hash_lg[t], kDirectRows) &&
-                             direct_bytes + rows[t] * 16 <= kDirectBudget
-                         ? 1
-                         : 0;
-    if (hash_direct[t]) direct_bytes += rows[t] * 16;  // both buffer sets
-    hash_off[t + 1] = hash_off[t] + (hash_direct[t] ? rows[t] : (1ull << hash_lg[t]));
   }
+  // large tables get direct-mapped sets where the cluster dedup kernel will run
+  // (it needs them; batches of <= kAutoClusterN lookups per table), hashed ones
+  // where the tile path will (TB shape 0.395 -> 0.379 ms, cfg1 0.200 -> 0.187:
+  // a 2^17-slot set stays in L2, a 40M-row direct one costs a DRAM sector per
+  // probe in each of k_insert, k_compact, k_inverse_partition)
+  plan_sets(max_n <= kAutoClusterN);
   const uint64_t store_elems = store_off[T] * D;
   if (storage == EC_STORAGE_HBM) {
     store_dev.alloc(store_elems);
@@ -380,12 +380,7 @@ void Engine::create(const ec_tables_config& c) {
   }
   remap.alloc(remap_off[T]);
   EC_CUDA(cudaMemset(remap.p, 0xFF, remap.bytes()));
-  // one dedup hash per batch-buffer set: a prefetched batch's dedup never
-  // waits for the current batch's gather to clean the shared slots
-  hash.alloc(kSets * hash_off[T]);
-  EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
-  idcnt.alloc(kSets * hash_off[T]);
-  EC_CUDA(cudaMemset(idcnt.p, 0, idcnt.bytes()));
+  alloc_sets();
   const uint64_t N = max_n * T;
   const uint64_t max_tiles = T * ((max_n + kTile - 1) / kTile) + T;
   for (BatchBufs& b : bb) {
@@ -426,18 +421,14 @@ void Engine::create(const ec_tables_config& c) {
   td_host.resize(T);
   for (uint32_t t = 0; t < T; ++t) {
     TableDev& d = td_host[t];
-    d.hash = hash.p + hash_off[t];
-    d.shift = 32 - hash_lg[t];
-    d.mask = static_cast<uint32_t>((1ull << hash_lg[t]) - 1);
-    d.direct = hash_direct[t];
     d.pad_ = 0;
-    d.idcnt = idcnt.p + hash_off[t];
     d.remap = remap.p + remap_off[t];
     d.store = store_base + store_off[t] * D;
     d.rows = rows[t];
     d.base = 0;
     d.n = 0;
   }
+  set_views();
   upload_tdev();
   select(cur);
   EC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -452,6 +443,63 @@ void Engine::create(const ec_tables_config& c) {
   EC_CUDA(cudaEventCreateWithFlags(&ev_part, cudaEventDisableTiming));
   EC_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   EC_CUDA(cudaDeviceSynchronize());
+}
+
+// Per table: hashed (open addressing, pow2 >= 2 * min(max lookups, rows)
+// slots) or direct-mapped (slot = id) dedup set.  Tables that fit the hash
+// capacity are always direct (no probing, one atomic per insert); larger ones
+// up to direct_rows_limit() rows when `direct_big`, within kDirectBudget.
+void Engine::plan_sets(bool direct_big) {
+  hash_off.assign(T + 1, 0);
+  hash_lg.resize(T);
+  hash_direct.resize(T);
+  uint64_t direct_bytes = 0;
+  for (uint32_t t = 0; t < T; ++t) {
+    hash_lg[t] = std::max<uint32_t>(5, log2_ceil(2 * std::min<uint64_t>(max_n, rows[t])));
+    const uint64_t lim = std::max<uint64_t>(1ull << hash_lg[t], direct_big ? direct_rows_limit() : 0);
+    hash_direct[t] = rows[t] <= lim && direct_bytes + rows[t] * 12 * kSets <= kDirectBudget ? 1 : 0;
+    if (hash_direct[t]) direct_bytes += rows[t] * 12 * kSets;  // hash + idcnt, every buffer set
+    hash_off[t + 1] = hash_off[t] + (hash_direct[t] ? rows[t] : (1ull << hash_lg[t]));
+  }
+}
+
+// One dedup set per batch-buffer set: a prefetched batch's dedup never waits
+// for the current batch's gather to clean the shared slots.
+void Engine::alloc_sets() {
+  hash.alloc(kSets * hash_off[T]);
+  EC_CUDA(cudaMemset(hash.p, 0xFF, hash.bytes()));
+  idcnt.alloc(kSets * hash_off[T]);
+  EC_CUDA(cudaMemset(idcnt.p, 0, idcnt.bytes()));
+}
+
+void Engine::set_views() {
+  for (uint32_t t = 0; t < T; ++t) {
+    TableDev& d = td_host[t];
+    d.hash = hash.p + hash_off[t];
+    d.shift = 32 - hash_lg[t];
+    d.mask = static_cast<uint32_t>((1ull << hash_lg[t]) - 1);
+    d.direct = hash_direct[t];
+    d.idcnt = idcnt.p + hash_off[t];
+  }
+}
+
+// Dedup modes 2 / 3 run kernels that need every set direct-mapped: re-lay the
+// sets out (between batches; pending prefetches dropped) when some are hashed.
+void Engine::require_direct_sets() {
+  bool all = true;
+  for (uint32_t t = 0; t < T; ++t) all = all && hash_direct[t];
+  if (all) return;
+  use_device(device);
+  EC_CUDA(cudaDeviceSynchronize());
+  drop_prefetch(nullptr);
+  EC_CUDA(cudaDeviceSynchronize());
+  plan_sets(true);
+  alloc_sets();
+  set_views();
+  upload_tdev();
+  select(cur);
+  have_geom = false;  // per-batch descriptors are re-uploaded with the next geometry
+  clear_graphs();
 }
 
 void Engine::upload_tdev() {
@@ -771,6 +819,7 @@ template <int VEC>
 void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   PhaseScope ph(prof, kPhaseScatter, st);
   fold_g64 = false;
+  direct_apply = false;
   if (fused()) {
     // -lr * grad scattered straight into the cache / HBM rows (SGD in the
     // scatter) for a row's first kLightAdds partials, the rest summed in fp64
@@ -798,8 +847,15 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
     return;
   }
   if (!ntiles) return;
+  // single rank, HBM rows: k_apply is ugrad's only consumer, so runs inside one
+  // chunk are applied by k_bwd_reduce itself (TB shape: k_apply 76 -> see DESIGN)
+  const DirectApply ap = world == 1 && !in_group && storage == EC_STORAGE_HBM
+                             ? DirectApply{urows.p, usrc.p, uniq.p, utab.p, tdev.p, cache.p, bwd_lr}
+                             : DirectApply{};
+  direct_apply = ap.urows != nullptr;
   if (bb[cur].lists) {  // the forward grouped the lookups already (tile path)
-    k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
+    k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p,
+                                                       ap);
     launched();
     finalize_transpose<VEC>(st);
     return;
@@ -817,7 +873,8 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
   k_bwd_fill<<<tgrid, kThreads, 0, st>>>(tiles.p, ntiles, tdev.p, bag_off, static_cast<int>(T), static_cast<int>(geom_b),
                                          static_cast<int>(geom_p), inv.p, off.p, cnt.p, list.p);
   launched();
-  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p);
+  k_bwd_reduce<VEC><<<row_grid(), kThreads, 0, st>>>(off.p, ctr.p, static_cast<int>(T), list.p, grad, ugrad.p, g64.p,
+                                                     ap);
   launched();
   finalize_transpose<VEC>(st);
 }
@@ -930,7 +987,7 @@ void Engine::bwd_apply_local(float lr, cudaStream_t st) {
     PhaseScope ph(prof, kPhaseApply, st);
     k_apply<VEC, 4><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, ctr.p, uniq.p, utab.p, usrc.p, urows.p, ugrad.p, lr,
                                                      cache.p, world == 1 ? 1 : 0, host ? 0 : 1, rank, world,
-                                                     fold_g64 ? off.p : nullptr, g64.p);
+                                                     fold_g64 ? off.p : nullptr, g64.p, direct_apply ? 1 : 0);
     launched();
   }
   if (host && world > 1) join_host_writes(st);
@@ -1517,6 +1574,7 @@ int ec_tables_dedup_mode(ec_tables t, int mode) {
     if (mode < 0 || mode > 3)
       invalid("dedup mode: 0 auto, 1 tiles, 2 cluster per table, 3 one CTA per table (when it fits)");
     Engine& e = E(t);
+    if (mode == 2 || mode == 3) e.require_direct_sets();
     e.dedup_mode = mode;
     e.clear_graphs();
   });

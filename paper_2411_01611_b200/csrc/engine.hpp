@@ -182,6 +182,7 @@ struct Engine {
   // rows, within a total budget; the cluster dedup kernel needs it
   static constexpr uint64_t kDirectRows = 1ull << 27;
   static constexpr uint64_t kDirectBudget = 16ull << 30;
+  static constexpr uint64_t kAutoClusterN = 32768;  // auto cluster dedup up to this many lookups per table
 
   DevBuf<float> store_dev;
   float* store_host = nullptr;  // pinned, mapped
@@ -304,6 +305,10 @@ struct Engine {
   int host_grid() const;
   static bool host_tma();
   void upload_tdev();
+  void plan_sets(bool direct_big);
+  void alloc_sets();
+  void set_views();
+  void require_direct_sets();
   int host_write_grid() const;
   int row_grid() const;
   void init_synthetic(uint64_t seed, float scale, cudaStream_t st);
@@ -319,6 +324,7 @@ struct Engine {
   template <int VEC> void bwd_scatter(const float* grad, cudaStream_t st);
   template <int VEC> void finalize_transpose(cudaStream_t st);
   bool fold_g64 = false;  // k_apply reads the fp64 sums of chunk-spanning rows itself
+  bool direct_apply = false;  // k_bwd_reduce applied the rows whose runs fit one chunk
   template <int VEC> void bwd_apply_local(float lr, cudaStream_t st);
   template <int VEC> void enqueue_host_writeback(float lr);
   void join_host_writes(cudaStream_t st);

@@ -944,7 +944,8 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
                                                     const int32_t* __restrict__ usrc, const float* __restrict__ urows,
                                                     const float* __restrict__ ugrad, float lr, float* __restrict__ cache,
                                                     int hits, int misses_local, int rank, int world,
-                                                    const int* __restrict__ off = nullptr, double* __restrict__ g64 = nullptr) {
+                                                    const int* __restrict__ off = nullptr, double* __restrict__ g64 = nullptr,
+                                                    int skip_sole = 0) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -956,6 +957,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(const TableDev* __restrict__
     for (int r = 0; r < R; ++r) {
       const int g = g0 + r * RPW + m.sub;
       if (g >= U) continue;
+      if (skip_sole && chunk_span(off[g], off[g + 1]) == 1) continue;  // k_bwd_reduce applied it
       const int32_t s = usrc[g];
       float* dst = nullptr;
       if (s >= 0) {
@@ -1677,11 +1679,25 @@ __global__ void __launch_bounds__(kThreads) k_bwd_fill(const Tile* __restrict__ 
   }
 }
 
+// Single rank, HBM rows (`ap.urows` set): a run wholly inside one chunk is the
+// row's whole gradient, so the SGD update w - lr * g is written straight to its
+// cache / HBM row here (the arithmetic k_apply would do, bit for bit) and
+// k_apply only handles rows whose runs cross a chunk edge.
+struct DirectApply {
+  const float* urows;  // null: store sums in ugrad
+  const int32_t* usrc;
+  const uint32_t* uniq;
+  const uint16_t* utab;
+  const TableDev* td;
+  float* cache;
+  float lr;
+};
+
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
                                                          const uint2* __restrict__ list,
                                                          const float* __restrict__ grad, float* __restrict__ ugrad,
-                                                         double* __restrict__ g64) {
+                                                         double* __restrict__ g64, DirectApply ap = {}) {
   constexpr int D = VEC * 4;
   const RowMap<VEC> m;
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
@@ -1702,7 +1718,13 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
       const float4 a = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
                                    static_cast<float>(acc[2]), static_cast<float>(acc[3]));
       float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
-      if (!spans) st4(dst, a);
+      if (!spans && ap.urows) {
+        const int32_t sr = ap.usrc[cu];
+        float* row = sr >= 0 ? ap.cache + static_cast<int64_t>(sr) * D
+                             : ap.td[ap.utab[cu]].store + static_cast<int64_t>(ap.uniq[cu]) * D;
+        const float4 w = ldg4(ap.urows + static_cast<int64_t>(cu) * D + m.c * 4);
+        st4(row + m.c * 4, make_float4(w.x - ap.lr * a.x, w.y - ap.lr * a.y, w.z - ap.lr * a.z, w.w - ap.lr * a.w));
+      } else if (!spans) st4(dst, a);
       else if (chunk_span(off[cu], off[cu + 1]) > kLightAdds) red_g64<VEC>(g64, cu, m.c, acc[0], acc[1], acc[2], acc[3]);
       else atomicAdd(reinterpret_cast<float4*>(dst), a);
     };
