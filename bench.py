@@ -262,10 +262,15 @@ def phase_bytes(st, wl, T, fused=False):
         "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out
         "k_gather": U * 4 + hbm_src * row + U * row + U * row,       # usrc in, rows in, urows out, ugrad zeroed
         "k_gather_host": host_rows * (4 + row + row),  # missq in, host rows in (host link), urows out
-        # A_pool (rows read from the compact, L2-resident copy), or
-        # A_fused when the pool reads each unique row at its source (no K3 gather)
-        "k_pool": (U * 4 + U * row + n * 4 + B * T * row) if fused else (n * 4 + n * row + B * T * row),
-        "k_scatter": B * T * row + n * 4 + n * 4 + n * row,  # grads in, inverse + counts in, row-grad reductions
+        # compulsory bytes only (a row read twice counts once): A_fused (SURVEY
+        # 8d) when the pool reads each unique row at its source; on the gathering
+        # path the compact copy's U rows (SURVEY's A_pool also counts the n row
+        # reads, which hit L2 and can exceed the HBM peak)
+        "k_pool": U * 4 + U * row + n * 4 + B * T * row if fused else U * row + n * 4 + B * T * row,
+        # bag gradients in once, inverse (or grouped list) + counts, each unique
+        # row's update read and written once (its cache / HBM row, or urows in
+        # and the row out); the per-lookup partial sums stay in registers / L2
+        "k_scatter": B * T * row + n * 4 + n * 4 + 2 * U * row,
         # fused path (k_apply_g64): per-unique counts read and cleared; the
         # rows past 64 lookups (not counted here) get their fp64 sums applied
         "k_apply": U * 8 if fused else (U - host_rows) * (4 + row * 3),  # else: usrc, urows, ugrad in, rows out
