@@ -435,13 +435,14 @@ def run_ours(args, wl):
     host_ptr = [t.data_ptr() for t in host_ids]
     cs_ptr = copy_stream.cuda_stream
     lib = ec._native.lib()
-    copy_fn = (lambda d, s: lib.ec_copy_async_pull(d, s, nbytes_ids, pull, cs_ptr)) if pull else \
-        (lambda d, s: lib.ec_copy_async(d, s, nbytes_ids, cs_ptr))
+    copy_path = {"ctas": pull}
 
     def h2d(k):  # step k's ids, pinned host -> device, on the copy stream
         if k >= NS:  # the slot's previous batch was consumed by its forward
             copy_stream.wait_event(consumed[k % NS])
-        rc = copy_fn(dev_ptr[k % NS], host_ptr[k % N_BATCHES])
+        ctas = copy_path["ctas"]
+        rc = (lib.ec_copy_async_pull(dev_ptr[k % NS], host_ptr[k % N_BATCHES], nbytes_ids, ctas, cs_ptr) if ctas
+              else lib.ec_copy_async(dev_ptr[k % NS], host_ptr[k % N_BATCHES], nbytes_ids, cs_ptr))
         if rc:
             ec._native.check(rc)
         copied[k % NS].record(copy_stream)
@@ -491,6 +492,23 @@ def run_ours(args, wl):
         return res
 
     e2e_steps(max(args.warmup, 12))  # untimed: captures the graphs of this buffer rotation
+    # input path by trial inside the real loop, untimed: the isolated probe
+    # above does not see how each path shares the host link with the step's
+    # own row traffic, and that varies across this pool's boxes (e2e 0.11 vs
+    # 0.19 ms with the same probe numbers)
+    trial = {}
+    cands = [pull, 0 if pull else 8] if world == 1 else [pull]  # (ranks must agree: N>1 keeps the probe's pick)
+    for ctas in cands:
+        copy_path["ctas"] = ctas
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        e2e_steps(24)
+        b.record(stream)
+        torch.cuda.synchronize()
+        trial[ctas] = a.elapsed_time(b) / 24
+    pull = copy_path["ctas"] = min(cands, key=lambda c: trial[c])
+    H2D_PROBE["in_loop_trial_ms"] = {(f"pull{c}" if c else "copy_engine"): round(v, 5) for c, v in trial.items()}
     barrier()
     torch.cuda.synchronize()
     torch.cuda._sleep(HEAD_START_CYCLES)
