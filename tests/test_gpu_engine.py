@@ -299,6 +299,36 @@ def test_config2_kaggle_shape_training_step(ec, torch, storage):
     run_training_step(ec, torch, KAGGLE, 16, 16384, 1, storage, 256 << 20, 909)
 
 
+@pytest.mark.parametrize("cache_bytes", [0, 64 * 16 * 4])
+def test_host_tier_heavy_misses_training_step(ec, torch, cache_bytes):
+    """Pinned-host misses with thousands of lookups each (no cache, or a
+    64-row one, over small Zipf tables): their gradients take the fp64 path
+    and are rounded once by k_g64_misses before the host write-back."""
+    run_training_step(ec, torch, [1000, 50, 200000, 3], 16, 16384, 1, "host", cache_bytes, 4711)
+
+
+def test_dedup_mode_switch_relays_sets_out(ec, torch, ref):
+    """Tables sized for the tile path get hashed sets for their large tables;
+    forcing the cluster kernel re-lays them out direct-mapped, and going back
+    to tiles keeps working: sets, inverse, hit/miss and rows vs the oracle."""
+    rows = [3, 24, 5000, 142572, 10131227]
+    n_max = 40000  # > the auto-cluster bound: hashed sets for the two large tables
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    caches = [d.top_ids(k) for d, k in zip(dists, [1, 0, 100, 1000, 20000])]
+    D, B, P = 8, 40000, 1
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=n_max, max_batch_size=B)
+    tab.init_synthetic(4, 0.5)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [n_max] * len(rows), 77)
+    ids_h = ids.cpu().numpy().view(np.uint32)
+    for mode in ["auto", "cluster", "tiles", "cluster"]:
+        tab.dedup_mode(mode)
+        out = tab.forward(ids, offs, B, P)
+        check_batch(ec, tab, ids_h, offs, caches, rows, D, 4, 0.5, P=P, B=B, out=out, ref=ref)
+        tab.backward(torch.zeros(B, len(rows) * D, device="cuda"), 0.0)
+    tab.close()
+
+
 @pytest.mark.parametrize("scatter", [None, "atomic"])
 def test_config1_full_size_training_step(ec, torch, scatter):
     """configs[0] at full size (8 x 1M rows, D=64, b=4096, P=20, no cache, as
