@@ -275,7 +275,7 @@ def phase_bytes(st, wl, T, fused=False):
         # rows past 64 lookups (not counted here) get their fp64 sums applied
         "k_apply": U * 8 if fused else (U - host_rows) * (4 + row * 3),  # else: usrc, urows, ugrad in, rows out
         "k_apply_host": host_rows * (4 + row * 3),
-        "k_g64_misses": host_rows * 8,                 # miss queue + per-unique counts (heavy rows' sums: rare)
+        "k_clear_miss_sums": U * 4,                    # the last batch's per-unique counts (heavy rows' sums: rare)
     }
 
 

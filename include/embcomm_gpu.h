@@ -297,7 +297,8 @@ int ec_tables_memory(ec_tables t, uint64_t* device_bytes, uint64_t* host_bytes);
  * HBM), 4 k_gather_host (K3 pinned host, side stream), 5 exchange (K4),
  * 6 k_pool (K5), 7 k_scatter (K6a), 8 k_apply (K6b), 9 k_apply_host (K6b
  * pinned host, side stream), 10 k_dedup_cluster (K1+K2, one cluster per
- * table), 11 k_g64_misses (K6 pinned-host misses' fp64 sums, fused path).
+ * table), 11 k_clear_miss_sums (per-unique counts and heavy rows' fp64
+ * sums a set's last batch left, cleared before its next counting dedup).
  * profile_read returns accumulated ms and call counts per slot (12
  * entries) and the number of kernels the engine launched; reset != 0 clears
  * them. */

@@ -905,6 +905,9 @@ void Engine::enqueue_host_writeback(float lr) {
   const bool patch = h >= 0 && bb[h].gathered;
   const BatchBufs& nx = bb[patch ? h : cur];
   const TableDev* nxt_td = tdev_buf.p + static_cast<size_t>(patch ? h : cur) * T;
+  // fused path: heavy misses' gradients are read from the fp64 sums (miss_sgd)
+  const double* sums = fused() && bb[cur].counted ? g64.p : nullptr;
+  const int* cnts = sums ? ucount.p : nullptr;
   if (patch && host_tma()) {
     // one kernel writes the rows back and refreshes the prefetched batch's
     // copies: it starts once that batch's host gather is done (host reads and
@@ -913,7 +916,7 @@ void Engine::enqueue_host_writeback(float lr) {
     PhaseScope ph(prof, kPhaseApplyHost, side2);
     k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
                                                                       ugrad.p, lr, rank, world, nxt_td, nx.usrc.p,
-                                                                      nx.urows.p);
+                                                                      nx.urows.p, sums, cnts);
     launched();
     EC_CUDA(cudaEventRecord(ev_side2, side2));
     EC_CUDA(cudaEventRecord(ev_patch, side2));
@@ -923,10 +926,11 @@ void Engine::enqueue_host_writeback(float lr) {
     PhaseScope ph(prof, kPhaseApplyHost, side2);
     if (host_tma())
       k_apply_host_tma<VEC><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                        urows.p, ugrad.p, lr, rank, world);
+                                                                        urows.p, ugrad.p, lr, rank, world, nullptr,
+                                                                        nullptr, nullptr, sums, cnts);
     else
       k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
-                                                                       urows.p, ugrad.p, lr, rank, world);
+                                                                       urows.p, ugrad.p, lr, rank, world, sums, cnts);
     launched();
   }
   EC_CUDA(cudaEventRecord(ev_side2, side2));
@@ -935,7 +939,8 @@ void Engine::enqueue_host_writeback(float lr) {
     EC_CUDA(cudaStreamWaitEvent(side, nx.ev_pf, 0));
     // (the prefetched ids are found in the pending set's hash)
     k_patch_prefetch<VEC, 4><<<sm_count(device), kThreads, 0, side>>>(nxt_td, T, ctr.p, missq.p, uniq.p, utab.p, urows.p,
-                                                                      ugrad.p, lr, rank, world, nx.usrc.p, nx.urows.p);
+                                                                      ugrad.p, lr, rank, world, nx.usrc.p, nx.urows.p,
+                                                                      sums, cnts);
     launched();
     EC_CUDA(cudaEventRecord(ev_patch, side));
   }
@@ -956,12 +961,14 @@ void Engine::join_host_writes(cudaStream_t st) {
 template <int VEC>
 void Engine::bwd_apply_local(float lr, cudaStream_t st) {
   const bool host = storage == EC_STORAGE_HOST;
-  if (fused() && host) {
-    // the misses' gradients first (heavy ones' fp64 sums into ugrad): the host
-    // write-back starts at ev_grad, right after, and overlaps k_apply_g64
-    PhaseScope ph(prof, kPhaseG64Misses, st);
-    k_g64_misses<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, missq.p,
-                                                             bb[cur].counted ? ucount.p : nullptr, ugrad.p, g64.p);
+  // fused host tier: with counts the write-back reads heavy misses' fp64 sums
+  // itself (miss_sgd), so it starts at ev_grad right after the scatter and
+  // overlaps k_apply_g64 (k_clear_miss_sums clears the sums before the set's
+  // next dedup); without counts every miss's sum is folded into ugrad first
+  if (fused() && host && !bb[cur].counted) {
+    PhaseScope ph(prof, kPhaseApply, st);
+    k_g64_misses<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, missq.p, nullptr, ugrad.p,
+                                                             g64.p);
     launched();
   }
   if (host) {
@@ -1318,8 +1325,21 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
                                                                          storage == EC_STORAGE_HOST ? 1 : 0);
 }
 
+// The per-unique counts (and the fp64 sums of the rows they made heavy) the
+// set's last batch left behind -- the fused host tier's misses, read by their
+// write-back, or a batch whose backward never ran -- cleared before the next
+// dedup that counts, from the last batch's counters (before their reset).
+// Launched whenever the cluster kernel counts, so captured graphs hold it.
+template <int VEC>
+void Engine::clear_sums(cudaStream_t st) {
+  PhaseScope ph(prof, kPhaseClearSums, st);
+  k_clear_miss_sums<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, ucount.p, g64.p);
+  launched();
+}
+
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   bb[cur].counted = !use_table_kernel() && use_cluster();
+  if (bb[cur].counted) EC_DISPATCH_VEC(clear_sums, st);
   if (use_table_kernel()) {
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));
@@ -1437,7 +1457,7 @@ NvtxRange::~NvtxRange() { nvtxRangePop(); }
 const char* phase_name(int phase) {
   static const char* const names[kNumPhases] = {"ec:insert",  "ec:compact", "ec:inverse_partition", "ec:gather",
                                                 "ec:gather_host", "ec:exchange", "ec:pool", "ec:scatter",
-                                                "ec:apply", "ec:apply_host", "ec:dedup_cluster", "ec:g64_misses"};
+                                                "ec:apply", "ec:apply_host", "ec:dedup_cluster", "ec:clear_miss_sums"};
   return phase >= 0 && phase < kNumPhases ? names[phase] : "ec:?";
 }
 

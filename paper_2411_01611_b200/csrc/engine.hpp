@@ -111,7 +111,7 @@ struct BatchBufs {
 
 // One timing slot per kernel of the batch pipeline (ec_tables_profile_read order).
 enum { kPhaseInsert = 0, kPhaseCompact, kPhaseInversePartition, kPhaseGather, kPhaseGatherHost, kPhaseExchange,
-       kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kPhaseDedupCluster, kPhaseG64Misses, kNumPhases };
+       kPhasePool, kPhaseScatter, kPhaseApply, kPhaseApplyHost, kPhaseDedupCluster, kPhaseClearSums, kNumPhases };
 
 // Optional per-phase CUDA-event timing on the launching streams.
 struct Profiler {
@@ -327,6 +327,7 @@ struct Engine {
   bool direct_apply = false;  // k_bwd_reduce applied the rows whose runs fit one chunk
   template <int VEC> void bwd_apply_local(float lr, cudaStream_t st);
   template <int VEC> void enqueue_host_writeback(float lr);
+  template <int VEC> void clear_sums(cudaStream_t st);
   void join_host_writes(cudaStream_t st);
   void enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st);
   void gather_for_export();

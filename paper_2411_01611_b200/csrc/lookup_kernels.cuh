@@ -842,11 +842,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_scatter(const TableDev* __restr
   }
 }
 
-// Fused single-rank SGD, pinned-host tier, first: the misses' gradients for
-// the host write-back.  A miss heavier than kLightAdds gets its fp64 sum
-// rounded once into ugrad; every miss's count and sums are left zeroed.  Walks
-// the miss queue (M entries, not U), so the host write-back that waits for it
-// starts early while k_apply_g64 updates the cached rows beside it.
+// Fused single-rank SGD, pinned-host tier: a miss's new row.  A miss heavier
+// than kLightAdds lookups (every miss without counts) has its whole gradient
+// in g64 -- w - lr * sum rounded once, read without clearing, so the host
+// write-back and the prefetch patch (two streams) compute the same row; a
+// light one sums in ugrad.  `g64` null: the gradient is in ugrad (other paths).
+template <int VEC>
+__device__ __forceinline__ float4 miss_sgd(float4 w, const float* __restrict__ ugrad, const double* __restrict__ g64,
+                                           const int* __restrict__ ucount, uint32_t g, int c, float lr) {
+  constexpr int D = VEC * 4;
+  if (g64 && (!ucount || __ldcg(ucount + g) > kLightAdds)) {
+    const double* p = g64 + static_cast<int64_t>(g) * D + c;
+    double gs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) gs[k] = __ldcg(p + k * VEC);
+    return sgd4(w, gs, lr);
+  }
+  const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4);
+  return make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+}
+
+// Fused single-rank SGD, pinned-host tier without per-unique counts (dedup by
+// the tile path: every row took the fp64 path): each miss's fp64 sum rounded
+// into ugrad for the host write-back, sums and counts left zeroed.  Walks the
+// miss queue.  (With counts the write-back reads the heavy misses' sums itself
+// -- miss_sgd -- and k_clear_miss_sums clears them before the set's next dedup.)
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_g64_misses(int T, const int* __restrict__ ctr,
                                                          const uint32_t* __restrict__ missq, int* __restrict__ ucount,
@@ -884,10 +904,38 @@ __global__ void __launch_bounds__(kThreads) k_g64_misses(int T, const int* __res
   }
 }
 
+// Before a buffer set's next dedup, on that dedup's stream (off the host
+// link's path): every per-unique count its last batch left (the fused host
+// tier's misses, read by their write-back; any batch whose backward never ran,
+// e.g. a dropped prefetch), and the fp64 sums of the rows those counts made
+// heavy.  Reads the last batch's counters, so it runs before their reset.
+template <int VEC>
+__global__ void __launch_bounds__(kThreads) k_clear_miss_sums(int T, const int* __restrict__ ctr,
+                                                              int* __restrict__ ucount, double* __restrict__ g64) {
+  constexpr int D = VEC * 4;
+  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
+  const RowMap<VEC> m;
+  const int n = counters(const_cast<int*>(ctr), T).ubase[T];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int g = warp * RPW + m.sub; g < n; g += nwarps * RPW) {
+    const int cnt = __ldcg(ucount + g);
+    __syncwarp(((1u << VEC) - 1) << (m.sub * VEC));  // the row's lanes read its count before lane 0 clears it
+    if (!cnt) continue;
+    if (m.c == 0) ucount[g] = 0;
+    if (cnt > kLightAdds) {
+      double* p = g64 + static_cast<int64_t>(g) * D + m.c;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) p[k * VEC] = 0.0;
+    }
+  }
+}
+
 // Fused single-rank SGD, second half: rows heavier than kLightAdds (their
 // partials went to g64) get w - lr * sum(g64) with one rounding (cache row,
-// or the HBM shard row of a miss).  Pinned-host misses are k_g64_misses' (and
-// skipped here).  Leaves g64 and ucount zeroed.
+// or the HBM shard row of a miss).  Pinned-host misses are the host
+// write-back's (miss_sgd; skipped here, their sums cleared by
+// k_clear_miss_sums).  Leaves the other rows' g64 and ucount zeroed.
 template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restrict__ td, int T, const int* __restrict__ ctr,
                                                         const uint32_t* __restrict__ uniq, const uint16_t* __restrict__ utab,
@@ -903,7 +951,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_g64(const TableDev* __restri
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int g0 = warp * RPW * R; g0 < U; g0 += nwarps * RPW * R) {
     int n[R];
-    bool own[R];  // not a pinned-host miss (those are k_g64_misses')
+    bool own[R];  // not a pinned-host miss (those are the host write-back's)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int g = g0 + r * RPW + m.sub;
@@ -988,7 +1036,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
                                                          const uint32_t* __restrict__ missq,
                                                          const uint32_t* __restrict__ uniq,
                                                          const uint16_t* __restrict__ utab, const float* __restrict__ urows,
-                                                         const float* __restrict__ ugrad, float lr, int rank, int world) {
+                                                         const float* __restrict__ ugrad, float lr, int rank, int world,
+                                                         const double* __restrict__ g64 = nullptr,
+                                                         const int* __restrict__ ucount = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -1004,8 +1054,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_host(const TableDev* __restr
       const uint32_t id = uniq[g];
       if (static_cast<int>(id % world) != rank) continue;
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
-      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
-      const float4 nw = make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      const float4 nw = miss_sgd<VEC>(w, ugrad, g64, ucount, g, m.c, lr);
       st4(td[utab[g]].store + static_cast<int64_t>(id / world) * D + m.c * 4, nw);
     }
   }
@@ -1024,7 +1073,9 @@ __global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __r
                                                              const float* __restrict__ urows,
                                                              const float* __restrict__ ugrad, float lr, int rank,
                                                              int world, const int32_t* __restrict__ nxt_usrc,
-                                                             float* __restrict__ nxt_urows) {
+                                                             float* __restrict__ nxt_urows,
+                                                             const double* __restrict__ g64 = nullptr,
+                                                             const int* __restrict__ ucount = nullptr) {
   constexpr int D = VEC * 4;
   constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
   const RowMap<VEC> m;
@@ -1048,9 +1099,7 @@ __global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __r
           const uint32_t g2 = static_cast<uint32_t>(v) & ~kRankTag;
           if (nxt_usrc[g2] < 0) {
             const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + m.c * 4);
-            const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + m.c * 4);
-            st4(nxt_urows + static_cast<int64_t>(g2) * D + m.c * 4,
-                make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w));
+            st4(nxt_urows + static_cast<int64_t>(g2) * D + m.c * 4, miss_sgd<VEC>(w, ugrad, g64, ucount, g, m.c, lr));
           }
           break;
         }
@@ -1936,7 +1985,9 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
                                                              const float* __restrict__ ugrad, float lr, int rank,
                                                              int world, const TableDev* __restrict__ nxt_td = nullptr,
                                                              const int32_t* __restrict__ nxt_usrc = nullptr,
-                                                             float* __restrict__ nxt_urows = nullptr) {
+                                                             float* __restrict__ nxt_urows = nullptr,
+                                                             const double* __restrict__ g64 = nullptr,
+                                                             const int* __restrict__ ucount = nullptr) {
   constexpr int D = VEC * 4;
   constexpr uint32_t kRowBytes = D * 4;
   constexpr int kTmaRows = kTmaBytes / (D * 4) < 256 ? kTmaBytes / (D * 4) : 256;
@@ -1975,8 +2026,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
       const uint32_t g = dst_g[r];
       if (g == 0xFFFFFFFFu) continue;
       const float4 w = ldg4(urows + static_cast<int64_t>(g) * D + c * 4);
-      const float4 gr = ldg4(ugrad + static_cast<int64_t>(g) * D + c * 4);
-      const float4 nw = make_float4(w.x - lr * gr.x, w.y - lr * gr.y, w.z - lr * gr.z, w.w - lr * gr.w);
+      const float4 nw = miss_sgd<VEC>(w, ugrad, g64, ucount, g, c, lr);
       *reinterpret_cast<float4*>(buf + r * D + c * 4) = nw;
       if (pat_g[r] != 0xFFFFFFFFu) st4(nxt_urows + static_cast<int64_t>(pat_g[r]) * D + c * 4, nw);
     }

@@ -86,7 +86,7 @@ class EmbeddingTables:
         return {"device_bytes": d.value, "host_bytes": h.value}
 
     PHASES = ("k_insert", "k_compact", "k_inverse_partition", "k_gather", "k_gather_host", "exchange", "k_pool",
-              "k_scatter", "k_apply", "k_apply_host", "k_dedup_cluster", "k_g64_misses")
+              "k_scatter", "k_apply", "k_apply_host", "k_dedup_cluster", "k_clear_miss_sums")
 
     def use_graphs(self, enable: bool = True):
         """CUDA-graph replay of forward/backward (needs a non-default stream)."""
