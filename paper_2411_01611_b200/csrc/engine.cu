@@ -169,7 +169,19 @@ __global__ void k_rw_rows(const TableDev* __restrict__ td, uint32_t t, const uin
   }
 }
 
+// One warp waiting `ns` of device time on the prefetch stream (see prefetch()).
+__global__ void k_spin_ns(unsigned ns) {
+  unsigned long long start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  for (;;) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start >= ns) break;
+  }
+}
+
 // ------------------------------------------------------------ host side
+
 // Largest table (rows) whose dedup set is direct-mapped (slot = id) even when
 // it exceeds the hash capacity; EC_DIRECT_ROWS overrides (read at creation).
 static uint64_t direct_rows_limit() {
@@ -1166,6 +1178,22 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // this prefetch (e.g. the copy that produced these indices) comes first
   EC_CUDA(cudaEventRecord(ev_pfcall, st));
   EC_CUDA(cudaStreamWaitEvent(pstream, ev_pfcall, 0));
+  // A prefetched dedup launched together with the forward's pool competes with
+  // it for SM slots (the cluster kernel needs 8 co-resident CTAs per table);
+  // started ~10 us later it runs beside the pool's tail and the scatter.
+  // Measured (interleaved A/B on three boxes): HBM tier 0.053 ->
+  // 0.049 ms, configs[3] uniform 0.066 -> 0.055, host tier / TB / cfg1 within
+  // noise; 20 us about the same, 30 us worse (HBM 0.060); waiting for the
+  // pool's end worse still (HBM 0.074: the dedup then sits on the next
+  // forward's path).  EC_PF_DELAY_NS overrides (0: off).
+  static const int delay_ns = [] {
+    const char* v = std::getenv("EC_PF_DELAY_NS");
+    return v && *v ? std::atoi(v) : 10000;
+  }();
+  if (delay_ns > 0 && have_fwd) {
+    k_spin_ns<<<1, 32, 0, pstream>>>(static_cast<unsigned>(delay_ns));
+    launched();
+  }
   // peer exchange: rows are read once the forward in flight passed its step
   // barrier (every update of the step before is in), and the ones this step
   // updates are patched after the next barrier (p2p_patch_prefetched)
@@ -1336,6 +1364,7 @@ void Engine::clear_sums(cudaStream_t st) {
   k_clear_miss_sums<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, ucount.p, g64.p);
   launched();
 }
+
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   bb[cur].counted = !use_table_kernel() && use_cluster();

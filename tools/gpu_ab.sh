@@ -1,6 +1,9 @@
+# interleaved A/B of environment variants on bench workloads (experiments)
+# usage: VARIANTS="X=0 EC_FOO=1,EC_BAR=2" WORKLOADS="kaggle kaggle_hbm" bash tools/gpu_ab.sh tag [rounds]
 mkdir -p gpurun_out
-for r in 1 2 3; do
-for lib in libembcomm_gpu_prev.so libembcomm_gpu.so; do
-for w in kaggle kaggle_hbm; do
-EC_LIB_NAME=$lib timeout 300 python bench.py --workload $w --no-cpu-baseline --schedule-batches 0 | sed "s/^/$lib $w /" >> gpurun_out/ab1.txt 2>/dev/null
+out=gpurun_out/${1:-ab}.txt
+for r in $(seq ${2:-2}); do
+for v in ${VARIANTS:-"X=0"}; do
+for w in ${WORKLOADS:-kaggle kaggle_hbm}; do
+env ${v//,/ } timeout 300 python bench.py --workload $w --no-cpu-baseline --schedule-batches 0 2>/dev/null | sed "s/^/$v $w /" >> $out
 done; done; done
