@@ -30,7 +30,7 @@ step_kernels = {k: v for k, v in agg.items() if not any(s in k for s in ("init_s
                                                                            "sample_stream", "FillFunctor", "Fill", "spin_kernel",
                                                                            "direct_copy", "arange", "k_classify",
                                                                            "k_stable_order", "k_scan_", "k_gather_batch",
-                                                                           "k_h2d_pull"))}
+                                                                           "k_h2d_pull", "k_spin_ns"))}
 tot = sum(sum(v) / len(v) for v in step_kernels.values()) or 1.0
 with open(prefix + "_launches.md", "w") as f:
     f.write(f"# ncu launch list summary ({launches})\n\n")
@@ -40,7 +40,8 @@ with open(prefix + "_launches.md", "w") as f:
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
         m = sum(v) / len(v)
         share = (f"{100 * m / tot:.1f}%" if k in step_kernels else
-                 "e2e input copy (not a step kernel)" if "k_h2d_pull" in k else "setup")
+                 "e2e input copy (not a step kernel)" if "k_h2d_pull" in k else
+                 "prefetch delay (a one-warp device wait, not work)" if "k_spin_ns" in k else "setup")
         f.write(f"| `{k}` | {len(v)} | {m:.0f} | {min(v):.0f} | {share} |\n")
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
