@@ -1743,7 +1743,7 @@ struct DirectApply {
 };
 
 template <int VEC>
-__global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
+__global__ void __launch_bounds__(kThreads, 4) k_bwd_reduce(const int* __restrict__ off, const int* __restrict__ ctr, int T,
                                                          const uint2* __restrict__ list,
                                                          const float* __restrict__ grad, float* __restrict__ ugrad,
                                                          double* __restrict__ g64, DirectApply ap = {}) {
@@ -1763,15 +1763,31 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
     // adds its part to ugrad (zeroed) -- or, for rows spread over more than
     // kLightAdds chunks, to the row's fp64 sum, which k_g64_finalize rounds
     // into ugrad (at most kLightAdds fp32 roundings per row either way)
+    // direct apply: the run's row operands are loaded when the run starts, so
+    // they arrive while its gradients are summed (at the run's end they were a
+    // dependent usrc -> row chain on every short run: 23% of stall samples).
+    // Held to 64 registers (4 CTAs/SM): TB 0.378 -> 0.369 ms, cfg1 0.189 ->
+    // 0.181; unbounded (79 registers, 3 CTAs/SM) it was slower than before.
+    int32_t p_sr = 0;
+    uint32_t p_id = 0;
+    uint16_t p_t = 0;
+    float4 p_w = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto prep = [&](uint32_t u) {
+      if (!ap.urows) return;
+      p_sr = ap.usrc[u];
+      p_id = ap.uniq[u];
+      p_t = ap.utab[u];
+      p_w = ldg4(ap.urows + static_cast<int64_t>(u) * D + m.c * 4);
+    };
+    prep(cu);
     auto flush = [&](bool spans) {
       const float4 a = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
                                    static_cast<float>(acc[2]), static_cast<float>(acc[3]));
       float* dst = ugrad + static_cast<int64_t>(cu) * D + m.c * 4;
       if (!spans && ap.urows) {
-        const int32_t sr = ap.usrc[cu];
-        float* row = sr >= 0 ? ap.cache + static_cast<int64_t>(sr) * D
-                             : ap.td[ap.utab[cu]].store + static_cast<int64_t>(ap.uniq[cu]) * D;
-        const float4 w = ldg4(ap.urows + static_cast<int64_t>(cu) * D + m.c * 4);
+        float* row = p_sr >= 0 ? ap.cache + static_cast<int64_t>(p_sr) * D
+                               : ap.td[p_t].store + static_cast<int64_t>(p_id) * D;
+        const float4 w = p_w;
         st4(row + m.c * 4, make_float4(w.x - ap.lr * a.x, w.y - ap.lr * a.y, w.z - ap.lr * a.z, w.w - ap.lr * a.w));
       } else if (!spans) st4(dst, a);
       else if (chunk_span(off[cu], off[cu + 1]) > kLightAdds) red_g64<VEC>(g64, cu, m.c, acc[0], acc[1], acc[2], acc[3]);
@@ -1799,6 +1815,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_reduce(const int* __restrict__
           flush(first_run && off[cu] < c0);
           first_run = false;
           cu = u4[k];
+          prep(cu);
           acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
         }
         acc[0] += v4[k].x;
