@@ -652,7 +652,7 @@ def run_ours(args, wl):
                    if world > 1 else "single GPU"},
         "e2e": {"value": round(lookups_per_step * world / (e2e_ms * 1e-3), 1), "unit": "lookups/s",
                 "ms_per_step": round(e2e_ms, 5), "step_ms_dist": e2e_dist,
-                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 4) * 4),
+                "h2d_bytes_per_step": int(ids[0].numel() * 4), "d2h_bytes_per_step": int((2 * T + 7) * 4),
                 "h2d_path": ("ec_copy_async_pull, %d CTAs" % pull) if pull else "ec_copy_async (copy engine)",
                 "h2d_probe": H2D_PROBE,
                 # host time per step outside the blocking result reads: when it
