@@ -1,7 +1,7 @@
 """Peer-memory exchange on one GPU: W ranks of a row-sharded job in one process
 (ec_group_set_p2p), each with its own batch, stepped through the same kernels a
 one-process-per-GPU job runs over NVLink (remote-row loads in the gather,
-owner updates by atomics or inboxes, rank-ordered hot lists, device barriers).
+owner updates by atomics or inboxes, owner-partitioned hot-row sync, device barriers).
 On one GPU the W ranks' kernels share the SMs and the "remote" traffic is
 local HBM, so this is a functional and overhead probe, not a scaling number.
 
@@ -56,9 +56,12 @@ for p2p in (False, True):
     ev[1].record(st)
     torch.cuda.synchronize()
     ms_step = ev[0].elapsed_time(ev[1]) / steps
-    wire = sum(m.stats()["wire_rows"] for m in ms)
+    sts = [m.stats() for m in ms]
+    wire = sum(x["wire_rows"] for x in sts)
+    hot = max(x.get("hot_sync_bytes", 0) for x in sts)
     print(f"{wl['name']}: world {W} on one GPU, {'p2p' if p2p else 'staged copies'}: "
-          f"{ms_step:.3f} ms per group step ({ms_step / W:.3f} ms per rank-step), remote rows {wire}")
+          f"{ms_step:.3f} ms per group step ({ms_step / W:.3f} ms per rank-step), remote rows {wire}, "
+          f"max hot-sync bytes per rank {hot}")
     g.close()
     for m in ms:
         m.close()
