@@ -187,6 +187,22 @@ int main(int argc, char** argv) {
   std::printf("table %zu rows (%.2f GB), M = %d rows of 64 B\n", rows, bytes / 1e9, M);
   time_gpu("gpu_gather", [&] { k_rand_read<<<20, 256, 0, s>>>(tab_d, idx_d, M, rows_d); });
   time_gpu("gpu_scatter", [&] { k_rand_write<<<20, 256, 0, s>>>(tab_d, idx_d, M, rows_d); });
+  {  // the same rows in ascending address order (IOMMU / page locality)
+    std::vector<uint32_t> sidx(idx);
+    std::sort(sidx.begin(), sidx.end());
+    uint32_t* sidx_d;
+    CK(cudaMalloc(&sidx_d, M * 4));
+    CK(cudaMemcpy(sidx_d, sidx.data(), M * 4, cudaMemcpyHostToDevice));
+    time_gpu("gpu_gather_sorted", [&] { k_rand_read<<<20, 256, 0, s>>>(tab_d, sidx_d, M, rows_d); });
+    time_gpu("gpu_scatter_sorted", [&] { k_rand_write<<<20, 256, 0, s>>>(tab_d, sidx_d, M, rows_d); });
+    for (int g : {40, 80}) {
+      char nm[40];
+      std::snprintf(nm, sizeof nm, "gpu_gather_sorted_g%d", g);
+      time_gpu(nm, [&] { k_rand_read<<<g, 256, 0, s>>>(tab_d, sidx_d, M, rows_d); });
+      std::snprintf(nm, sizeof nm, "gpu_gather_g%d", g);
+      time_gpu(nm, [&] { k_rand_read<<<g, 256, 0, s>>>(tab_d, idx_d, M, rows_d); });
+    }
+  }
   time_cpu("cpu_gather", true);
   time_cpu("cpu_scatter", false);
   const int n16 = M * 4;
