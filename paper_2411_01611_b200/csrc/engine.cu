@@ -206,8 +206,14 @@ int Engine::host_grid() const {
   // 0.103-0.110/0.107-0.113 ms; 8 CTAs starve the link (0.109), TMA at 296
   // CTAs 0.105-0.107 with the pool slowed 14 -> 30 us.  Re-measured with the
   // final row grid and pool (gather and write-back together, interleaved):
-  // 16/20/24 CTAs 0.1015-0.1034 / 0.0995-0.1001 / 0.1036-0.1047 ms.
-  return host_tma() ? sm_count(device) * 2 : 20;
+  // 16/20/24 CTAs 0.1015-0.1034 / 0.0995-0.1001 / 0.1036-0.1047 ms.  Round 2
+  // (write-back right after the scatter, prefetched dedup 10 us late), three
+  // interleaved sweeps, medians: 8/10/12/16/20 CTAs 0.1049/0.1019-0.1022/
+  // 0.1054/0.1032/0.1115 ms; split read/write grids and TMA at 32/64/148 CTAs
+  // no better than 10 (0.1026/0.1008-0.1018/0.1065).  Fewer CTAs in flight
+  // slow the gather itself (50 -> 54 us) but leave the pool and scatter beside
+  // it more room, and the write-back runs faster (40 -> 33 us).
+  return host_tma() ? sm_count(device) * 2 : 10;
 }
 // Host-link row traffic goes through SM loads/stores (k_gather_host /
 // k_apply_host) unless EC_HOST_TMA=1 selects the TMA bulk-copy kernels; with
