@@ -240,10 +240,13 @@ int Engine::row_grid() const {
   }();
   // measured per regime: fused HBM tier 5 (Kaggle 0.0618 -> 0.0596 ms; the
   // fifth CTA per SM waits for registers and fills SMs the concurrent dedup
-  // frees); pinned-host tier 4 (Kaggle 0.1042-0.1046 at 3, 0.1017-0.1020 at
-  // 4, interleaved); tile/transpose HBM path 4 (TB 0.398 vs 0.409, cfg1
-  // 0.195 vs 0.201 at 5)
-  return sm_count(device) * (env > 0 ? env : storage == EC_STORAGE_HBM && fused() ? 5 : 4);
+  // frees); pinned-host tier 4 in round 1 (Kaggle 0.1042-0.1046 at 3,
+  // 0.1017-0.1020 at 4, interleaved), 3 with round 2's pipeline (10 host
+  // CTAs, write-back right after the scatter: medians 0.0964-0.0967 at 3 vs
+  // 0.1037-0.1038 at 4 in two interleaved sweeps); tile/transpose HBM path 4
+  // (TB 0.398 vs 0.409, cfg1 0.195 vs 0.201 at 5)
+  const int per = storage == EC_STORAGE_HBM ? (fused() ? 5 : 4) : (fused() ? 3 : 4);
+  return sm_count(device) * (env > 0 ? env : per);
 }
 
 static uint32_t log2_ceil(uint64_t x) {
