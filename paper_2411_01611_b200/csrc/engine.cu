@@ -180,6 +180,11 @@ __global__ void k_spin_ns(unsigned ns) {
   }
 }
 
+#ifndef EC_HOST_R
+#define EC_HOST_R 4
+#endif
+constexpr int kHostR = EC_HOST_R;  // rows in flight per lane group in the host-link row kernels
+
 // ------------------------------------------------------------ host side
 
 // Largest table (rows) whose dedup set is direct-mapped (slot = id) even when
@@ -950,7 +955,7 @@ void Engine::enqueue_host_writeback(float lr) {
                                                                         urows.p, ugrad.p, lr, rank, world, nullptr,
                                                                         nullptr, nullptr, sums, cnts);
     else
-      k_apply_host<VEC, 4><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
+      k_apply_host<VEC, kHostR><<<host_write_grid(), kThreads, 0, side2>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p,
                                                                        urows.p, ugrad.p, lr, rank, world, sums, cnts);
     launched();
   }
@@ -1258,7 +1263,7 @@ void Engine::launch_gather_host(cudaStream_t s) {
     k_gather_host_tma<VEC><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
                                                              world);
   else  // (peer exchange: remote owners' rows from their shared host shards, over this GPU's link)
-    k_gather_host<VEC, 4><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
+    k_gather_host<VEC, kHostR><<<host_grid(), kThreads, 0, s>>>(tdev.p, T, ctr.p, missq.p, uniq.p, utab.p, urows.p, rank,
                                                             world, p2p_peers(), p2p_shard_off());
   launched();
 }
