@@ -497,7 +497,8 @@ def run_ours(args, wl):
     # own row traffic, and that varies across this pool's boxes (e2e 0.11 vs
     # 0.19 ms with the same probe numbers)
     trial = {}
-    cands = [pull, 0 if pull else 8] if world == 1 else [pull]  # (ranks must agree: N>1 keeps the probe's pick)
+    # (ranks must agree: N>1 keeps the probe's pick)
+    cands = list(dict.fromkeys([pull, 0, 4, 8, 16])) if world == 1 else [pull]
     for ctas in cands:
         copy_path["ctas"] = ctas
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
