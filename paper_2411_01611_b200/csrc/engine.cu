@@ -184,6 +184,14 @@ __global__ void k_spin_ns(unsigned ns) {
 #define EC_HOST_R 4
 #endif
 constexpr int kHostR = EC_HOST_R;  // rows in flight per lane group in the host-link row kernels
+#ifndef EC_FUSED_POOL_R
+#define EC_FUSED_POOL_R 4
+#endif
+#ifndef EC_FUSED_SCATTER_R
+#define EC_FUSED_SCATTER_R 4
+#endif
+constexpr int kFusedPoolR = EC_FUSED_POOL_R;        // bags in flight per thread, fused pooling-1 pool
+constexpr int kFusedScatterR = EC_FUSED_SCATTER_R;  // bag windows in flight per thread, fused SGD scatter
 
 // ------------------------------------------------------------ host side
 
@@ -823,7 +831,7 @@ void Engine::fwd_pool(cudaStream_t st) {
     // 4 bags in flight per thread (measured, Kaggle: HBM tier 0.0647 -> 0.0615
     // ms vs 8; host tier, with 4 row CTAs per SM, 0.1007-0.1014 -> 0.0984-0.0995)
     if (!bag_off && geom_p == 1)
-      k_pool1<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
+      k_pool1<VEC, kFusedPoolR, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
                                                           pb, ro);
     else
       k_pool<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
@@ -851,7 +859,7 @@ void Engine::bwd_scatter(const float* grad, cudaStream_t st) {
     // scatter) for a row's first kLightAdds partials, the rest summed in fp64
     // (g64) for k_apply_g64; pinned-host misses accumulate in ugrad
     const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
-    k_scatter<VEC, 4, true><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
+    k_scatter<VEC, kFusedScatterR, true><<<row_grid(), kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
                                                              bag_off, inv.p, grad, ugrad.p, g64.p,
                                                              bb[cur].counted ? ucount.p : nullptr, ctr.p, rs, bwd_lr);
     launched();
