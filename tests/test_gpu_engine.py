@@ -299,6 +299,19 @@ def test_config2_kaggle_shape_training_step(ec, torch, storage):
     run_training_step(ec, torch, KAGGLE, 16, 16384, 1, storage, 256 << 20, 909)
 
 
+@pytest.mark.parametrize("D", [4, 32, 128])
+@pytest.mark.parametrize("storage,mode,scatter", [("hbm", None, None), ("host", None, None),
+                                                  ("hbm", "tiles", "transpose"), ("host", "tiles", "atomic")])
+def test_every_row_width_training_step(ec, torch, D, storage, mode, scatter):
+    """The row kernels at the widths the other tests do not use (4, 32 and
+    128 floats per row: 1, 8 and 32 lanes per row): the fused path (cluster
+    dedup, SGD in the scatter), the tile path with the transpose backward
+    (SGD of single-chunk rows inside k_bwd_reduce on HBM rows) and the atomic
+    scatter with the pinned-host write-back; pooling 4, a small cache."""
+    run_training_step(ec, torch, [1000, 37, 50000, 3], D, 512, 4, storage, 100 * D * 4, 31 + D, mode=mode,
+                      scatter=scatter)
+
+
 @pytest.mark.parametrize("cache_bytes", [0, 64 * 16 * 4])
 def test_host_tier_heavy_misses_training_step(ec, torch, cache_bytes):
     """Pinned-host misses with thousands of lookups each (no cache, or a
