@@ -1365,6 +1365,8 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   static bool attr_set[64] = {};  // per device
   if (!attr_set[device & 63]) {
+    if (kClusterCtas > 8)  // (a build with 16-CTA clusters: non-portable size)
+      EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     attr_set[device & 63] = true;

@@ -38,6 +38,7 @@ template <int ITEMS>
 static void launch(const TableDev* td, int T, const uint32_t* idx, unsigned long long* tstat, int* ctr, uint32_t* uniq,
                    uint32_t* uslot, uint16_t* utab, uint32_t* inv, int32_t* usrc, uint32_t* missq, int* ucount, int tag) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
+  if (kClusterCtas > 8) CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem>>>(td, T, idx, tstat, ctr, uniq, uslot, utab, inv, usrc,
                                                                        missq, ucount, tag);
