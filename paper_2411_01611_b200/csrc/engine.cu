@@ -401,7 +401,9 @@ void Engine::create(const ec_tables_config& c) {
   // where the tile path will (TB shape 0.395 -> 0.379 ms, cfg1 0.200 -> 0.187:
   // a 2^17-slot set stays in L2, a 40M-row direct one costs a DRAM sector per
   // probe in each of k_insert, k_compact, k_inverse_partition)
-  plan_sets(max_n <= kAutoClusterN);
+  // (the auto choice of set_geometry: cluster kernel iff every table's batch
+  // fits 8 items per thread and the tables alone fill the GPU)
+  plan_sets(max_n <= kAutoClusterN && static_cast<int64_t>(T) * kClusterCtas >= sm_count(device));
   const uint64_t store_elems = store_off[T] * D;
   if (storage == EC_STORAGE_HBM) {
     store_dev.alloc(store_elems);
