@@ -1210,10 +1210,15 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
   // noise; 20 us about the same, 30 us worse (HBM 0.060); waiting for the
   // pool's end worse still (HBM 0.074: the dedup then sits on the next
   // forward's path).  EC_PF_DELAY_NS overrides (0: off).
-  static const int delay_ns = [] {
+  // Default 10 us for the pinned-host tier, 20 us with HBM rows (re-measured
+  // after k_clear_miss_sums, which runs just before the dedup, became 12 -> 8
+  // us: HBM tier 0.0529 at 10 vs 0.0490 at 20; configs[3] uniform 0.0622 vs
+  // 0.0540; host tier 0.0979 at 10 vs 0.0995 at 20).
+  static const int env_delay = [] {
     const char* v = std::getenv("EC_PF_DELAY_NS");
-    return v && *v ? std::atoi(v) : 10000;
+    return v && *v ? std::atoi(v) : -1;
   }();
+  const int delay_ns = env_delay >= 0 ? env_delay : storage == EC_STORAGE_HBM ? 20000 : 10000;
   if (delay_ns > 0 && have_fwd) {
     k_spin_ns<<<1, 32, 0, pstream>>>(static_cast<unsigned>(delay_ns));
     launched();
@@ -1387,7 +1392,7 @@ void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
 template <int VEC>
 void Engine::clear_sums(cudaStream_t st) {
   PhaseScope ph(prof, kPhaseClearSums, st);
-  k_clear_miss_sums<VEC><<<sm_count(device), kThreads, 0, st>>>(static_cast<int>(T), ctr.p, ucount.p, g64.p);
+  k_clear_miss_sums<VEC><<<sm_count(device) * 4, kThreads, 0, st>>>(static_cast<int>(T), ctr.p, ucount.p, g64.p);
   launched();
 }
 

@@ -913,20 +913,18 @@ template <int VEC>
 __global__ void __launch_bounds__(kThreads) k_clear_miss_sums(int T, const int* __restrict__ ctr,
                                                               int* __restrict__ ucount, double* __restrict__ g64) {
   constexpr int D = VEC * 4;
-  constexpr int RPW = RowMap<VEC>::kRowsPerWarp;
-  const RowMap<VEC> m;
   const int n = counters(const_cast<int*>(ctr), T).ubase[T];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int g = warp * RPW + m.sub; g < n; g += nwarps * RPW) {
+  // one count per thread (coalesced, all in flight); a heavy row's D sums by
+  // its own thread (rare).  (One row per lane group, as the row kernels do,
+  // left 16 lanes per count at D = 64: 117 us for the TB shape's 266K uniques.)
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
     const int cnt = __ldcg(ucount + g);
-    __syncwarp(((1u << VEC) - 1) << (m.sub * VEC));  // the row's lanes read its count before lane 0 clears it
     if (!cnt) continue;
-    if (m.c == 0) ucount[g] = 0;
+    ucount[g] = 0;
     if (cnt > kLightAdds) {
-      double* p = g64 + static_cast<int64_t>(g) * D + m.c;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) p[k * VEC] = 0.0;
+      double2* p = reinterpret_cast<double2*>(g64 + static_cast<int64_t>(g) * D);
+#pragma unroll 4
+      for (int k = 0; k < D / 2; ++k) p[k] = make_double2(0.0, 0.0);
     }
   }
 }
