@@ -1,15 +1,25 @@
 // Lookup engine: row-sharded fp32 tables, replicated HBM hot-row cache, and
 // the per-batch forward/backward pipeline (K1..K6).
 //
-//   forward  K1 dedup      k_insert -> k_compact (single-pass look-back scan + emit)
-//            K2 partition  k_inverse_partition (inverse | hit/miss per unique, miss queue)
-//            K3 gather     k_gather (HBM: cache hits and local-HBM misses; resets the
-//                          hash slot, zeroes the gradient row)
-//                          k_gather_host (pinned host misses, side stream)
-//            K4 exchange   exchange.cu (world > 1)
-//            K5 pool       k_pool (EmbeddingBag sum through inverse indices)
-//   backward K6            k_scatter (bag grads -> unique rows, smem aggregation)
-//                          -> k_apply (SGD; k_apply_host for pinned-host rows)
+// Fused single-rank path (<= 32768 lookups per table, e.g. the Kaggle configs):
+//   forward  K1+K2 k_dedup_cluster (one thread-block cluster per table: dedup,
+//                  inverse, hit/miss, miss queue), prefetched a step or two ahead
+//                  on its own stream (after k_clear_miss_sums and a short wait)
+//            K3h   k_gather_host (pinned-host misses, side stream)
+//            K5    k_pool1 / k_pool reading each unique row where it lives;
+//                  trailing blocks reset the batch's set slots
+//   backward K6    k_scatter<SGD> (-lr * g straight into cache / HBM rows; rows
+//                  with > 64 lookups summed in fp64) -> k_apply_g64 (one rounding
+//                  for those); pinned host: k_apply_host + k_patch_prefetch
+// Tile path (larger batches, TB / cfg1) and multi-rank:
+//   forward  K1    k_insert -> k_compact (single-pass look-back scan + emit)
+//            K2    k_inverse_partition (inverse | hit/miss per unique, miss queue)
+//            K3    k_gather (cache hits and HBM misses into compact rows)
+//            K4    exchange.cu (world > 1)
+//            K5    k_pool1 / k_pool from the compact rows
+//   backward K6    k_scatter or the transpose (k_bwd_count/fill/reduce; single
+//                  rank with HBM rows: SGD of one-chunk rows inside k_bwd_reduce)
+//                  -> k_apply (SGD; k_apply_host for pinned-host rows)
 // Kernels live in lookup_kernels.cuh.
 //
 // Reference anchors: the dedup reproduces count_batch_unique's distinct and
@@ -27,8 +37,9 @@
 //            pinned host (mapped, read by the GPU over PCIe/C2C)
 //   cache  : K_total rows x D fp32 (replicated top-k rows of every table)
 //   remap  : per table, int32[E_t]: global cache row or -1
-//   hash   : per table, uint64[cap_t] open-addressing set, (id << 32 | value);
-//            cap_t = pow2 >= 2*min(max lookups, E_t); self-cleaning per batch
+//   hash   : per table and buffer set, (id << 32 | value): an open-addressing
+//            set of pow2 >= 2*min(max lookups, E_t) slots, or direct-mapped
+//            (slot = id) where the cluster kernel runs; self-cleaning per batch
 //   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
 //            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
 #include <nvtx3/nvToolsExt.h>
