@@ -1229,10 +1229,11 @@ void Engine::prefetch(const ec_batch& b, cudaStream_t st) {
     const char* v = std::getenv("EC_PF_DELAY_NS");
     return v && *v ? std::atoi(v) : -1;
   }();
-  // The tile path (TB, cfg1: a longer pool, a three-kernel dedup) wants more:
-  // TB 0.368 / 0.360 / 0.354 / 0.353 ms at 0 / 20 / 40 / 80 us, cfg1 0.178 /
-  // 0.180 / 0.173 / 0.183.
-  const int delay_ns = env_delay >= 0 ? env_delay : !fused() ? 40000 : storage == EC_STORAGE_HBM ? 20000 : 10000;
+  // The tile path (TB, cfg1) gains a little more at 40 us (TB 0.368 / 0.360 /
+  // 0.354 / 0.353 ms at 0 / 20 / 40 / 80 us, cfg1 0.178 / 0.180 / 0.173 /
+  // 0.183), but the later dedup chain then overlaps K3: k_gather falls from
+  // 0.56 to 0.36 of the HBM roofline (north star: >= 0.5), so it stays at 20.
+  const int delay_ns = env_delay >= 0 ? env_delay : storage == EC_STORAGE_HBM ? 20000 : 10000;
   if (delay_ns > 0 && have_fwd) {
     k_spin_ns<<<1, 32, 0, pstream>>>(static_cast<unsigned>(delay_ns));
     launched();
