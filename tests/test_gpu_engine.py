@@ -350,6 +350,50 @@ def test_host_tier_heavy_misses_consecutive_steps(ec, torch, mode):
     tab.close()
 
 
+@pytest.mark.parametrize("mode", ["cluster", "tiles", "auto"])
+def test_many_tables_cross_table_scan(ec, torch, ref, mode):
+    """100 tables: the cluster kernel's warp-parallel look-back walks more than
+    32 lower tables (several rounds), and k_compact's tile look-back spans 100
+    tables' tiles; sizes from 1 to 200K rows, some tables empty in the batch.
+    Sets, inverse, hit/miss and rows vs the oracle; then a training step."""
+    rng = np.random.default_rng(17)
+    rows = [int(x) for x in rng.choice([1, 3, 40, 900, 5000, 70000, 200000], size=100)]
+    n = [0 if t % 17 == 5 else int(rng.integers(1, 3000)) for t in range(100)]
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
+    caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, rng.integers(0, 50, size=100))]
+    D, B = 8, 1
+    offs = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+    bag = np.concatenate([[0], offs[1:]]).astype(np.int64)
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=max(n), max_batch_size=B)
+    tab.dedup_mode(mode)
+    tab.init_synthetic(6, 0.5)
+    tab.place_cache(caches)
+    ids, _ = make_ids(ec, torch, dists, n, 1234)
+    bag_t = torch.from_numpy(bag).cuda()
+    out = tab.forward(ids, offs, B, bag_offsets=bag_t)
+    check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, rows, D, 6, 0.5, bag_offs=bag, B=B, ref=ref)
+    tab.backward(torch.zeros(B, len(rows) * D, device="cuda"), 0.0)
+    tab.close()
+
+
+@pytest.mark.parametrize("mode", ["cluster", "tiles"])
+def test_single_table(ec, torch, ref, mode):
+    """One table (no lower tables to look back on; the last table is the
+    first): sets, inverse, hit/miss and rows vs the oracle, fused training step."""
+    rows, D, B, P = [50000], 16, 5000, 4
+    dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, rows[0], 1.05))]
+    caches = [dists[0].top_ids(100)]
+    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=B * P, max_batch_size=B)
+    tab.dedup_mode(mode)
+    tab.init_synthetic(8, 0.2)
+    tab.place_cache(caches)
+    ids, offs = make_ids(ec, torch, dists, [B * P], 55)
+    out = tab.forward(ids, offs, B, P)
+    check_batch(ec, tab, ids.cpu().numpy().view(np.uint32), offs, caches, rows, D, 8, 0.2, P=P, B=B, out=out, ref=ref)
+    tab.backward(torch.zeros(B, D, device="cuda"), 0.0)
+    tab.close()
+
+
 def test_dedup_mode_switch_relays_sets_out(ec, torch, ref):
     """Tables sized for the tile path get hashed sets for their large tables;
     forcing the cluster kernel re-lays them out direct-mapped, and going back
