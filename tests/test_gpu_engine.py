@@ -136,7 +136,8 @@ def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
     tab.close()
 
 
-def test_csr_bags_empty_bags_and_empty_table(ec, torch):
+@pytest.mark.parametrize("storage", ["hbm", "host"])
+def test_csr_bags_empty_bags_and_empty_table(ec, torch, storage):
     rows, D, B = [300, 50, 1000], 8, 40
     rng = np.random.default_rng(3)
     lens = [rng.integers(0, 9, B), np.zeros(B, np.int64), rng.integers(0, 4, B)]
@@ -145,7 +146,7 @@ def test_csr_bags_empty_bags_and_empty_table(ec, torch):
     offs = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
     ids_h = np.concatenate([rng.integers(0, r, k) for r, k in zip(rows, n)]).astype(np.uint32)
     bag = np.concatenate([[0], np.cumsum(np.concatenate(lens))]).astype(np.int64)
-    tab = ec.EmbeddingTables(rows, D, max_lookups_per_table=max(n), max_batch_size=B)
+    tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=max(n), max_batch_size=B)
     tab.init_synthetic(5, 1.0)
     w0 = [tab.read_rows(t, np.arange(rows[t])) for t in range(3)]
     caches = [np.arange(10), [], np.arange(0, 1000, 3)]
