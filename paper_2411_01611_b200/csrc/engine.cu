@@ -1414,7 +1414,12 @@ void Engine::clear_sums(cudaStream_t st) {
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   bb[cur].counted = !use_table_kernel() && use_cluster();
-  if (bb[cur].counted) EC_DISPATCH_VEC(clear_sums, st);
+  // also after a counting batch when this one does not count (a mode or
+  // geometry change): its heavy rows' fp64 sums would otherwise meet the next
+  // scatter that sums into g64.  (Graphs are re-captured on such changes, and a
+  // clear with nothing left is a no-op.)
+  if (bb[cur].counted || bb[cur].left_counts) EC_DISPATCH_VEC(clear_sums, st);
+  bb[cur].left_counts = bb[cur].counted;
   if (use_table_kernel()) {
     EC_CUDA(cudaMemsetAsync(ctr.p, 0, (counters_size(T) - 1) * sizeof(int), st));  // keeps err
     EC_CUDA(cudaMemsetAsync(tstat.p, 0, T * sizeof(unsigned long long), st));

@@ -102,6 +102,7 @@ struct BatchBufs {
   cudaEvent_t ev_pf = nullptr;        // its prefetch complete (dedup + host gather)
   bool lists = false;                 // its forward built the unique-grouped gradient lists
   bool counted = false;               // its dedup wrote ucount (cluster kernel)
+  bool left_counts = false;           // a batch in this set left per-unique counts / sums to clear
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
            utab.bytes() + urows.bytes() + ugrad.bytes() + g64.bytes() + ucount.bytes() + status.bytes() + tstat.bytes() + ctr.bytes() +

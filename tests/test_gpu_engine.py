@@ -321,7 +321,7 @@ def test_host_tier_heavy_misses_training_step(ec, torch, cache_bytes):
     run_training_step(ec, torch, [1000, 50, 200000, 3], 16, 16384, 1, "host", cache_bytes, 4711)
 
 
-@pytest.mark.parametrize("mode", ["auto", "tiles"])
+@pytest.mark.parametrize("mode", ["auto", "tiles", "auto->tiles", "tiles->auto"])
 def test_host_tier_heavy_misses_consecutive_steps(ec, torch, mode):
     """Four training steps on the same tables with heavy pinned-host misses:
     every step's updated rows within 1e-5 of the fp64 update from the rows it
@@ -331,10 +331,11 @@ def test_host_tier_heavy_misses_consecutive_steps(ec, torch, mode):
     rows, D, B, P, lr = [1000, 50, 3, 20000], 16, 16384, 1, 0.01
     dists = [ec.materialize(ec.DistributionSpec.parametric(ec.DistributionKind.zipf, r, 1.05)) for r in rows]
     tab = ec.EmbeddingTables(rows, D, storage="host", max_lookups_per_table=B * P, max_batch_size=B)
-    tab.dedup_mode(mode)
+    modes = mode.split("->")  # a switch half way: counts / sums one path left must not reach the other
     tab.init_synthetic(4, 0.05)
     bag = np.arange(B + 1, dtype=np.int64) * P
     for step in range(4):
+        tab.dedup_mode(modes[min(step // 2, len(modes) - 1)])
         ids, offs = make_ids(ec, torch, dists, [B * P] * len(rows), 300 + step)
         out = tab.forward(ids, offs, B, P)
         torch.cuda.synchronize()
