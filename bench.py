@@ -254,9 +254,12 @@ def phase_bytes(st, wl, T, fused=False):
     row = D * 4
     hbm_src = U if wl["storage"] == "hbm" else H      # rows k_gather reads from HBM
     host_rows = 0 if wl["storage"] == "hbm" else M
+    # fused pinned-host tier: the cluster dedup also writes each lookup's row
+    # source, which the pool reads instead of inverse -> usrc
+    rsrc = fused and wl["storage"] != "hbm"
     return {
         # ids in, inverse out; uniq, uslot, utab, remap->usrc; per-unique lookup counts
-        "k_dedup_cluster": n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4 + 4),
+        "k_dedup_cluster": n * 4 + n * 4 + U * (4 + 4 + 2 + 4 + 4 + 4) + (n * 4 if rsrc else 0),
         "k_insert": n * 4 + n * 4,                     # ids in, slot_of out
         "k_compact": n * 4 + U * (4 + 4 + 2),          # slot_of in; uniq, uslot, utab out
         "k_inverse_partition": n * 4 + n * 4 + U * (4 + 2 + 4 + 4),  # slot_of in, inverse out; uniq, utab, remap in, usrc out
@@ -266,7 +269,7 @@ def phase_bytes(st, wl, T, fused=False):
         # 8d) when the pool reads each unique row at its source; on the gathering
         # path the compact copy's U rows (SURVEY's A_pool also counts the n row
         # reads, which hit L2 and can exceed the HBM peak)
-        "k_pool": U * 4 + U * row + n * 4 + B * T * row if fused else U * row + n * 4 + B * T * row,
+        "k_pool": (0 if rsrc else U * 4) + U * row + n * 4 + B * T * row if fused else U * row + n * 4 + B * T * row,
         # bag gradients in once, inverse (or grouped list) + counts, each unique
         # row's update read and written once (its cache / HBM row, or urows in
         # and the row out); the per-lookup partial sums stay in registers / L2

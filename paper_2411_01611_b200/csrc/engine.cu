@@ -201,6 +201,14 @@ constexpr int kHostR = EC_HOST_R;  // rows in flight per lane group in the host-
 #ifndef EC_FUSED_SCATTER_R
 #define EC_FUSED_SCATTER_R 4
 #endif
+// EC_ROW_SOURCES=all: per-lookup row sources on the HBM tier too (A/B)
+static bool row_sources_all() {
+  static const bool v = [] {
+    const char* e = std::getenv("EC_ROW_SOURCES");
+    return e && !std::strcmp(e, "all");
+  }();
+  return v;
+}
 constexpr int kFusedPoolR = EC_FUSED_POOL_R;        // bags in flight per thread, fused pooling-1 pool
 constexpr int kFusedScatterR = EC_FUSED_SCATTER_R;  // bag windows in flight per thread, fused SGD scatter
 
@@ -837,18 +845,20 @@ void Engine::fwd_pool(cudaStream_t st) {
   PhaseScope ph(prof, kPhasePool, st);
   if (fused()) {
     // rows read at their source; trailing blocks empty this batch's dedup set
-    const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0};
+    const RowSrc rs{usrc.p, uniq.p, cache.p, urows.p, storage == EC_STORAGE_HBM ? 1 : 0,
+                    bb[cur].row_sources ? reinterpret_cast<const int32_t*>(slot_of.p) : nullptr};
     const ResetOut ro{ctr.p, utab.p, uslot.p, usrc.p, ugrad.p, cnt.p,
                       !bb[cur].counted ? kResetAll : storage == EC_STORAGE_HOST ? kResetMisses : kResetNone};
     const int pb = row_grid(), rb = sm_count(device);
     // 4 bags in flight per thread (measured, Kaggle: HBM tier 0.0647 -> 0.0615
     // ms vs 8; host tier, with 4 row CTAs per SM, 0.1007-0.1014 -> 0.0984-0.0995)
+    const bool rsrc = bb[cur].row_sources;
     if (!bag_off && geom_p == 1)
-      k_pool1<VEC, kFusedPoolR, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs,
-                                                          pb, ro);
+      (rsrc ? k_pool1<VEC, kFusedPoolR, true, true> : k_pool1<VEC, kFusedPoolR, true, false>)<<<pb + rb, kThreads, 0, st>>>(
+          tdev.p, T, static_cast<int>(geom_b), inv.p, urows.p, out_ptr, rs, pb, ro);
     else
-      k_pool<VEC, 4, true><<<pb + rb, kThreads, 0, st>>>(tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p),
-                                                         bag_off, inv.p, urows.p, out_ptr, rs, pb, ro);
+      (rsrc ? k_pool<VEC, 4, true, true> : k_pool<VEC, 4, true, false>)<<<pb + rb, kThreads, 0, st>>>(
+          tdev.p, T, static_cast<int>(geom_b), static_cast<int>(geom_p), bag_off, inv.p, urows.p, out_ptr, rs, pb, ro);
     launched();
     return;
   }
@@ -1382,21 +1392,27 @@ void Engine::enqueue_forward(const uint32_t* indices, cudaStream_t st) {
   pool(st);
 }
 
-template <int ITEMS>
-void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
+template <int ITEMS, bool RSRC>
+void Engine::launch_dedup_cluster_k(const uint32_t* indices, cudaStream_t st) {
   constexpr size_t smem = cluster_smem_bytes(ITEMS);
   static bool attr_set[64] = {};  // per device
   if (!attr_set[device & 63]) {
     if (kClusterCtas > 8)  // (a build with 16-CTA clusters: non-portable size)
-      EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS, RSRC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    EC_CUDA(cudaFuncSetAttribute(k_dedup_cluster<ITEMS, RSRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     attr_set[device & 63] = true;
   }
-  k_dedup_cluster<ITEMS><<<kClusterCtas * T, kClusterThreads, smem, st>>>(tdev.p, static_cast<int>(T), indices, tstat.p,
-                                                                         ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p,
-                                                                         missq.p, ucount.p,
-                                                                         storage == EC_STORAGE_HOST ? 1 : 0);
+  k_dedup_cluster<ITEMS, RSRC><<<kClusterCtas * T, kClusterThreads, smem, st>>>(
+      tdev.p, static_cast<int>(T), indices, tstat.p, ctr.p, uniq.p, uslot.p, utab.p, inv.p, usrc.p, missq.p, ucount.p,
+      storage == EC_STORAGE_HOST ? 1 : 0, RSRC ? reinterpret_cast<int32_t*>(slot_of.p) : nullptr);
+}
+template <int ITEMS>
+void Engine::launch_dedup_cluster(const uint32_t* indices, cudaStream_t st) {
+  // (row sources only on the fused path: per-table batches < 32768, ITEMS <= 8)
+  if constexpr (ITEMS <= 8)
+    if (bb[cur].row_sources) return launch_dedup_cluster_k<ITEMS, true>(indices, st);
+  launch_dedup_cluster_k<ITEMS, false>(indices, st);
 }
 
 // The per-unique counts (and the fp64 sums of the rows they made heavy) the
@@ -1414,6 +1430,14 @@ void Engine::clear_sums(cudaStream_t st) {
 
 void Engine::enqueue_dedup_partition(const uint32_t* indices, cudaStream_t st) {
   bb[cur].counted = !use_table_kernel() && use_cluster();
+  // the fused pool's per-lookup row sources (slot_of is the tile path's
+  // buffer), pinned-host tier only.  Interleaved A/B (profiles/r02/
+  // row_sources_ab.txt): the host-tier step 0.096-0.099 -> 0.089-0.093 ms
+  // (the pool reads one word per lookup, no inverse -> usrc hop; the
+  // prefetched dedup has slack there), but with HBM rows the dedup's extra
+  // work lands on the step (Kaggle HBM 0.049 -> 0.050, uniform skew 0.054 ->
+  // 0.062 ms); EC_ROW_SOURCES=all turns them on there too
+  bb[cur].row_sources = bb[cur].counted && fused() && (storage == EC_STORAGE_HOST || row_sources_all());
   // also after a counting batch when this one does not count (a mode or
   // geometry change): its heavy rows' fp64 sums would otherwise meet the next
   // scatter that sums into g64.  (Graphs are re-captured on such changes, and a

@@ -102,6 +102,7 @@ struct BatchBufs {
   cudaEvent_t ev_pf = nullptr;        // its prefetch complete (dedup + host gather)
   bool lists = false;                 // its forward built the unique-grouped gradient lists
   bool counted = false;               // its dedup wrote ucount (cluster kernel)
+  bool row_sources = false;           // its dedup wrote per-lookup row sources into slot_of (cluster kernel, fused path)
   bool left_counts = false;           // a batch in this set left per-unique counts / sums to clear
   uint64_t bytes() const {
     return slot_of.bytes() + inv.bytes() + uniq.bytes() + uslot.bytes() + missq.bytes() + usrc.bytes() +
@@ -338,6 +339,8 @@ struct Engine {
   float bwd_lr = 0.f;  // learning rate of the backward being enqueued
   template <int ITEMS>
   void launch_dedup_cluster(const uint32_t* indices, cudaStream_t st);
+  template <int ITEMS, bool RSRC>
+  void launch_dedup_cluster_k(const uint32_t* indices, cudaStream_t st);
   void forward_prologue(const ec_batch& b, float* out, cudaStream_t st);
   void gather_local(cudaStream_t st);
   void pool(cudaStream_t st);

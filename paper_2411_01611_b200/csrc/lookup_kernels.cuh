@@ -491,12 +491,29 @@ struct RowSrc {
   const float* cache;
   const float* urows;
   int local_hbm;
+  const int32_t* isrc = nullptr;  // per lookup: row_source() words (cluster dedup; pools with RSRC)
 };
 __device__ __forceinline__ const float* src_row(const RowSrc& rs, const TableDev& tb, uint32_t u, int D) {
   const int32_t s = rs.usrc[u];
   if (s >= 0) return rs.cache + static_cast<int64_t>(s) * D;
   if (rs.local_hbm) return tb.store + static_cast<int64_t>(rs.uniq[u]) * D;
   return rs.urows + static_cast<int64_t>(u) * D;
+}
+
+// Per-lookup row source word written by the cluster dedup (k_dedup_cluster,
+// phase I): the cache row (>= 0), ~unique index for a miss (its row is the
+// local HBM shard's uniq[g], or the compact buffer's row g), kNoSource for an
+// invalid lookup (pools a zero row).  Unique indices < 2^31 - 1.
+constexpr int32_t kNoSource = INT32_MIN;
+__device__ __forceinline__ int32_t row_source(uint32_t g, int32_t cache_row) {
+  return g == kInvalidSlot ? kNoSource : cache_row >= 0 ? cache_row : ~static_cast<int32_t>(g);
+}
+__device__ __forceinline__ const float* src_of_word(const RowSrc& rs, const TableDev& tb, int32_t w, int D) {
+  if (w >= 0) return rs.cache + static_cast<int64_t>(w) * D;
+  if (w == kNoSource) return nullptr;
+  const uint32_t g = static_cast<uint32_t>(~w);
+  if (rs.local_hbm) return tb.store + static_cast<int64_t>(rs.uniq[g]) * D;
+  return rs.urows + static_cast<int64_t>(g) * D;
 }
 
 // Reset tail of a direct-source pool (what k_gather does on the gathering
@@ -539,7 +556,7 @@ __device__ __forceinline__ void reset_sets(const TableDev* td, int T, const Rese
 // Bags visited sample-major (q = s*T + t) so a warp writes a contiguous
 // stretch of the [B, T*D] output; R bags in flight per thread; each bag is
 // summed in lookup order.
-template <int VEC, int R, bool DIRECT = false>
+template <int VEC, int R, bool DIRECT = false, bool RSRC = false>
 __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict__ td, int T, int B, int P,
                                                    const int64_t* __restrict__ bag_off, const uint32_t* __restrict__ inv,
                                                    const float* __restrict__ urows, float* __restrict__ out,
@@ -576,14 +593,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
     for (int r = 0; r < R; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = 0; i < maxlen; ++i) {
       uint32_t u[R];
+      if constexpr (RSRC) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+        for (int r = 0; r < R; ++r) u[r] = i < len[r] ? static_cast<uint32_t>(rs.isrc[lo[r] + i]) : kNoSource;
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[r] = i < len[r] ? inv[lo[r] + i] : kInvalidSlot;
+      }
       if constexpr (DIRECT) {
         const float* src[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int q = q0 + r * RPW + m.sub;
-          src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, td[q - (q / T) * T], u[r], D);
+          const TableDev& tb = td[q - (q / T) * T];
+          if constexpr (RSRC) src[r] = src_of_word(rs, tb, static_cast<int32_t>(u[r]), D);
+          else src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, tb, u[r], D);
         }
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -604,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_pool(const TableDev* __restrict
 // Pooling 1 (the Criteo configs): every bag is one lookup, so the pool is an
 // indexed row copy; R bags in flight per thread, evict-first stores for the
 // [B, T*D] output (written once, not re-read by this step).
-template <int VEC, int R, bool DIRECT = false>
+template <int VEC, int R, bool DIRECT = false, bool RSRC = false>
 __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__ td, int T, int B,
                                                     const uint32_t* __restrict__ inv, const float* __restrict__ urows,
                                                     float* __restrict__ out, RowSrc rs = {}, int pool_blocks = 0,
@@ -624,10 +648,11 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = q0 + r * RPW + m.sub;
-      u[r] = kInvalidSlot;
+      u[r] = RSRC ? static_cast<uint32_t>(kNoSource) : kInvalidSlot;
       if (q < nbags) {
         const int s = q / T, t = q - s * T;
-        u[r] = __ldcs(inv + static_cast<int64_t>(t) * B + s);  // pooling 1: table t's lookups start at t*B
+        // pooling 1: table t's lookups start at t*B
+        u[r] = __ldcs((RSRC ? reinterpret_cast<const uint32_t*>(rs.isrc) : inv) + static_cast<int64_t>(t) * B + s);
       }
     }
     float4 v[R];
@@ -636,7 +661,9 @@ __global__ void __launch_bounds__(kThreads) k_pool1(const TableDev* __restrict__
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int q = q0 + r * RPW + m.sub;
-        src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, td[q - (q / T) * T], u[r], D);
+        const TableDev& tb = td[q - (q / T) * T];
+        if constexpr (RSRC) src[r] = src_of_word(rs, tb, static_cast<int32_t>(u[r]), D);
+        else src[r] = u[r] == kInvalidSlot ? nullptr : src_row(rs, tb, u[r], D);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = src[r] ? ldg4(src[r] + m.c * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1149,7 +1176,8 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
 //      hit/miss partition (usrc, miss queue, per-table miss counts); empty
 //      their L2 slots, or with `tag` tag the misses' (read by k_patch_prefetch)
 //   I  inverse: representatives hold their index, hot duplicates read it from
-//      shared memory
+//      shared memory; with RSRC, each lookup's row source into `isrc` (the fused
+//      pool then reads one word per lookup and the row: no inverse -> usrc hop)
 // ===================================================================
 #ifdef EC_TRACE  // phase timestamps for tools/dedup_bench.cu only
 __device__ unsigned long long* g_trace;
@@ -1185,13 +1213,14 @@ constexpr unsigned long long kTabInc = 1ull << 40;
 __host__ __device__ constexpr size_t cluster_smem_bytes(int) { return kClusterLocal * sizeof(uint32_t); }
 
 
-template <int ITEMS>
+template <int ITEMS, bool RSRC = false>
 __global__ void __cluster_dims__(kClusterCtas, 1, 1)
 __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1) : (ITEMS <= 8 ? 3 : 2))
     k_dedup_cluster(const TableDev* __restrict__ td, int T, const uint32_t* __restrict__ indices,
                     unsigned long long* __restrict__ tstatus, int* __restrict__ ctr, uint32_t* __restrict__ uniq,
                     uint32_t* __restrict__ uslot, uint16_t* __restrict__ utab, uint32_t* __restrict__ inv,
-                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, int* __restrict__ ucount, int tag) {
+                    int32_t* __restrict__ usrc, uint32_t* __restrict__ missq, int* __restrict__ ucount, int tag,
+                    int32_t* __restrict__ isrc = nullptr) {
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
@@ -1239,8 +1268,11 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   __syncthreads();
   EC_TRACE_AT(2);
 
-  // ---- G: representatives insert into the direct-mapped L2 set
+  // ---- G: representatives insert into the direct-mapped L2 set.  With
+  // RSRC every lookup needs its remap entry (phase I): loaded here, in
+  // flight across both cluster barriers (duplicates share the first's sector)
   uint32_t rep = 0;
+  int32_t rm[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const bool r = id[j] < nloc ? sval[id[j]] == static_cast<uint32_t>(p0 + j) : id[j] != kEmptyKey;
@@ -1248,6 +1280,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
       rep |= 1u << j;
       atomicMin(tb.hash + id[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p0 + j));
     }
+    if constexpr (RSRC) rm[j] = id[j] != kEmptyKey ? __ldg(tb.remap + id[j]) : 0;
   }
   EC_TRACE_AT(3);
   cluster.sync();  // every insert of this table is done
@@ -1270,10 +1303,11 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   EC_TRACE_AT(4);
   cluster.sync();
 
-  // remap of the firsts, in flight during the look-back
-  int32_t rm[ITEMS];
+  // remap of the firsts, in flight during the look-back (RSRC: loaded in G)
+  if constexpr (!RSRC) {
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) rm[j] = ((first >> j) & 1) ? __ldg(tb.remap + id[j]) : 0;
+    for (int j = 0; j < ITEMS; ++j) rm[j] = ((first >> j) & 1) ? __ldg(tb.remap + id[j]) : 0;
+  }
 
   // ---- B: unique base of the table and of every CTA of it
   if (threadIdx.x < 32) {
@@ -1398,6 +1432,9 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
                        : ((rep >> j) & 1) ? pf[j]
                        : hot ? static_cast<uint32_t>(tbase) + (sval[id[j]] >> 16) : kInvalidSlot;
     if (j < my) inv[tb.base + p0 + j] = g;
+    if (RSRC && j < my) {
+      isrc[tb.base + p0 + j] = row_source(g, rm[j]);
+    }
     const unsigned peers = __match_any_sync(kFull, g);
     if (g != kInvalidSlot && __ffs(peers) - 1 == lane_id()) {
       if (hot) atomicAdd(sval + id[j], __popc(peers));

@@ -185,6 +185,34 @@ def test_out_of_range_id_is_a_validation_error(ec, torch):
     tab.close()
 
 
+@pytest.mark.parametrize("storage", ["hbm", "host"])
+@pytest.mark.parametrize("mode", ["cluster", "tiles"])
+def test_out_of_range_id_pools_a_zero_row(ec, torch, storage, mode):
+    """An out-of-range id is skipped (inverse kInvalidSlot, reported as a
+    ValidationError by stats) and pools a zero row; every other bag still
+    pools its row -- on the fused cluster path too, whose pinned-host tier
+    pools through per-lookup row-source words (kNoSource for the bad id)."""
+    import numpy as np
+    tab = ec.EmbeddingTables([10, 300], 4, storage=storage, max_lookups_per_table=4, max_batch_size=4)
+    tab.init_synthetic(1, 1.0)
+    tab.place_cache([[1, 2], [5]])
+    tab.dedup_mode(mode)
+    ids = torch.tensor([1, 2, 10, 3, 5, 299, 7, 300], dtype=torch.int32, device="cuda")
+    out = tab.forward(ids, [0, 4, 8], 4, 1).cpu().numpy()
+    with pytest.raises(ec.ValidationError):
+        tab.stats()
+    h = ids.cpu().numpy()
+    for t in range(2):
+        for s in range(4):
+            i = int(h[t * 4 + s])
+            got = out[s, t * 4:(t + 1) * 4]
+            if i >= [10, 300][t]:
+                assert (got == 0).all()
+            else:
+                np.testing.assert_array_equal(got, tab.read_rows(t, np.array([i], np.uint32))[0])
+    tab.close()
+
+
 @pytest.mark.parametrize("mode", ["auto", "cluster"])
 def test_config1_full_size_counts_and_sets(ec, torch, ref, mode):
     """Config 1 (BASELINE.json configs[0]): 8 tables x 1M rows, D=64, b=4096,
