@@ -3,11 +3,14 @@
 //
 // Fused single-rank path (<= 32768 lookups per table, e.g. the Kaggle configs):
 //   forward  K1+K2 k_dedup_cluster (one thread-block cluster per table: dedup,
-//                  inverse, hit/miss, miss queue), prefetched a step or two ahead
-//                  on its own stream (after k_clear_miss_sums and a short wait)
+//                  inverse, hit/miss, miss queue; pinned-host tier: also each
+//                  lookup's row source, in slot_of), prefetched a step or two
+//                  ahead on its own stream (after k_clear_miss_sums and a short
+//                  wait)
 //            K3h   k_gather_host (pinned-host misses, side stream)
-//            K5    k_pool1 / k_pool reading each unique row where it lives;
-//                  trailing blocks reset the batch's set slots
+//            K5    k_pool1 / k_pool reading each unique row where it lives
+//                  (pinned-host tier: through the row sources, else inverse ->
+//                  usrc); trailing blocks reset the batch's set slots
 //   backward K6    k_scatter<SGD> (-lr * g straight into cache / HBM rows; rows
 //                  with > 64 lookups summed in fp64) -> k_apply_g64 (one rounding
 //                  for those); pinned host: k_apply_host + k_patch_prefetch
@@ -40,7 +43,8 @@
 //   hash   : per table and buffer set, (id << 32 | value): an open-addressing
 //            set of pow2 >= 2*min(max lookups, E_t) slots, or direct-mapped
 //            (slot = id) where the cluster kernel runs; self-cleaning per batch
-//   per-batch: slot_of/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
+//   per-batch: slot_of (tile path: lookup -> set slot; fused pinned-host
+//            path: lookup -> row source)/inverse (uint32[N]), uniq/uslot/usrc (uint32[N]),
 //            utab (uint16[N]), urows (fp32[N x D]), ugrad (fp32[N x D])
 #include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
