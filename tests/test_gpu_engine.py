@@ -74,7 +74,11 @@ def check_batch(ec, tab, ids_host, offs, caches, rows, D, seed, scale, bag_offs=
                                                  ("hbm", True, "auto"), ("host", True, "auto"),
                                                  ("hbm", False, "tiles"), ("host", True, "tiles"),
                                                  ("hbm", False, "cluster"), ("host", True, "cluster"),
-                                                 ("hbm", False, "table"), ("host", True, "table")])
+                                                 ("hbm", False, "table"), ("host", True, "table"),
+                                                 # fused path (auto scatter) with the cluster dedup: the
+                                                 # pinned-host tier pools through per-lookup row sources
+                                                 ("hbm", True, "cluster-fused"), ("host", True, "cluster-fused"),
+                                                 ("host", False, "cluster-fused")])
 def test_small_fixed_pooling_fwd_bwd(ec, torch, ref, storage, graphs, mode):
     if graphs:  # CUDA-graph capture/replay needs a non-default stream
         with torch.cuda.stream(torch.cuda.Stream()):
@@ -89,8 +93,12 @@ def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
     caches = [d.top_ids(min(len(d), k)) for d, k in zip(dists, [50, 0, 500, 1])]
     tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=B * P, max_batch_size=B)
     tab.use_graphs(graphs)
-    tab.dedup_mode(mode)
-    tab.scatter_mode("atomic" if mode == "tiles" else "transpose")
+    if mode == "cluster-fused":
+        tab.dedup_mode("cluster")
+        tab.scatter_mode("auto")
+    else:
+        tab.dedup_mode(mode)
+        tab.scatter_mode("atomic" if mode == "tiles" else "transpose")
     seed, scale = 1234, 0.05
     tab.init_synthetic(seed, scale)
     tab.place_cache(caches)
@@ -137,7 +145,8 @@ def _small_fixed_pooling(ec, torch, ref, storage, graphs, mode):
 
 
 @pytest.mark.parametrize("storage", ["hbm", "host"])
-def test_csr_bags_empty_bags_and_empty_table(ec, torch, storage):
+@pytest.mark.parametrize("mode", ["auto", "cluster"])
+def test_csr_bags_empty_bags_and_empty_table(ec, torch, storage, mode):
     rows, D, B = [300, 50, 1000], 8, 40
     rng = np.random.default_rng(3)
     lens = [rng.integers(0, 9, B), np.zeros(B, np.int64), rng.integers(0, 4, B)]
@@ -147,6 +156,7 @@ def test_csr_bags_empty_bags_and_empty_table(ec, torch, storage):
     ids_h = np.concatenate([rng.integers(0, r, k) for r, k in zip(rows, n)]).astype(np.uint32)
     bag = np.concatenate([[0], np.cumsum(np.concatenate(lens))]).astype(np.int64)
     tab = ec.EmbeddingTables(rows, D, storage=storage, max_lookups_per_table=max(n), max_batch_size=B)
+    tab.dedup_mode(mode)  # cluster: the fused path (pinned-host tier: row sources through CSR bags)
     tab.init_synthetic(5, 1.0)
     w0 = [tab.read_rows(t, np.arange(rows[t])) for t in range(3)]
     caches = [np.arange(10), [], np.arange(0, 1000, 3)]
