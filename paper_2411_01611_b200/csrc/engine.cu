@@ -110,6 +110,11 @@ __global__ void k_init_shard(float* __restrict__ store, uint64_t local_rows, uin
   }
 }
 
+__global__ void k_copy_remap(unsigned long long* __restrict__ words, const int32_t* __restrict__ remap, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    words[2 * i + 1] = static_cast<uint32_t>(remap[i]);
+}
+
 __global__ void k_set_remap(int32_t* __restrict__ remap, const uint32_t* __restrict__ ids, uint64_t k, int64_t slot0) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += (uint64_t)gridDim.x * blockDim.x)
     remap[ids[j]] = static_cast<int32_t>(slot0 + j);
@@ -516,9 +521,11 @@ void Engine::plan_sets(bool direct_big) {
   for (uint32_t t = 0; t < T; ++t) {
     hash_lg[t] = std::max<uint32_t>(5, log2_ceil(2 * std::min<uint64_t>(max_n, rows[t])));
     const uint64_t lim = std::max<uint64_t>(1ull << hash_lg[t], direct_big ? direct_rows_limit() : 0);
-    hash_direct[t] = rows[t] <= lim && direct_bytes + rows[t] * 12 * kSets <= kDirectBudget ? 1 : 0;
-    if (hash_direct[t]) direct_bytes += rows[t] * 12 * kSets;  // hash + idcnt, every buffer set
-    hash_off[t + 1] = hash_off[t] + (hash_direct[t] ? rows[t] : (1ull << hash_lg[t]));
+    hash_direct[t] = rows[t] <= lim && direct_bytes + rows[t] * 24 * kSets <= kDirectBudget ? 1 : 0;
+    if (hash_direct[t]) direct_bytes += rows[t] * 24 * kSets;  // hash (+ remap copy) + idcnt, every buffer set
+    // (64-bit words: a direct set interleaves each id's set word with a copy
+    // of its remap entry, lookup_kernels.cuh:set_word)
+    hash_off[t + 1] = hash_off[t] + (hash_direct[t] ? 2 * rows[t] : (1ull << hash_lg[t]));
   }
 }
 
@@ -554,6 +561,7 @@ void Engine::require_direct_sets() {
   EC_CUDA(cudaDeviceSynchronize());
   plan_sets(true);
   alloc_sets();
+  sync_set_remap();
   set_views();
   upload_tdev();
   select(cur);
@@ -718,7 +726,20 @@ void Engine::place_cache(const uint32_t* const* ids, const uint64_t* k) {
         remap.p + remap_off[t], cache_ids.p + koff[t], kt, static_cast<int64_t>(koff[t]));
     EC_LAUNCH();
   }
+  sync_set_remap();
   EC_CUDA(cudaDeviceSynchronize());
+}
+
+// Direct-mapped dedup sets carry a copy of `remap` beside every id's set word
+// (odd words), in every buffer set: refreshed whenever remap or the sets change.
+void Engine::sync_set_remap() {
+  for (int k = 0; k < kSets; ++k)
+    for (uint32_t t = 0; t < T; ++t) {
+      if (!hash_direct[t] || !rows[t]) continue;
+      const int grid = static_cast<int>(std::min<uint64_t>((rows[t] + 255) / 256, persistent_grid(device) * 4ull));
+      k_copy_remap<<<grid, 256>>>(hash.p + k * hash_off[T] + hash_off[t], remap.p + remap_off[t], rows[t]);
+      EC_LAUNCH();
+    }
 }
 
 void Engine::rw_rows(uint32_t t, const uint32_t* ids, uint64_t n, float* buf_host, bool write) {

@@ -309,6 +309,7 @@ struct Engine {
   void upload_tdev();
   void plan_sets(bool direct_big);
   void alloc_sets();
+  void sync_set_remap();
   void set_views();
   void require_direct_sets();
   int host_write_grid() const;

@@ -57,6 +57,19 @@ __device__ __forceinline__ uint32_t hash_insert_from(unsigned long long* tab, ui
   }
 }
 
+// The 64-bit set word of `slot`.  A direct-mapped set interleaves (set word,
+// copy of the id's remap entry) per id, so the DRAM sector a unique's first
+// insert pulls into L2 also holds its cache row: one random sector per unique
+// instead of two (the cluster dedup reads the copy; Engine::sync_set_remap
+// keeps it equal to `remap`).  Hashed sets: one word per slot.
+__device__ __forceinline__ unsigned long long* set_word(const TableDev& t, uint32_t slot) {
+  return t.hash + (t.direct ? 2 * static_cast<uint64_t>(slot) : static_cast<uint64_t>(slot));
+}
+// id's cache row from a direct-mapped set's interleaved remap copy
+__device__ __forceinline__ int32_t set_remap(const TableDev& t, uint32_t id) {
+  return __ldg(reinterpret_cast<const int32_t*>(t.hash + 2 * static_cast<uint64_t>(id) + 1));
+}
+
 // Slot of `id` in a table's dedup set: the id itself when direct-mapped.
 __device__ __forceinline__ uint32_t table_slot(const TableDev& t, uint32_t id) {
   return t.direct ? id : hash_slot(id, t.shift);
@@ -67,7 +80,7 @@ __device__ __forceinline__ uint32_t table_slot(const TableDev& t, uint32_t id) {
 __device__ __forceinline__ uint32_t set_insert(const TableDev& t, uint32_t id, uint32_t lpos) {
   const unsigned long long mine = (static_cast<unsigned long long>(id) << 32) | lpos;
   if (t.direct) {
-    atomicMin(t.hash + id, mine);
+    atomicMin(set_word(t, id), mine);
     return id;
   }
   const uint32_t h = hash_slot(id, t.shift);
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j)  // home-slot probes of all items in flight together
-    cur[j] = (live[j] && __ffs(peers[j]) - 1 == lane_id()) ? __ldcg(t.hash + h[j]) : 0;
+    cur[j] = (live[j] && __ffs(peers[j]) - 1 == lane_id()) ? __ldcg(set_word(t, h[j])) : 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t off = j * kThreads + threadIdx.x;
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
     if (live[j] && leader == lane_id()) {
       if (t.direct) {
         if (static_cast<uint32_t>(cur[j]) > static_cast<uint32_t>(p - t.base))
-          atomicMin(t.hash + h[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p - t.base));
+          atomicMin(set_word(t, h[j]), (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p - t.base));
         slot = h[j];
       } else {
         slot = hash_insert_from(t.hash, t.mask, h[j], cur[j], id[j], static_cast<uint32_t>(p - t.base));
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(kThreads) k_insert(const Tile* __restrict__ ti
 // Lookup p is its id's first occurrence iff the slot's packed minimum is p.
 __device__ __forceinline__ bool is_first(const TableDev& t, const uint32_t* slot_of, int64_t p, uint32_t* h) {
   *h = slot_of[p];
-  return *h != kInvalidSlot && static_cast<uint32_t>(__ldcg(t.hash + *h)) == static_cast<uint32_t>(p - t.base);
+  return *h != kInvalidSlot && static_cast<uint32_t>(__ldcg(set_word(t, *h))) == static_cast<uint32_t>(p - t.base);
 }
 
 constexpr unsigned long long kStatAgg = 1ull << 32;  // status word: (flag << 32) | value
@@ -209,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
   for (int j = 0; j < kItems; ++j) {
     const uint32_t off = j * kThreads + threadIdx.x;
     first[j] = h[j] != kInvalidSlot &&
-               static_cast<uint32_t>(__ldcg(t.hash + h[j])) == static_cast<uint32_t>(tile.start + off - t.base);
+               static_cast<uint32_t>(__ldcg(set_word(t, h[j]))) == static_cast<uint32_t>(tile.start + off - t.base);
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {  // position order within the tile: j-major, then thread
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(const Tile* __restrict__ t
     utab[g] = static_cast<uint16_t>(tile.table);
     if (ucnt) ucnt[g] = static_cast<int>(t.idcnt[h[j]]);  // lookups of this unique (k_insert counted them)
     // only this thread writes this slot; concurrent flag tests never match a tagged value
-    t.hash[h[j]] = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
+    *set_word(t, h[j]) = (static_cast<unsigned long long>(id) << 32) | kRankTag | g;
   }
 }
 
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(kThreads) k_inverse_partition(const Tile* __re
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const uint32_t off = j * kThreads + threadIdx.x;
-      u[j] = hs[j] == kInvalidSlot ? kInvalidSlot : static_cast<uint32_t>(__ldcg(t.hash + hs[j])) & ~kRankTag;
+      u[j] = hs[j] == kInvalidSlot ? kInvalidSlot : static_cast<uint32_t>(__ldcg(set_word(t, hs[j]))) & ~kRankTag;
       if (off < tile.count) inv[tile.start + off] = u[j];
     }
     if (gf.list) {  // K6 grouping: lookup -> its unique's group (offsets from the scan of the counts)
@@ -396,7 +409,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(const TableDev* __restrict_
         }
         if (m.c == 0) {
           const TableDev& tb = td[tab];
-          tb.hash[uslot[g]] = kEmptySlot;  // leave the set empty for the next batch
+          *set_word(tb, uslot[g]) = kEmptySlot;  // leave the set empty for the next batch
           tb.idcnt[uslot[g]] = 0;
           cnt[g] = 0;  // backward occurrence count
         }
@@ -544,7 +557,7 @@ __device__ __forceinline__ void reset_sets(const TableDev* td, int T, const Rese
     if (c == 0) {
       if (ro.hash_reset == kResetAll || (ro.hash_reset == kResetMisses && miss)) {
         const TableDev& tb = td[ro.utab[g]];
-        tb.hash[ro.uslot[g]] = kEmptySlot;
+        *set_word(tb, ro.uslot[g]) = kEmptySlot;
         if (ro.hash_reset == kResetAll) tb.idcnt[ro.uslot[g]] = 0;
       }
       ro.cnt[g] = 0;
@@ -1118,7 +1131,7 @@ __global__ void __launch_bounds__(kThreads) k_patch_prefetch(const TableDev* __r
       const TableDev tb = td[utab[g]];
       uint32_t h = table_slot(tb, id);
       for (;;) {
-        const unsigned long long v = __ldcg(tb.hash + h);
+        const unsigned long long v = __ldcg(set_word(tb, h));
         if (v == kEmptySlot) break;
         if (static_cast<uint32_t>(v >> 32) == id) {
           const uint32_t g2 = static_cast<uint32_t>(v) & ~kRankTag;
@@ -1140,7 +1153,7 @@ __global__ void k_clear_hash(const TableDev* __restrict__ td, int T, const int* 
   const int U = counters(const_cast<int*>(ctr), T).ubase[T];
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < U; g += gridDim.x * blockDim.x) {
     const TableDev& tb = td[utab[g]];
-    tb.hash[uslot[g]] = kEmptySlot;
+    *set_word(tb, uslot[g]) = kEmptySlot;
     tb.idcnt[uslot[g]] = 0;
   }
 }
@@ -1278,9 +1291,9 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
     const bool r = id[j] < nloc ? sval[id[j]] == static_cast<uint32_t>(p0 + j) : id[j] != kEmptyKey;
     if (r) {
       rep |= 1u << j;
-      atomicMin(tb.hash + id[j], (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p0 + j));
+      atomicMin(set_word(tb, id[j]), (static_cast<unsigned long long>(id[j]) << 32) | static_cast<uint32_t>(p0 + j));
     }
-    if constexpr (RSRC) rm[j] = id[j] != kEmptyKey ? __ldg(tb.remap + id[j]) : 0;
+    if constexpr (RSRC) rm[j] = id[j] != kEmptyKey ? set_remap(tb, id[j]) : 0;
   }
   EC_TRACE_AT(3);
   cluster.sync();  // every insert of this table is done
@@ -1288,7 +1301,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   // ---- F: first positions; firsts; CTA scan
   uint32_t pf[ITEMS], first = 0;
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) pf[j] = ((rep >> j) & 1) ? static_cast<uint32_t>(__ldcg(tb.hash + id[j])) : 0u;
+  for (int j = 0; j < ITEMS; ++j) pf[j] = ((rep >> j) & 1) ? static_cast<uint32_t>(__ldcg(set_word(tb, id[j]))) : 0u;
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j)
     if (((rep >> j) & 1) && pf[j] == static_cast<uint32_t>(p0 + j)) first |= 1u << j;
@@ -1306,7 +1319,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   // remap of the firsts, in flight during the look-back (RSRC: loaded in G)
   if constexpr (!RSRC) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) rm[j] = ((first >> j) & 1) ? __ldg(tb.remap + id[j]) : 0;
+    for (int j = 0; j < ITEMS; ++j) rm[j] = ((first >> j) & 1) ? set_remap(tb, id[j]) : 0;
   }
 
   // ---- B: unique base of the table and of every CTA of it
@@ -1398,7 +1411,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
       // (pinned-host tier) each miss's unique index for k_patch_prefetch; every
       // other slot goes back to empty here (every read of it was before the
       // second cluster barrier), so the pool's reset tail touches misses only
-      tb.hash[id[j]] = tag && rm[j] < 0 ? (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g : kEmptySlot;
+      *set_word(tb, id[j]) = tag && rm[j] < 0 ? (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g : kEmptySlot;
     }
     // miss queue: one atomic per warp
     const int nm = __popc(missm);
@@ -1543,7 +1556,7 @@ __global__ void __launch_bounds__(kTableThreads, 1)
       if (key != kEmptyKey) {
         if (__ffs(peers) - 1 == lane_id()) atomicMin(sval + key, static_cast<uint32_t>(p0 + j));
       } else if (id != kEmptyKey) {
-        atomicMin(tb.hash + id, (static_cast<unsigned long long>(id) << 32) | static_cast<uint32_t>(p0 + j));
+        atomicMin(set_word(tb, id), (static_cast<unsigned long long>(id) << 32) | static_cast<uint32_t>(p0 + j));
       }
     }
   }
@@ -1557,7 +1570,7 @@ __global__ void __launch_bounds__(kTableThreads, 1)
     for (int k = 0; k < kTableRound; ++k) {
       const int j = r0 + k;
       const uint32_t id = j < my ? s_id[j * kTableThreads + tid] : kEmptyKey;
-      w[k] = id == kEmptyKey ? kEmptyKey : id < nloc ? sval[id] : static_cast<uint32_t>(__ldcg(tb.hash + id));
+      w[k] = id == kEmptyKey ? kEmptyKey : id < nloc ? sval[id] : static_cast<uint32_t>(__ldcg(set_word(tb, id)));
     }
 #pragma unroll
     for (int k = 0; k < kTableRound; ++k)
@@ -1613,7 +1626,7 @@ __global__ void __launch_bounds__(kTableThreads, 1)
         utab[g] = static_cast<uint16_t>(t);
         usrc[g] = rm[k];  // a miss iff the id is not cached (core/src/simulator.cpp:99)
         if (id[k] < nloc) sval[id[k]] = static_cast<uint32_t>(g);
-        tb.hash[id[k]] = (static_cast<unsigned long long>(id[k]) << 32) | kRankTag | static_cast<uint32_t>(g);
+        *set_word(tb, id[k]) = (static_cast<unsigned long long>(id[k]) << 32) | kRankTag | static_cast<uint32_t>(g);
         if (rm[k] < 0) missm |= 1u << k;
         id[k] = static_cast<uint32_t>(g++);  // now the unique index
       }
@@ -1648,7 +1661,7 @@ __global__ void __launch_bounds__(kTableThreads, 1)
       const uint32_t id = j < my ? s_id[j * kTableThreads + tid] : kEmptyKey;
       g[k] = id == kEmptyKey ? kInvalidSlot
              : id < nloc     ? sval[id]
-                             : static_cast<uint32_t>(__ldcg(tb.hash + id)) & ~kRankTag;
+                             : static_cast<uint32_t>(__ldcg(set_word(tb, id))) & ~kRankTag;
     }
 #pragma unroll
     for (int k = 0; k < kTableRound; ++k)
@@ -2060,7 +2073,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_host_tma(const TableDev* __r
         const TableDev tb = nxt_td[utab[g]];
         uint32_t h = table_slot(tb, id);
         for (;;) {
-          const unsigned long long v = __ldcg(tb.hash + h);
+          const unsigned long long v = __ldcg(set_word(tb, h));
           if (v == kEmptySlot) break;
           if (static_cast<uint32_t>(v >> 32) == id) {
             const uint32_t u2 = static_cast<uint32_t>(v) & ~kRankTag;

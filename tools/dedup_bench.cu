@@ -58,6 +58,7 @@ int main(int argc, char** argv) {
   std::vector<TableDev> td(T);
   std::vector<void*> allocs;
   std::vector<uint64_t> hslots;
+  std::vector<std::vector<unsigned long long>> hinit;  // each table's set as laid out before a launch
   uint64_t expect_u = 0;
   for (int t = 0; t < T; ++t) {
     const uint64_t E = rows[t];
@@ -84,8 +85,12 @@ int main(int argc, char** argv) {
     hslots.push_back(slots);
     unsigned long long* h;
     int32_t* rm;
-    CK(cudaMalloc(&h, slots * 8));
-    CK(cudaMemset(h, 0xFF, slots * 8));
+    // direct sets interleave (set word, remap copy) per id (lookup_kernels.cuh:set_word)
+    std::vector<unsigned long long> init(2 * slots, ~0ull);
+    for (uint64_t i = 0; i < E; ++i) init[2 * i + 1] = static_cast<uint32_t>(remap[i]);
+    hinit.push_back(init);
+    CK(cudaMalloc(&h, 2 * slots * 8));
+    CK(cudaMemcpy(h, init.data(), 2 * slots * 8, cudaMemcpyHostToDevice));
     CK(cudaMalloc(&rm, E * 4));
     CK(cudaMemcpy(rm, remap.data(), E * 4, cudaMemcpyHostToDevice));
     allocs.push_back(h);
@@ -126,9 +131,7 @@ int main(int argc, char** argv) {
   for (int it = 0; it < iters + 3; ++it) {
     CK(cudaMemset(ctr, 0, (counters_size(T) - 1) * 4));
     CK(cudaMemset(tstat, 0, T * 8));
-    for (int t = 0; t < T; ++t) {
-      CK(cudaMemset(td[t].hash, 0xFF, hslots[t] * 8));
-    }
+    for (int t = 0; t < T; ++t) CK(cudaMemcpy(td[t].hash, hinit[t].data(), hinit[t].size() * 8, cudaMemcpyHostToDevice));
     unsigned long long* tp = it == iters + 2 ? trace : nullptr;
     CK(cudaMemcpyToSymbol(g_trace, &tp, sizeof(tp)));
     CK(cudaDeviceSynchronize());
@@ -173,8 +176,13 @@ int main(int argc, char** argv) {
     // the L2 set after the kernel: the tagged misses (tag) or nothing
     long left = 0, bad_tag = 0;
     for (int t = 0; t < T; ++t) {
+      std::vector<unsigned long long> hw(2 * hslots[t]);
+      CK(cudaMemcpy(hw.data(), td[t].hash, hw.size() * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < hslots[t]; ++i) {
+        if (hw[2 * i + 1] != hinit[t][2 * i + 1]) ++bad_tag;  // remap copies untouched
+      }
       std::vector<unsigned long long> hs(hslots[t]);
-      CK(cudaMemcpy(hs.data(), td[t].hash, hslots[t] * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < hslots[t]; ++i) hs[i] = hw[2 * i];
       for (uint64_t i = 0; i < hslots[t]; ++i)
         if (hs[i] != ~0ull) {
           ++left;
