@@ -562,6 +562,7 @@ void Engine::require_direct_sets() {
   plan_sets(true);
   alloc_sets();
   sync_set_remap();
+  EC_CUDA(cudaDeviceSynchronize());  // (legacy-stream copies; the engine's streams do not wait for them)
   set_views();
   upload_tdev();
   select(cur);
