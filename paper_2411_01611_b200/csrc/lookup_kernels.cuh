@@ -1237,7 +1237,7 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
   static_assert(ITEMS <= 16, "per-thread first masks are 16 bits");
   extern __shared__ __align__(16) uint32_t sval[];  // hot id -> local min position, later its unique index
   __shared__ uint32_t sxm[kClusterThreads];          // per thread: (exclusive first count << 16) | first mask
-  __shared__ int s_total, s_base, s_pref[kClusterCtas];
+  __shared__ int s_total, s_base, s_qbase, s_pref[kClusterCtas];
   __shared__ int sw[kClusterThreads / 32];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
@@ -1413,26 +1413,21 @@ __launch_bounds__(kClusterThreads, kClusterThreads >= 512 ? (ITEMS <= 4 ? 2 : 1)
       // second cluster barrier), so the pool's reset tail touches misses only
       *set_word(tb, id[j]) = tag && rm[j] < 0 ? (static_cast<unsigned long long>(id[j]) << 32) | kRankTag | g : kEmptySlot;
     }
-    // miss queue: one atomic per warp
+    // miss queue: one atomic per CTA (the queue counter is shared by every
+    // CTA of every table; per-warp atomics queued ~3.3K same-address returns)
     const int nm = __popc(missm);
-    int incl = nm;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, incl, o);
-      if (lane_id() >= o) incl += y;
+    int mtot;
+    const int mex = block_exclusive_scan<kClusterThreads>(nm, sw, &mtot);
+    if (threadIdx.x == 0) {
+      s_qbase = mtot ? atomicAdd(c.miss_total, mtot) : 0;
+      if (mtot) atomicAdd(c.M + t, mtot);
     }
-    const int wtot = __shfl_sync(kFull, incl, 31);
-    int qbase = 0;
-    if (lane_id() == 31 && wtot) {
-      qbase = atomicAdd(c.miss_total, wtot);
-      atomicAdd(c.M + t, wtot);
-    }
-    qbase = __shfl_sync(kFull, qbase, 31) + incl - nm;
+    __syncthreads();
+    int qbase = s_qbase + mex;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j)
       if ((missm >> j) & 1) missq[qbase++] = pf[j];
   }
-  __syncthreads();
   EC_TRACE_AT(6);
 
   // ---- I: inverse, and each unique's lookup count (the backward's fp32 /
